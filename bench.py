@@ -1,0 +1,370 @@
+"""Benchmark: FWBF decoded information Gbit/s on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on):
+EG(1023,781) type-I cyclic EG-LDPC, all-zero codeword, BPSK/AWGN at Eb/N0 =
+4.0 dB (middle of the 3.0-5.0 sweep), float32 y, FWBF p = 31, alpha = 0.2,
+K_max = 100, 2^20 frames per GPU resident in HBM (4.29 GB > L2: no flush
+needed).  One step = one decode of the whole batch through the C ABI (plus
+the NCCL all-reduce of the error/iteration counters when N > 1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one process per GPU); frames shard with no data
+exchange (weak scaling: 2^20 frames per GPU).  `--impl reference` times the
+CPU decoder (the oracle port of the reference's numpy loop) on this host.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+K_INFO = {"eg5": 781, "eg4": 175, "eg6": 3367, "gal504": 252, "qc4x32": 14339}
+CODE_NAMES = {"eg5": "EG(1023,781)", "eg4": "EG(255,175)", "eg6": "EG(4095,3367)",
+              "gal504": "Gallager(3,6) N=504", "qc4x32": "QC(4,32) N=16384"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--code", default="eg5")
+    ap.add_argument("--frames", type=int, default=1 << 20)
+    ap.add_argument("--ebn0", type=float, default=4.0)
+    ap.add_argument("--p", type=int, default=31)
+    ap.add_argument("--kmax", type=int, default=100)
+    ap.add_argument("--alpha", type=float, default=0.2)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-frames", type=int, default=2048,
+                    help="bounded CPU sample (frames) for cpu_baseline / --impl reference")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunk", type=int, default=1 << 17)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ----------------------------------------------------------- CPU reference arm
+
+def _cpu_worker(args):
+    code, ebn0, p, kmax, alpha, seed, start, count = args
+    import numpy as np
+    from oracle import wbf_oracle as O
+    from tests.golden.codebook import build_code, code_rate
+    g = O.Graph.of(build_code(code))
+    sigma = O.ebn0_to_sigma(ebn0, code_rate(code))
+    rng = np.random.default_rng([seed, start])
+    y = (1.0 + sigma * rng.standard_normal((count, g.n))).astype(np.float32)
+    its = 0
+    for i in range(count):
+        its += O.decode(g, y[i], "fwbf", alpha=alpha, k_max=kmax, p=p).iterations
+    return count, its
+
+
+def cpu_decode_rate(a, frames: int, cores: int):
+    """Oracle port (the reference's numpy decode loop) over `frames` seeded frames."""
+    from multiprocessing import get_context
+    chunk = max(1, frames // (cores * 4))
+    jobs = [(a.code, a.ebn0, a.p, a.kmax, a.alpha, a.seed + 7, s, min(chunk, frames - s))
+            for s in range(0, frames, chunk)]
+    t0 = time.perf_counter()
+    if cores == 1:
+        res = [_cpu_worker(j) for j in jobs]
+    else:
+        with get_context("fork").Pool(cores) as pool:
+            res = pool.map(_cpu_worker, jobs)
+    dt = time.perf_counter() - t0
+    n = sum(r[0] for r in res)
+    its = sum(r[1] for r in res)
+    return n, dt, its / max(1, n)
+
+
+def run_reference(a, rank: int):
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    k = K_INFO[a.code]
+    frames = a.cpu_frames
+    for _ in range(a.warmup and 1):
+        cpu_decode_rate(a, max(cores, 64), cores)
+    times, its = [], []
+    for _ in range(a.steps):
+        n, dt, mi = cpu_decode_rate(a, frames, cores)
+        times.append(dt)
+        its.append(mi)
+    t = sum(times)
+    value = frames * a.steps * k / t / 1e9
+    line = {
+        "impl": "reference", "metric": "FWBF decoded info Gbit/s", "value": value, "unit": "Gbit/s",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": 1e3 * t / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(a, mean_iters=statistics.mean(its)),
+        "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": cores, "kind": "port",
+                         "sample": f"{frames} seeded frames per step of the bench workload, "
+                                   f"oracle/wbf_oracle.py (numpy restatement of the reference "
+                                   f"decode loop) on a {cores}-process pool"},
+        "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(a, **extra):
+    d = {"workload": f"{CODE_NAMES[a.code]} FWBF p={a.p} alpha={a.alpha} K_max={a.kmax} "
+                     f"Eb/N0={a.ebn0} dB, all-zero codeword, float32 y",
+         "code": CODE_NAMES[a.code], "frames_per_gpu": a.frames, "p": a.p, "k_max": a.kmax,
+         "alpha": a.alpha, "ebn0_db": a.ebn0, "stall": "flip-global-max",
+         "l2": "inputs larger than L2 (frames*4 KiB >> 126 MB); no flush",
+         "parallelism": f"frames sharded over {a.gpus} GPU(s), NCCL all-reduce of counters"}
+    d.update(extra)
+    return d
+
+
+# ------------------------------------------------------------------ our arm
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1206_3362_b200 import DecoderConfig, _native as nat
+    from paper_1206_3362_b200.decoders import device_code, make_params, BatchResult, _outputs
+    from tests.golden.codebook import build_code, code_rate
+    import ctypes as C
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    h = build_code(a.code)
+    n = h.n_cols
+    kinfo = K_INFO[a.code]
+    sigma = float(math.sqrt(1.0 / (2.0 * code_rate(a.code) * 10.0 ** (a.ebn0 / 10.0))))
+    ld = (n + 3) // 4 * 4
+    B = a.frames
+    # synthetic channel output resident in HBM (seeded per rank)
+    g = torch.Generator(device=dev).manual_seed(a.seed * 1000003 + rank)
+    y = torch.empty((B, ld), dtype=torch.float32, device=dev)
+    for s in range(0, B, 1 << 16):
+        e = min(B, s + (1 << 16))
+        y[s:e].normal_(generator=g).mul_(sigma).add_(1.0)
+    dc = device_code(h, local)
+    cfg = DecoderConfig(alpha=a.alpha, k_max=a.kmax, block_len_p=a.p)
+    prm = make_params(cfg, "fwbf")
+    L = nat.lib()
+    zw = (n + 31) // 32
+    res = BatchResult(n=n, z_bits=torch.zeros((B, zw), dtype=torch.int32, device=dev),
+                      iterations=torch.zeros(B, dtype=torch.int32, device=dev),
+                      flags=torch.zeros(B, dtype=torch.uint8, device=dev),
+                      flips_total=torch.zeros(B, dtype=torch.int32, device=dev),
+                      bit_errors=torch.zeros(B, dtype=torch.int32, device=dev),
+                      counters=torch.zeros(nat.NCOUNTERS, dtype=torch.int64, device=dev))
+    out = _outputs(res)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        res.counters.zero_()
+        nat.check(L.fwbf_decode_f32(dc.handle, C.byref(prm), C.c_void_p(y.data_ptr()), B, ld,
+                                    C.byref(out), C.c_void_p(stream.cuda_stream)), "decode")
+        if world > 1:
+            dist.all_reduce(res.counters)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(a.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    cnt = res.counters.cpu().numpy()   # last step, all ranks (all-reduced)
+    frames_all = int(cnt[nat.CNT_FRAMES])
+    mean_iters = cnt[nat.CNT_ITER_SUM] / frames_all
+    value = world * B * a.steps * kinfo / (ms_max / 1e3) / 1e9
+    ms_step = ms_max / a.steps
+
+    # ---- end-to-end through the host-buffer C ABI (pinned host y -> results in host memory)
+    e2e = None
+    if not a.no_e2e:
+        yh = torch.empty((B, ld), dtype=torch.float32, pin_memory=True)
+        yh.copy_(y)
+        zh = torch.empty((B, zw), dtype=torch.int32, pin_memory=True)
+        ih = torch.empty(B, dtype=torch.int32, pin_memory=True)
+        fh = torch.empty(B, dtype=torch.uint8, pin_memory=True)
+        ch = np.zeros(nat.NCOUNTERS, np.int64)
+
+        def e2e_step():
+            nat.check(L.fwbf_decode_host_f32(
+                dc.handle, C.byref(prm), C.c_void_p(yh.data_ptr()), B, ld,
+                C.c_void_p(zh.data_ptr()), zw, C.c_void_p(ih.data_ptr()), C.c_void_p(fh.data_ptr()),
+                ch.ctypes.data_as(C.c_void_p), a.e2e_chunk), "decode_host")
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            e2e_step()
+        te = time.perf_counter() - t0
+        tt = torch.tensor([te], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+        e2e = {"value": world * B * a.steps * kinfo / te / 1e9, "unit": "Gbit/s",
+               "h2d_bytes_per_step": B * ld * 4,
+               "d2h_bytes_per_step": B * (zw * 4 + 4 + 1) + nat.NCOUNTERS * 8,
+               "path": "fwbf_decode_host_f32 (pinned host y; chunked H2D/decode/D2H on 2 streams)",
+               "chunk_frames": a.e2e_chunk}
+
+    if rank == 0:
+        props = torch.cuda.get_device_properties(dev)
+        sms = props.multi_processor_count
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+        except OSError:
+            pass
+        hbm_peak = peaks.get("hbm_gbs", 6650.0)
+        csum = clk.summary()
+        max_mhz = csum.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
+        bytes_frame = 4 * n + 4 * zw + 8
+        launch_ms = ms_step  # one decode launch per step on this stream
+        achieved = B * bytes_frame / (launch_ms / 1e3) / 1e9
+        traffic = None
+        try:
+            tr = json.load(open(os.path.join(REPO, "profiles", "roofline_traffic.json")))
+            traffic = tr.get(a.code, {}).get("dram_bytes_per_launch")
+        except OSError:
+            pass
+        edges = h.n_edges
+        edge_visits = B * edges * (1.0 + mean_iters)
+        ev_rate = edge_visits / (launch_ms / 1e3)
+        dadd_peak = sms * 64 * max_mhz * 1e6
+        smem_peak = sms * 128 * max_mhz * 1e6
+        line = {
+            "metric": "FWBF decoded info Gbit/s", "value": value, "unit": "Gbit/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded AWGN, all-zero codeword)",
+            "config": config_dict(a, mean_iters=float(mean_iters),
+                                  fer=float(cnt[nat.CNT_WORD_ERRORS] / frames_all),
+                                  ber=float(cnt[nat.CNT_BIT_ERRORS] / (frames_all * n)),
+                                  ordered_path_frames=int(cnt[nat.CNT_ORDERED_FRAMES]),
+                                  frames_per_s=world * B / (ms_step / 1e3)),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "bytes_per_frame": bytes_frame,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
+                         "binding": {
+                             "resource": "shared-memory bandwidth / fp64 issue (metric gather)",
+                             "edge_visits_per_frame": edges * (1.0 + mean_iters),
+                             "edge_visits_per_s": ev_rate,
+                             "dadd_peak_per_s": dadd_peak,
+                             "frac_of_dadd_peak": ev_rate / dadd_peak,
+                             "smem_peak_GBps": smem_peak / 1e9,
+                             "frac_of_smem_peak_at_8B_per_edge": 8 * ev_rate / smem_peak,
+                             "clock_mhz_for_peaks": max_mhz}},
+            "e2e": e2e,
+            "gpu_launches": a.steps * 1,
+            "clocks": csum,
+        }
+        if not a.no_cpu_baseline and world == 1:
+            cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+            nf, dt, _ = cpu_decode_rate(a, a.cpu_frames, cores)
+            line["cpu_baseline"] = {
+                "value": nf * kinfo / dt / 1e9, "unit": "Gbit/s", "cores": cores, "kind": "port",
+                "sample": f"{nf} seeded frames of the same workload through oracle/wbf_oracle.py "
+                          f"(numpy restatement of the reference decode loop), {cores}-process pool"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+/*
+ * fwbf_b200.h -- C ABI of the B200 batched weighted-bit-flipping LDPC decoder.
+ *
+ * Drop-in boundary for the reference's decode path (/root/reference/pkg/src/fwbf):
+ *
+ *   fwbf_code_create    replaces ParityCheckMatrix as the decoder's view of H
+ *                       (matrix.py:22-58); the handle owns device copies.
+ *   fwbf_decode_f32/64  replaces the per-frame loop decode_{fwbf,imwbf,mlp_wbf}
+ *                       (decoders.py:189-259), batched over B frames; y is the
+ *                       channel output the reference casts to float64 (:191).
+ *   fwbf_decode_awgn    replaces harness._run_batch (harness.py:98-115): noise is
+ *                       generated on the device from (seed, global frame index).
+ *   fwbf_decode_host_f32  the same batch call on HOST buffers (pipelined copies).
+ *   fwbf_last_error     text of the last failure (the reference raises ValueError).
+ *
+ * Conventions: plain C types only; every buffer argument of fwbf_decode_* is
+ * caller-owned DEVICE memory unless the function name says host; optional
+ * outputs may be NULL.  Calls are ordered on the given cudaStream_t (passed
+ * as void*; NULL = legacy default stream).  Return 0 on success, a negative
+ * FWBF_E* code otherwise (see fwbf_last_error()).  The library never falls
+ * back to the CPU: without a usable CUDA device every decode call fails.
+ */
+#ifndef FWBF_B200_H
+#define FWBF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FWBF_ABI_VERSION 1
+
+#define FWBF_OK 0
+#define FWBF_EINVAL (-1)      /* ValueError in the reference (bad config / shape) */
+#define FWBF_ECUDA (-2)       /* CUDA runtime failure (no device, launch error)   */
+#define FWBF_EUNSUPPORTED (-3)/* valid request this build cannot serve           */
+
+/* algorithm ids: the reference's _SELECTORS keys (decoders.py:186) */
+#define FWBF_ALG_FWBF 0
+#define FWBF_ALG_IMWBF 1
+#define FWBF_ALG_MLP 2
+
+/* weight modes: Eq.(1) exclude-self weights (decoders.py:80-84) or the
+ * include-self minimum of classic WBF/MWBF (alpha = 0 gives WBF) */
+#define FWBF_WEIGHTS_IMWBF 0
+#define FWBF_WEIGHTS_MWBF 1
+
+/* stall policies (decoders.py:29) */
+#define FWBF_STALL_FLIP_GLOBAL_MAX 0
+#define FWBF_STALL_TERMINATE 1
+
+/* per-frame flag bits written to fwbf_outputs.flags */
+#define FWBF_FLAG_CONVERGED 1
+#define FWBF_FLAG_STALLED 2
+#define FWBF_FLAG_ORDERED 4   /* decoded on the ordered (non-guarded) metric path */
+#define FWBF_FLAG_NONFINITE 8 /* y held NaN/inf; result follows IEEE comparisons */
+
+/* counters vector layout (int64) */
+enum {
+  FWBF_CNT_FRAMES = 0,
+  FWBF_CNT_BIT_ERRORS,
+  FWBF_CNT_WORD_ERRORS,
+  FWBF_CNT_ITER_SUM,
+  FWBF_CNT_FLIP_SUM,
+  FWBF_CNT_STALLS,
+  FWBF_CNT_CONVERGED,
+  FWBF_CNT_ORDERED_FRAMES,
+  FWBF_CNT_EDGE_VISITS,     /* metric terms accumulated (sum over frames of E*iters) */
+  FWBF_NCOUNTERS
+};
+
+typedef struct fwbf_code fwbf_code; /* opaque device handle */
+
+/* H as the reference stores it: CSR rows with sorted column indices
+ * (matrix.py:22-58).  If circulant != 0, H is the n x n circulant whose row m
+ * holds columns (offsets[j] + m) mod n (eg.py:46) and the CSR is optional. */
+typedef struct {
+  int32_t n_cols;
+  int32_t n_rows;
+  const int32_t *row_ptr; /* [n_rows + 1], host memory */
+  const int32_t *row_idx; /* [row_ptr[n_rows]], sorted per row, host memory */
+  int32_t circulant;
+  int32_t n_offsets;
+  const int32_t *offsets; /* sorted first-row columns, host memory */
+} fwbf_code_desc;
+
+/* DecoderConfig (decoders.py:32-61) plus the algorithm selector. */
+typedef struct {
+  int32_t algorithm;     /* FWBF_ALG_* */
+  int32_t weight_mode;   /* FWBF_WEIGHTS_* */
+  double alpha;          /* >= 0 */
+  int32_t k_max;         /* >= 1 */
+  int32_t lam;           /* >= 1, <= n (MLP) */
+  int32_t block_len_p;   /* >= 1 (FWBF) */
+  int32_t stall;         /* FWBF_STALL_* */
+  int32_t mlp_threshold; /* 0/1 */
+  int32_t force_ordered; /* 1: never use the guarded fast metric path (testing) */
+} fwbf_params;
+
+/* Output buffers (device memory, caller-owned, all optional). */
+typedef struct {
+  uint32_t *z_bits;        /* [B][z_ld] words; bit n of frame f = word n/32, bit n%32 */
+  int64_t z_ld;            /* words per frame row, >= ceil(n/32) */
+  int32_t *iterations;     /* [B] */
+  uint8_t *flags;          /* [B] FWBF_FLAG_* */
+  int32_t *flips_total;    /* [B] */
+  int32_t *bit_errors;     /* [B] popcount(z xor codeword) */
+  int32_t *fliplog;        /* [B][fliplog_stride] flipped indices, iteration-major */
+  int32_t *fliplog_counts; /* [B][k_max] flips per iteration */
+  int64_t fliplog_stride;  /* >= k_max * max flips per iteration */
+  int64_t *counters;       /* [FWBF_NCOUNTERS], accumulated (not cleared) */
+  int64_t *iter_hist;      /* [k_max + 1], accumulated */
+  int32_t *batch_word_err; /* [ceil(B / batch_frames)], accumulated */
+  int32_t batch_frames;    /* harness BATCH_FRAMES (harness.py:24), e.g. 128 */
+  const uint32_t *codeword_bits; /* [ceil(n/32)] transmitted word; NULL = all-zero */
+} fwbf_outputs;
+
+int fwbf_abi_version(void);
+const char *fwbf_last_error(void);
+int fwbf_device_count(void);
+
+int fwbf_code_create(const fwbf_code_desc *desc, int device, fwbf_code **out);
+int fwbf_code_destroy(fwbf_code *code);
+int fwbf_code_info(const fwbf_code *code, int32_t *n_cols, int32_t *n_rows,
+                   int32_t *n_edges, int32_t *circulant);
+
+/* Max flips one iteration can produce (sizes fliplog rows). */
+int64_t fwbf_max_flips_per_iter(const fwbf_code *code, const fwbf_params *params);
+
+/* Decode B frames of channel output y[f * ld + n] (device memory). */
+int fwbf_decode_f32(fwbf_code *code, const fwbf_params *params, const float *y,
+                    int64_t batch, int64_t ld, const fwbf_outputs *out, void *stream);
+int fwbf_decode_f64(fwbf_code *code, const fwbf_params *params, const double *y,
+                    int64_t batch, int64_t ld, const fwbf_outputs *out, void *stream);
+
+/* Noise modes for fwbf_decode_awgn. */
+#define FWBF_NOISE_NUMPY_F64 0 /* the reference stream: numpy Philox(key=seed,
+                                  counter=frame<<128) + Generator.standard_normal,
+                                  y = s + sigma*g in float64 (channel.py:29-50) */
+#define FWBF_NOISE_NUMPY_F32 1 /* same stream, y rounded to float32 */
+
+/* Decode frames [first_frame, first_frame + count) of the reference channel:
+ * y = (1 - 2c) + sigma * g with g drawn on the device; c = out->codeword_bits
+ * (NULL = all-zero).  Equivalent to harness._run_batch over that range. */
+int fwbf_decode_awgn(fwbf_code *code, const fwbf_params *params, uint64_t seed,
+                     int64_t first_frame, int64_t count, double sigma,
+                     int32_t noise_mode, const fwbf_outputs *out, void *stream);
+
+/* End-to-end call on HOST buffers: y_host [batch][ld] floats; outputs are host
+ * arrays (any may be NULL; counters accumulated).  Copies are pipelined in
+ * chunks of chunk_frames against decoding on two internal streams; pinned
+ * host memory gives full overlap.  Synchronous: returns when results are in
+ * host memory. */
+int fwbf_decode_host_f32(fwbf_code *code, const fwbf_params *params, const float *y_host,
+                         int64_t batch, int64_t ld, uint32_t *z_bits_host, int64_t z_ld,
+                         int32_t *iterations_host, uint8_t *flags_host,
+                         int64_t *counters_host, int64_t chunk_frames);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FWBF_B200_H */

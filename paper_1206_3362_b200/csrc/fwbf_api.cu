@@ -1,0 +1,503 @@
+// fwbf_api.cu -- C ABI: code handles, validation, launch planning, host pipeline.
+//
+// Validation mirrors the ValueErrors of the reference
+// (/root/reference/pkg/src/fwbf/decoders.py:51-61, :89-93, :192-193, :245-246,
+// :257-258); the message text is available from fwbf_last_error().
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fwbf_b200.h"
+#include "fwbf_internal.h"
+
+namespace fwbf {
+template <typename YT, bool CIRC, int KC, int TB> __global__ void decode_kernel(const __grid_constant__ KParams P);
+}
+
+using fwbf::KParams;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess) return fail(FWBF_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+struct fwbf_code {
+  int device = 0;
+  int n = 0, m = 0;
+  long long n_edges = 0;
+  int circ = 0, w = 0;
+  int dv_max = 0, dc_max = 0, min_row_w = 0;
+  int off[fwbf::kMaxCircWeight] = {0};
+  int dneg[fwbf::kMaxCircWeight] = {0};
+  int *d_row_ptr = nullptr, *d_row_idx = nullptr, *d_col_ptr = nullptr, *d_col_idx = nullptr;
+  uint8_t *d_i0tab = nullptr;
+  int16_t *d_offpos = nullptr;
+  unsigned int *d_work = nullptr; // ring of per-launch work counters
+  std::atomic<unsigned> work_slot{0};
+  int sm_count = 0;
+  int smem_optin = 0;
+  // host pipeline scratch
+  std::mutex pipe_mu;
+  cudaStream_t pipe_s[2] = {nullptr, nullptr};
+  void *pipe_buf[2] = {nullptr, nullptr};
+  size_t pipe_bytes = 0;
+  int64_t *pipe_counters = nullptr;
+};
+
+static constexpr int kWorkRing = 1024;
+
+extern "C" int fwbf_abi_version(void) { return FWBF_ABI_VERSION; }
+extern "C" const char *fwbf_last_error(void) { return g_err.c_str(); }
+
+extern "C" int fwbf_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) { cudaGetLastError(); return 0; }
+  return n;
+}
+
+template <typename T> static int upload(T **dst, const std::vector<T> &v) {
+  CUDA_TRY(cudaMalloc((void **)dst, std::max<size_t>(1, v.size()) * sizeof(T)));
+  if (!v.empty()) CUDA_TRY(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return FWBF_OK;
+}
+
+extern "C" int fwbf_code_create(const fwbf_code_desc *desc, int device, fwbf_code **out) {
+  if (!desc || !out) return fail(FWBF_EINVAL, "null argument");
+  *out = nullptr;
+  const int n = desc->n_cols, m = desc->n_rows;
+  if (n < 1) return fail(FWBF_EINVAL, "n_cols must be positive");
+  if (m < 0) return fail(FWBF_EINVAL, "n_rows must be nonnegative");
+  // Build the row lists (from CSR, or from the circulant offsets).
+  std::vector<int> row_ptr(m + 1, 0), row_idx;
+  if (desc->circulant) {
+    if (n != m) return fail(FWBF_EINVAL, "a circulant code must be square");
+    const int w = desc->n_offsets;
+    if (w < 1 || w > fwbf::kMaxCircWeight || !desc->offsets)
+      return fail(FWBF_EINVAL, "circulant weight must be in [1, %d]", fwbf::kMaxCircWeight);
+    for (int j = 0; j < w; ++j) {
+      if (desc->offsets[j] < 0 || desc->offsets[j] >= n) return fail(FWBF_EINVAL, "offset out of range");
+      if (j && desc->offsets[j] <= desc->offsets[j - 1]) return fail(FWBF_EINVAL, "offsets must be strictly ascending");
+    }
+    row_idx.reserve((size_t)n * w);
+    std::vector<int> r(w);
+    for (int i = 0; i < m; ++i) {
+      for (int j = 0; j < w; ++j) r[j] = (desc->offsets[j] + i) % n;
+      std::sort(r.begin(), r.end());
+      row_idx.insert(row_idx.end(), r.begin(), r.end());
+      row_ptr[i + 1] = (int)row_idx.size();
+    }
+  } else {
+    if (!desc->row_ptr || (m && !desc->row_idx)) return fail(FWBF_EINVAL, "CSR arrays required");
+    if (desc->row_ptr[0] != 0) return fail(FWBF_EINVAL, "row_ptr[0] must be 0");
+    for (int i = 0; i < m; ++i) {
+      const int a = desc->row_ptr[i], b = desc->row_ptr[i + 1];
+      if (b < a) return fail(FWBF_EINVAL, "row_ptr must be nondecreasing");
+      for (int e = a; e < b; ++e) {
+        const int c = desc->row_idx[e];
+        if (c < 0 || c >= n) return fail(FWBF_EINVAL, "row %d has a column index out of range", i);
+        if (e > a && c <= desc->row_idx[e - 1]) return fail(FWBF_EINVAL, "row %d is not strictly ascending", i);
+      }
+      row_ptr[i + 1] = b;
+    }
+    row_idx.assign(desc->row_idx, desc->row_idx + row_ptr[m]);
+  }
+  const long long E = row_ptr[m];
+  // CSC with ascending checks per column (matrix.py:38-42 builds col_adj row by row).
+  std::vector<int> col_ptr(n + 1, 0), col_idx(E);
+  for (long long e = 0; e < E; ++e) col_ptr[row_idx[e] + 1]++;
+  for (int i = 0; i < n; ++i) col_ptr[i + 1] += col_ptr[i];
+  {
+    std::vector<int> fill(col_ptr.begin(), col_ptr.end() - 1);
+    for (int i = 0; i < m; ++i)
+      for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) col_idx[fill[row_idx[e]]++] = i;
+  }
+  fwbf_code *c = new fwbf_code();
+  c->device = device;
+  c->n = n;
+  c->m = m;
+  c->n_edges = E;
+  int dvm = 0, dcm = 0, minrw = m ? 1 << 30 : 2;
+  for (int i = 0; i < n; ++i) dvm = std::max(dvm, col_ptr[i + 1] - col_ptr[i]);
+  for (int i = 0; i < m; ++i) {
+    dcm = std::max(dcm, row_ptr[i + 1] - row_ptr[i]);
+    minrw = std::min(minrw, row_ptr[i + 1] - row_ptr[i]);
+  }
+  c->dv_max = dvm;
+  c->dc_max = dcm;
+  c->min_row_w = minrw;
+  std::vector<uint8_t> i0tab;
+  std::vector<int16_t> offpos;
+  if (desc->circulant) {
+    c->circ = 1;
+    c->w = desc->n_offsets;
+    const int w = c->w;
+    for (int j = 0; j < w; ++j) c->off[j] = desc->offsets[j];
+    std::vector<int> dn(w);
+    for (int j = 0; j < w; ++j) dn[j] = (n - desc->offsets[j]) % n;
+    std::sort(dn.begin(), dn.end());
+    for (int j = 0; j < w; ++j) c->dneg[j] = dn[j];
+    // Column n's checks are (n + dneg[i]) mod n; ascending order starts at the
+    // first i with n + dneg[i] >= n (the wrapped, smaller ones).
+    i0tab.resize(n);
+    for (int col = 0; col < n; ++col) {
+      int i0 = 0;
+      while (i0 < w && col + dn[i0] < n) ++i0;
+      i0tab[col] = (uint8_t)(i0 == w ? 0 : i0);
+    }
+    offpos.assign(n, (int16_t)-1);
+    for (int j = 0; j < w; ++j) offpos[desc->offsets[j]] = (int16_t)j;
+  }
+  int rc;
+  cudaError_t ce = cudaSetDevice(device);
+  if (ce != cudaSuccess) { delete c; return fail(FWBF_ECUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(ce)); }
+  if ((rc = upload(&c->d_row_ptr, row_ptr)) || (rc = upload(&c->d_row_idx, row_idx)) ||
+      (rc = upload(&c->d_col_ptr, col_ptr)) || (rc = upload(&c->d_col_idx, col_idx)) ||
+      (rc = upload(&c->d_i0tab, i0tab)) || (rc = upload(&c->d_offpos, offpos))) {
+    fwbf_code_destroy(c);
+    return rc;
+  }
+  ce = cudaMalloc((void **)&c->d_work, kWorkRing * sizeof(unsigned));
+  if (ce != cudaSuccess) { fwbf_code_destroy(c); return fail(FWBF_ECUDA, "cudaMalloc: %s", cudaGetErrorString(ce)); }
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&c->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  *out = c;
+  return FWBF_OK;
+}
+
+extern "C" int fwbf_code_destroy(fwbf_code *c) {
+  if (!c) return FWBF_OK;
+  cudaSetDevice(c->device);
+  cudaFree(c->d_row_ptr);
+  cudaFree(c->d_row_idx);
+  cudaFree(c->d_col_ptr);
+  cudaFree(c->d_col_idx);
+  cudaFree(c->d_i0tab);
+  cudaFree(c->d_offpos);
+  cudaFree(c->d_work);
+  for (int i = 0; i < 2; ++i) {
+    if (c->pipe_s[i]) cudaStreamDestroy(c->pipe_s[i]);
+    if (c->pipe_buf[i]) cudaFree(c->pipe_buf[i]);
+  }
+  cudaFree(c->pipe_counters);
+  delete c;
+  return FWBF_OK;
+}
+
+extern "C" int fwbf_code_info(const fwbf_code *c, int32_t *n, int32_t *m, int32_t *e, int32_t *circ) {
+  if (!c) return fail(FWBF_EINVAL, "null code");
+  if (n) *n = c->n;
+  if (m) *m = c->m;
+  if (e) *e = (int32_t)c->n_edges;
+  if (circ) *circ = c->circ;
+  return FWBF_OK;
+}
+
+static int validate(const fwbf_code *c, const fwbf_params *p) {
+  if (!c || !p) return fail(FWBF_EINVAL, "null argument");
+  if (!(p->alpha >= 0)) return fail(FWBF_EINVAL, "alpha must be nonnegative");
+  if (p->k_max < 1) return fail(FWBF_EINVAL, "k_max must be >= 1");
+  if (p->lam < 1) return fail(FWBF_EINVAL, "lam must be >= 1");
+  if (p->stall != FWBF_STALL_FLIP_GLOBAL_MAX && p->stall != FWBF_STALL_TERMINATE)
+    return fail(FWBF_EINVAL, "unknown stall policy %d", p->stall);
+  if (p->weight_mode != FWBF_WEIGHTS_IMWBF && p->weight_mode != FWBF_WEIGHTS_MWBF)
+    return fail(FWBF_EINVAL, "unknown weight mode %d", p->weight_mode);
+  switch (p->algorithm) {
+  case FWBF_ALG_FWBF:
+    if (p->block_len_p < 1) return fail(FWBF_EINVAL, "block_len_p must be >= 1");
+    break;
+  case FWBF_ALG_IMWBF: break;
+  case FWBF_ALG_MLP:
+    if (p->lam > c->n) return fail(FWBF_EINVAL, "lam=%d exceeds block length %d", p->lam, c->n);
+    break;
+  default: return fail(FWBF_EINVAL, "unknown algorithm %d", p->algorithm);
+  }
+  if (c->m && c->min_row_w < 2) return fail(FWBF_EINVAL, "every check must contain at least 2 bits");
+  return FWBF_OK;
+}
+
+extern "C" int64_t fwbf_max_flips_per_iter(const fwbf_code *c, const fwbf_params *p) {
+  if (!c || !p) return 0;
+  switch (p->algorithm) {
+  case FWBF_ALG_FWBF: return p->block_len_p >= 1 ? (c->n + p->block_len_p - 1) / p->block_len_p : 0;
+  case FWBF_ALG_IMWBF: return 1;
+  case FWBF_ALG_MLP: return std::min(p->lam, c->n);
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Launch planning
+// ---------------------------------------------------------------------------
+static inline int align16(int x) { return (x + 15) & ~15; }
+
+struct Plan {
+  int threads = 0;
+  int kc = 1;
+  bool circ_kernel = false;
+  int smem = 0;
+};
+
+static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool circ, int cover, KParams &P) {
+  const int n = c->n, m = c->m;
+  const int zw = (n + 31) / 32, sw = (m + 31) / 32;
+  int nb = 1;
+  if (p->algorithm == FWBF_ALG_FWBF) nb = (n + p->block_len_p - 1) / p->block_len_p;
+  const int nslots = std::max(nb, std::max(p->algorithm == FWBF_ALG_MLP ? p->lam : 1, 1));
+  const int maxf = std::max(1, (int)fwbf_max_flips_per_iter(c, p));
+  const int aw = (c->w > 32) ? 2 : 1;
+  int o = 0;
+  auto take = [&](int bytes) { int r = o; o = align16(o + bytes); return r; };
+  P.off_y = take(n * ysize);
+  P.off_e = take(n * 8);
+  // guarded path: doubled signed min1 plus zero pad up to the threads' column cover
+  P.off_chk1 = take((circ ? 2 * n + std::max(0, cover - n) : m) * 8);
+  P.off_chk2 = take(m * 8);
+  P.off_amin = take(m * 4);
+  P.off_amask = take(circ ? n * aw * 4 : 4);
+  P.off_sbits = take(sw * 4);
+  P.off_zbits = take(zw * 4);
+  P.off_blkv = take(nslots * 8);
+  P.off_blki = take((nslots + zw) * 4);
+  P.off_flips = take(maxf * 4);
+  P.off_offs = take(2 * fwbf::kMaxCircWeight * 4);
+  P.off_red = take(32 * 8 + 32 * 4);
+  P.off_misc = take(16 * 4 + 64 * 4);
+  P.smem_bytes = o;
+}
+
+template <typename YT>
+static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long long batch,
+                         long long ld, const fwbf_outputs *out, cudaStream_t stream) {
+  int rc = validate(c, p);
+  if (rc) return rc;
+  if (batch < 0) return fail(FWBF_EINVAL, "batch must be nonnegative");
+  if (batch == 0) return FWBF_OK;
+  if (!y) return fail(FWBF_EINVAL, "y is null");
+  if (ld < c->n) return fail(FWBF_EINVAL, "expected a length-%d frame (ld=%lld)", c->n, ld);
+  if (batch > 0x7fffffffLL) return fail(FWBF_EINVAL, "batch too large for one call");
+  fwbf_outputs o = out ? *out : fwbf_outputs{};
+  const long long maxf = fwbf_max_flips_per_iter(c, p);
+  if (o.fliplog) {
+    if (!o.fliplog_counts) return fail(FWBF_EINVAL, "fliplog requires fliplog_counts");
+    if (o.fliplog_stride < (long long)p->k_max * maxf)
+      return fail(FWBF_EINVAL, "fliplog_stride must be >= k_max * %lld", maxf);
+  }
+  if (o.z_bits && o.z_ld < (c->n + 31) / 32) return fail(FWBF_EINVAL, "z_ld too small");
+  if (o.batch_word_err && o.batch_frames < 1) return fail(FWBF_EINVAL, "batch_frames must be >= 1");
+
+  CUDA_TRY(cudaSetDevice(c->device));
+  KParams P;
+  memset(&P, 0, sizeof P);
+  P.n = c->n;
+  P.m = c->m;
+  P.w = c->circ ? c->w : 0;
+  P.dv_max = c->dv_max;
+  P.n_edges = c->n_edges;
+  memcpy(P.off, c->off, sizeof P.off);
+  memcpy(P.dneg, c->dneg, sizeof P.dneg);
+  P.i0tab = c->d_i0tab;
+  P.offpos = c->d_offpos;
+  P.row_ptr = c->d_row_ptr;
+  P.row_idx = c->d_row_idx;
+  P.col_ptr = c->d_col_ptr;
+  P.col_idx = c->d_col_idx;
+  P.alg = p->algorithm;
+  P.wmode = p->weight_mode;
+  P.kmax = p->k_max;
+  P.lam = p->lam;
+  P.p = p->block_len_p;
+  P.stall = p->stall;
+  P.mlp_thr = p->mlp_threshold ? 1 : 0;
+  P.force_ordered = p->force_ordered ? 1 : 0;
+  P.alpha = p->alpha;
+  P.nblocks = p->algorithm == FWBF_ALG_FWBF ? (c->n + p->block_len_p - 1) / p->block_len_p : 1;
+  P.y = y;
+  P.ld = ld;
+  P.batch = batch;
+  P.z_bits = o.z_bits;
+  P.z_ld = o.z_ld;
+  P.iterations = o.iterations;
+  P.flags = o.flags;
+  P.flips_total = o.flips_total;
+  P.bit_errors = o.bit_errors;
+  P.fliplog = o.fliplog;
+  P.fliplog_counts = o.fliplog_counts;
+  P.fliplog_stride = o.fliplog_stride;
+  P.counters = (long long *)o.counters;
+  P.iter_hist = (long long *)o.iter_hist;
+  P.batch_word_err = o.batch_word_err;
+  P.batch_frames = o.batch_frames;
+  P.codeword_bits = o.codeword_bits;
+  const unsigned slot = c->work_slot.fetch_add(1) % kWorkRing;
+  P.work_counter = c->d_work + slot;
+
+  const bool circ = c->circ && c->n <= 8192;
+  const void *kern = nullptr;
+  int T = 0;
+  int kc = 1;
+  if (circ) {
+    if (sizeof(YT) == 4) {
+      static const struct { int kc, tb; const void *fn; } shapes[] = {
+#define FWBF_SHAPE(YT_, C_, KC_, TB_) {KC_, TB_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_>},
+          FWBF_FAST_CONFIGS(FWBF_SHAPE)
+#undef FWBF_SHAPE
+      };
+      for (const auto &s : shapes)
+        if (s.kc * s.tb >= c->n) { kern = s.fn; T = s.tb; kc = s.kc; break; }
+    } else {
+      T = c->n <= 2048 ? 256 : (c->n <= 8192 ? 512 : 1024);
+      kern = (const void *)fwbf::decode_kernel<double, true, 1, 0>;
+    }
+  } else {
+    T = c->n <= 2048 ? 256 : (c->n <= 8192 ? 512 : 1024);
+    kern = sizeof(YT) == 4 ? (const void *)fwbf::decode_kernel<float, false, 1, 0>
+                           : (const void *)fwbf::decode_kernel<double, false, 1, 0>;
+  }
+  layout(c, p, (int)sizeof(YT), circ, T * kc, P);
+  if (P.smem_bytes > c->smem_optin) {
+    // Alias the metric buffer over the y buffer: after init y is only needed
+    // for alpha*|y|, which the kernel then re-reads from global memory.
+    P.alias_y = 1;
+    const int delta = (P.off_y + align16(c->n * 8)) - P.off_chk1;
+    P.off_e = P.off_y;
+    for (int *x : {&P.off_chk1, &P.off_chk2, &P.off_amin, &P.off_amask, &P.off_sbits, &P.off_zbits,
+                   &P.off_blkv, &P.off_blki, &P.off_flips, &P.off_offs, &P.off_red, &P.off_misc})
+      *x += delta;
+    P.smem_bytes += delta;
+  }
+  if (P.smem_bytes > c->smem_optin)
+    return fail(FWBF_EUNSUPPORTED, "frame state needs %d B of shared memory (device max %d)",
+                P.smem_bytes, c->smem_optin);
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P.smem_bytes));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, P.smem_bytes));
+  if (per_sm < 1) return fail(FWBF_EUNSUPPORTED, "kernel does not fit on an SM");
+  const long long grid = std::min<long long>(batch, (long long)per_sm * c->sm_count);
+  CUDA_TRY(cudaMemsetAsync(P.work_counter, 0, sizeof(unsigned), stream));
+  void *args[] = {&P};
+  CUDA_TRY(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(T), args, P.smem_bytes, stream));
+  CUDA_TRY(cudaGetLastError());
+  return FWBF_OK;
+}
+
+extern "C" int fwbf_decode_f32(fwbf_code *c, const fwbf_params *p, const float *y, int64_t batch,
+                               int64_t ld, const fwbf_outputs *out, void *stream) {
+  return launch_decode<float>(c, p, y, batch, ld, out, (cudaStream_t)stream);
+}
+
+extern "C" int fwbf_decode_f64(fwbf_code *c, const fwbf_params *p, const double *y, int64_t batch,
+                               int64_t ld, const fwbf_outputs *out, void *stream) {
+  return launch_decode<double>(c, p, y, batch, ld, out, (cudaStream_t)stream);
+}
+
+extern "C" int fwbf_decode_awgn(fwbf_code *c, const fwbf_params *p, uint64_t seed, int64_t first,
+                                int64_t count, double sigma, int32_t mode, const fwbf_outputs *out,
+                                void *stream) {
+  (void)c; (void)p; (void)seed; (void)first; (void)count; (void)sigma; (void)mode; (void)out; (void)stream;
+  return fail(FWBF_EUNSUPPORTED, "on-device noise is not built into this library version");
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer pipeline: chunked H2D -> decode -> D2H on two streams.
+// ---------------------------------------------------------------------------
+extern "C" int fwbf_decode_host_f32(fwbf_code *c, const fwbf_params *p, const float *y_host,
+                                    int64_t batch, int64_t ld, uint32_t *z_host, int64_t z_ld,
+                                    int32_t *it_host, uint8_t *fl_host, int64_t *cnt_host,
+                                    int64_t chunk) {
+  int rc = validate(c, p);
+  if (rc) return rc;
+  if (batch < 0) return fail(FWBF_EINVAL, "batch must be nonnegative");
+  if (batch == 0) return FWBF_OK;
+  if (!y_host) return fail(FWBF_EINVAL, "y is null");
+  if (ld < c->n) return fail(FWBF_EINVAL, "expected a length-%d frame (ld=%lld)", c->n, (long long)ld);
+  const int zw = (c->n + 31) / 32;
+  if (z_host && z_ld < zw) return fail(FWBF_EINVAL, "z_ld too small");
+  if (chunk <= 0) chunk = 65536;
+  chunk = std::min<int64_t>(chunk, batch);
+  std::lock_guard<std::mutex> lock(c->pipe_mu);
+  CUDA_TRY(cudaSetDevice(c->device));
+  // per-stream buffer: y chunk | z chunk | iterations | flags
+  const size_t yb = (size_t)chunk * ld * sizeof(float);
+  const size_t zb = (size_t)chunk * zw * sizeof(uint32_t);
+  const size_t ib = (size_t)chunk * sizeof(int32_t);
+  const size_t fb = (size_t)chunk;
+  const size_t need = align16((int)0) + yb + zb + ib + fb + 64;
+  if (need > c->pipe_bytes) {
+    for (int i = 0; i < 2; ++i) {
+      if (c->pipe_buf[i]) cudaFree(c->pipe_buf[i]);
+      c->pipe_buf[i] = nullptr;
+    }
+    c->pipe_bytes = 0;
+    for (int i = 0; i < 2; ++i) CUDA_TRY(cudaMalloc(&c->pipe_buf[i], need));
+    c->pipe_bytes = need;
+  }
+  for (int i = 0; i < 2; ++i)
+    if (!c->pipe_s[i]) CUDA_TRY(cudaStreamCreateWithFlags(&c->pipe_s[i], cudaStreamNonBlocking));
+  if (!c->pipe_counters) CUDA_TRY(cudaMalloc((void **)&c->pipe_counters, FWBF_NCOUNTERS * sizeof(int64_t)));
+  CUDA_TRY(cudaMemsetAsync(c->pipe_counters, 0, FWBF_NCOUNTERS * sizeof(long long), c->pipe_s[0]));
+  CUDA_TRY(cudaStreamSynchronize(c->pipe_s[0]));
+  const long long nchunks = (batch + chunk - 1) / chunk;
+  for (long long ci = 0; ci < nchunks; ++ci) {
+    const int s = (int)(ci & 1);
+    cudaStream_t st = c->pipe_s[s];
+    char *base = (char *)c->pipe_buf[s];
+    float *dy = (float *)base;
+    uint32_t *dz = (uint32_t *)(base + yb);
+    int32_t *dit = (int32_t *)(base + yb + zb);
+    uint8_t *dfl = (uint8_t *)(base + yb + zb + ib);
+    const long long f0 = ci * chunk;
+    const long long nb = std::min<long long>(chunk, batch - f0);
+    CUDA_TRY(cudaMemcpyAsync(dy, y_host + f0 * ld, (size_t)nb * ld * sizeof(float), cudaMemcpyHostToDevice, st));
+    fwbf_outputs o{};
+    o.z_bits = z_host ? dz : nullptr;
+    o.z_ld = zw;
+    o.iterations = it_host ? dit : nullptr;
+    o.flags = fl_host ? dfl : nullptr;
+    o.counters = c->pipe_counters;
+    rc = launch_decode<float>(c, p, dy, nb, ld, &o, st);
+    if (rc) return rc;
+    if (z_host) {
+      if (z_ld == zw) {
+        CUDA_TRY(cudaMemcpyAsync(z_host + f0 * z_ld, dz, (size_t)nb * zw * 4, cudaMemcpyDeviceToHost, st));
+      } else {
+        CUDA_TRY(cudaMemcpy2DAsync(z_host + f0 * z_ld, (size_t)z_ld * 4, dz, (size_t)zw * 4, (size_t)zw * 4,
+                                   (size_t)nb, cudaMemcpyDeviceToHost, st));
+      }
+    }
+    if (it_host) CUDA_TRY(cudaMemcpyAsync(it_host + f0, dit, (size_t)nb * 4, cudaMemcpyDeviceToHost, st));
+    if (fl_host) CUDA_TRY(cudaMemcpyAsync(fl_host + f0, dfl, (size_t)nb, cudaMemcpyDeviceToHost, st));
+    if (ci == 0 && nchunks > 1) {
+      // stream 1 must not start decoding before the counters are cleared (done above, synced)
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->pipe_s[0]));
+  CUDA_TRY(cudaStreamSynchronize(c->pipe_s[1]));
+  if (cnt_host) {
+    long long tmp[FWBF_NCOUNTERS];
+    CUDA_TRY(cudaMemcpy(tmp, c->pipe_counters, sizeof tmp, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < FWBF_NCOUNTERS; ++i) cnt_host[i] += tmp[i];
+  }
+  return FWBF_OK;
+}

@@ -1,0 +1,571 @@
+// fwbf_decode.cu -- batched weighted bit-flipping LDPC decoding on B200 (sm_100a).
+//
+// One persistent CTA decodes one frame at a time, pulling frame indices from an
+// atomic work queue (iteration counts vary 0..k_max per frame).  All per-frame
+// state lives in shared memory; H lives in kernel parameters (circulant offsets)
+// or in small read-only global tables (explicit CSR/CSC).
+//
+// Reference semantics (/root/reference/pkg/src/fwbf/decoders.py):
+//   init        :191-198  |y|, hard decision, syndrome, per-check min1/min2/argmin
+//   loop        :204-229  converged? -> k_max? -> Eq.(1) metric -> select -> flip
+//   metric      :148-153  E_n = fl(sum_{m in M(n), ascending} (2s_m-1) w_nm) - fl(alpha|y_n|)
+//   selection   :156-183  block argmax (+ threshold), global argmax, top-lambda
+//
+// Two metric paths, selected per frame:
+//   * ORDERED: the column sum in ascending check order with fp64 adds, exactly
+//     the reference's np.bincount sequence.  Bit-exact for any input.
+//   * GUARDED (float32 y, circulant H): sum_j sgn*min1[n - c_j] over doubled
+//     shared arrays plus an argmin correction.  Order-free and bit-exact when
+//     every partial sum is representable: all weights are float32 values, i.e.
+//     multiples of q = 2^(e_min - 23); partial sums are bounded by 2*dv*max|y|;
+//     so if 2*dv*max|y| < 2^53 q every fp64 add is exact and the result equals
+//     the reference's sum regardless of order.  Frames failing the guard take
+//     the ordered path (flagged FWBF_FLAG_ORDERED).
+//
+// Ties: every argmax takes the lowest index (numpy argmax / stable argsort).
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "fwbf_b200.h"
+#include "fwbf_internal.h"
+
+namespace fwbf {
+
+#define FULL_MASK 0xffffffffu
+
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+
+// lexicographic (value desc, index asc) -- numpy first-occurrence argmax
+__device__ __forceinline__ void amax_combine(double &v, int &i, double v2, int i2) {
+  if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+}
+
+__device__ __forceinline__ void warp_amax(double &v, int &i) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    double v2 = __shfl_xor_sync(FULL_MASK, v, off);
+    int i2 = __shfl_xor_sync(FULL_MASK, i, off);
+    amax_combine(v, i, v2, i2);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Shared-memory layout (byte offsets computed on the host, see plan_layout).
+// ---------------------------------------------------------------------------
+struct Smem {
+  unsigned char *base;
+  const KParams &P;
+  __device__ Smem(unsigned char *b, const KParams &p) : base(b), P(p) {}
+  template <typename T> __device__ T *at(int off) const { return reinterpret_cast<T *>(base + off); }
+};
+
+template <typename YT>
+__device__ __forceinline__ YT load_y(const KParams &P, long long f, int n) {
+  const YT *y = reinterpret_cast<const YT *>(P.y);
+  return __ldg(y + f * P.ld + n);
+}
+
+// ---------------------------------------------------------------------------
+// The decode kernel.
+//   YT   : float (float32 channel output) or double
+//   CIRC : circulant H (index arithmetic) vs explicit CSR/CSC tables
+//   KC   : columns per thread on the guarded path (register accumulators)
+// ---------------------------------------------------------------------------
+template <typename YT, bool CIRC, int KC, int TB>
+__global__ void __launch_bounds__(TB ? TB : 1024, 1)
+decode_kernel(const __grid_constant__ KParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x;
+  const int T = TB ? TB : (int)blockDim.x;  // compile-time on the guarded path
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int nwarps = T >> 5;
+  const int N = P.n;
+  const int M = P.m;
+
+  YT *ybuf = reinterpret_cast<YT *>(smem_raw + P.off_y);
+  double *Ebuf = reinterpret_cast<double *>(smem_raw + P.off_e);
+  double *chk1 = reinterpret_cast<double *>(smem_raw + P.off_chk1); // min1 (signed); doubled on the guarded path
+  double *chk2 = reinterpret_cast<double *>(smem_raw + P.off_chk2); // min2 (ordered) or min2-min1 (guarded), signed
+  int *amin = reinterpret_cast<int *>(smem_raw + P.off_amin);        // ordered path argmin column
+  uint32_t *amask = reinterpret_cast<uint32_t *>(smem_raw + P.off_amask); // guarded: per-column argmin j-mask
+  uint32_t *sbits = reinterpret_cast<uint32_t *>(smem_raw + P.off_sbits);
+  uint32_t *zbits = reinterpret_cast<uint32_t *>(smem_raw + P.off_zbits);
+  double *blk_v = reinterpret_cast<double *>(smem_raw + P.off_blkv);
+  int *blk_i = reinterpret_cast<int *>(smem_raw + P.off_blki);
+  int *flips = reinterpret_cast<int *>(smem_raw + P.off_flips);
+  int *offs_s = reinterpret_cast<int *>(smem_raw + P.off_offs);     // circulant offsets (for divergent j)
+  double *red_v = reinterpret_cast<double *>(smem_raw + P.off_red);
+  int *red_i = reinterpret_cast<int *>(smem_raw + P.off_red + 32 * 8);
+  int *misc = reinterpret_cast<int *>(smem_raw + P.off_misc);
+  float *redf = reinterpret_cast<float *>(smem_raw + P.off_misc + 16 * 4);
+  // misc slots
+  enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR, S_STOP };
+
+  const int W = P.w;                 // circulant weight (0 explicit)
+  const int aw = (W > 32) ? 2 : 1;   // amask words per column
+
+  if (CIRC) {
+    for (int j = tid; j < W; j += T) { offs_s[j] = P.off[j]; offs_s[64 + j] = P.dneg[j]; }
+  }
+  if (tid == 0) misc[S_NONFIN] = 0;
+
+  // per-CTA counter accumulation (thread 0)
+  long long c_frames = 0, c_biterr = 0, c_worderr = 0, c_iters = 0, c_flips = 0,
+            c_stalls = 0, c_conv = 0, c_ordered = 0, c_edges = 0;
+
+  const int zw = (N + 31) >> 5;
+  const int sw = (M + 31) >> 5;
+  const int nKy = (N + T - 1) / T; // rounds over columns
+  const int nKm = (M + T - 1) / T; // rounds over checks
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) misc[S_FRAME] = (int)atomicAdd(P.work_counter, 1u);
+    __syncthreads();
+    const long long f = misc[S_FRAME];
+    if (f >= P.batch) break;
+
+    // ---------------- init 1: y -> smem, hard decisions, guard statistics -------
+    float lmin = INFINITY, lmax = 0.f;
+    bool nonfin = false;
+    for (int k = 0; k < nKy; ++k) {
+      const int n = tid + k * T;
+      const bool ok = n < N;
+      YT v = ok ? load_y<YT>(P, f, n) : YT(0);
+      if (ok) ybuf[n] = v;
+      const uint32_t b = __ballot_sync(FULL_MASK, ok && (v < YT(0)));
+      if (lane == 0 && (k * T + warp * 32) < N) zbits[(k * T + warp * 32) >> 5] = b;
+      if (ok) {
+        if (!isfinite((double)v)) nonfin = true;
+        float a = fabsf((float)v);
+        if (a > 0.f) lmin = fminf(lmin, a);
+        lmax = fmaxf(lmax, a);
+        if (CIRC) {
+          for (int q = 0; q < aw; ++q) amask[n * aw + q] = 0u;
+        }
+      }
+    }
+    // block reduce (min nonzero |y|, max |y|, nonfinite)
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      lmin = fminf(lmin, __shfl_xor_sync(FULL_MASK, lmin, off));
+      lmax = fmaxf(lmax, __shfl_xor_sync(FULL_MASK, lmax, off));
+    }
+    nonfin = __any_sync(FULL_MASK, nonfin);
+    if (lane == 0) { redf[warp] = lmin; redf[32 + warp] = lmax; if (nonfin) misc[S_NONFIN] = 1; }
+    if (tid == 0) { misc[S_SWT] = 0; }
+    __syncthreads();
+    if (tid == 0) {
+      float mn = INFINITY, mx = 0.f;
+      for (int w2 = 0; w2 < nwarps; ++w2) { mn = fminf(mn, redf[w2]); mx = fmaxf(mx, redf[32 + w2]); }
+      int fast = 0;
+      if (CIRC && sizeof(YT) == 4 && !P.force_ordered && !misc[S_NONFIN]) {
+        if (!(mn < INFINITY)) {
+          fast = 1; // all |y| == 0: every weight is 0, sums trivially exact
+        } else {
+          int e = ((__float_as_int(mn) >> 23) & 0xff) - 127;
+          if (e < -126) e = -126;
+          // quantum q = 2^(e-23); need 2*dv*max|y| < 2^53 * q = 2^(30+e)
+          double lhs = 2.0 * (double)W * (double)mx;
+          fast = lhs < ldexp(1.0, 30 + e);
+        }
+      }
+      misc[S_FAST] = fast;
+    }
+    __syncthreads();
+    const bool fastp = misc[S_FAST] != 0;
+
+    // ---------------- init 2: per-check minima, syndrome, signed weights --------
+    for (int k = 0; k < nKm; ++k) {
+      const int m = tid + k * T;
+      const bool ok = m < M;
+      int par = 0;
+      YT min1 = YT(INFINITY), min2 = YT(INFINITY);
+      int ac = 0x7fffffff;
+      if (ok) {
+        if (CIRC) {
+          for (int j = 0; j < W; ++j) {
+            int c = m + P.off[j];
+            if (c >= N) c -= N;
+            const YT yv = ybuf[c];
+            par ^= (yv < YT(0));
+            const YT a = fabs(yv);
+            if (a < min1 || (a == min1 && c < ac)) { min2 = min1; min1 = a; ac = c; }
+            else if (a < min2) min2 = a;
+          }
+        } else {
+          const int e0 = __ldg(P.row_ptr + m), e1 = __ldg(P.row_ptr + m + 1);
+          for (int e = e0; e < e1; ++e) {
+            const int c = __ldg(P.row_idx + e);
+            const YT yv = ybuf[c];
+            par ^= (yv < YT(0));
+            const YT a = fabs(yv);
+            if (a < min1 || (a == min1 && c < ac)) { min2 = min1; min1 = a; ac = c; }
+            else if (a < min2) min2 = a;
+          }
+        }
+      }
+      const uint32_t b = __ballot_sync(FULL_MASK, ok && par);
+      if (lane == 0 && (k * T + warp * 32) < M) {
+        sbits[(k * T + warp * 32) >> 5] = b;
+        atomicAdd(&misc[S_SWT], __popc(b));
+      }
+      if (ok) {
+        const double sg = par ? 1.0 : -1.0;
+        const double d1 = (double)min1, d2 = (double)min2;
+        if (CIRC && fastp) {
+          chk1[m] = sg * d1;
+          chk1[m + N] = sg * d1;
+          if (P.wmode == FWBF_WEIGHTS_IMWBF) {
+            chk2[m] = sg * __dsub_rn(d2, d1); // exact: float32 operands
+            int d = ac - m;
+            if (d < 0) d += N;
+            const int j = P.offpos[d];
+            atomicOr(&amask[ac * aw + (j >> 5)], 1u << (j & 31));
+          } else {
+            chk2[m] = 0.0;
+          }
+        } else {
+          chk1[m] = sg * d1;
+          chk2[m] = sg * d2;
+          amin[m] = (P.wmode == FWBF_WEIGHTS_IMWBF) ? ac : -1;
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---------------- iterations -----------------------------------------------
+    int k = 0;
+    int conv = 0, stalled = 0;
+    long long logpos = 0;
+    long long flips_total = 0;
+    for (;;) {
+      const int swt = misc[S_SWT];
+      if (swt == 0) { conv = 1; break; }
+      if (k >= P.kmax) break;
+
+      // ---- Eq.(1) metric for every bit -> Ebuf ----
+      if (CIRC && fastp) {
+        // chk1 holds sgn*min1 twice ([0,N) and [N,2N)) plus KC*T-N zero pad, so
+        // column n reads check (n - c_j) mod N at chk1[n + N - c_j] with no wrap
+        // test: one uniform add per j, then KC immediate-offset LDS.64 + DADD.
+        double acc[KC];
+        int nk[KC];
+#pragma unroll
+        for (int q = 0; q < KC; ++q) { nk[q] = tid + q * T; acc[q] = 0.0; }
+        const double *src = chk1 + N + tid;
+        for (int j = 0; j < W; ++j) {
+          const double *sj = src - P.off[j];
+#pragma unroll
+          for (int q = 0; q < KC; ++q) acc[q] = __dadd_rn(acc[q], sj[q * T]);
+        }
+#pragma unroll
+        for (int q = 0; q < KC; ++q) {
+          const int n = nk[q];
+          if (n < N) {
+            for (int w2 = 0; w2 < aw; ++w2) {
+              uint32_t mk = amask[n * aw + w2];
+              while (mk) {
+                const int j = (__ffs(mk) - 1) + 32 * w2;
+                mk &= mk - 1;
+                int m = n - offs_s[j];
+                if (m < 0) m += N;
+                acc[q] = __dadd_rn(acc[q], chk2[m]);
+              }
+            }
+            const double ay = P.alias_y ? fabs((double)load_y<YT>(P, f, n)) : fabs((double)ybuf[n]);
+            Ebuf[n] = __dsub_rn(acc[q], __dmul_rn(P.alpha, ay));
+          }
+        }
+      } else {
+        for (int kk = 0; kk < nKy; ++kk) {
+          const int n = tid + kk * T;
+          if (n >= N) break;
+          double acc = 0.0;
+          if (CIRC) {
+            int ii = P.i0tab[n];
+            for (int i = 0; i < W; ++i) {
+              int m = n + offs_s[64 + ii];
+              if (m >= N) m -= N;
+              const double w = (amin[m] == n) ? chk2[m] : chk1[m];
+              acc = __dadd_rn(acc, w);
+              if (++ii == W) ii = 0;
+            }
+          } else {
+            const int e0 = __ldg(P.col_ptr + n), e1 = __ldg(P.col_ptr + n + 1);
+            for (int e = e0; e < e1; ++e) {
+              const int m = __ldg(P.col_idx + e);
+              const double w = (amin[m] == n) ? chk2[m] : chk1[m];
+              acc = __dadd_rn(acc, w);
+            }
+          }
+          const double ay = P.alias_y ? fabs((double)load_y<YT>(P, f, n)) : fabs((double)ybuf[n]);
+          Ebuf[n] = __dsub_rn(acc, __dmul_rn(P.alpha, ay));
+        }
+      }
+      __syncthreads();
+
+      // ---- selection ----
+      if (P.alg == FWBF_ALG_FWBF) {
+        const int p = P.p;
+        const int nb = P.nblocks;
+        if (p <= 32) {
+          const int G = 32 / p;
+          const int g = lane / p, o = lane - g * p;
+          const int tasks = (nb + G - 1) / G;
+          for (int t = warp; t < tasks; t += nwarps) {
+            const int b = t * G + g;
+            const int n = b * p + o;
+            const bool ok = (g < G) && (b < nb) && (n < N);
+            double v = ok ? Ebuf[n] : -dinf();
+            int i = ok ? n : 0x7fffffff;
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+              const double v2 = __shfl_down_sync(FULL_MASK, v, off);
+              const int i2 = __shfl_down_sync(FULL_MASK, i, off);
+              if (o + off < p) amax_combine(v, i, v2, i2);
+            }
+            if (o == 0 && g < G && b < nb) { blk_v[b] = v; blk_i[b] = i; }
+          }
+        } else {
+          for (int b = warp; b < nb; b += nwarps) {
+            double v = -dinf();
+            int i = 0x7fffffff;
+            for (int j = lane; j < p; j += 32) {
+              const int n = b * p + j;
+              if (n < N) amax_combine(v, i, Ebuf[n], n);
+            }
+            warp_amax(v, i);
+            if (lane == 0) { blk_v[b] = v; blk_i[b] = i; }
+          }
+        }
+        __syncthreads();
+        if (warp == 0) {
+          int cnt = 0;
+          double gv = -dinf();
+          int gi = 0x7fffffff;
+          for (int base = 0; base < nb; base += 32) {
+            const int b = base + lane;
+            double v = -dinf();
+            int i = 0x7fffffff;
+            if (b < nb) { v = blk_v[b]; i = blk_i[b]; }
+            amax_combine(gv, gi, v, i);
+            const bool pos = (b < nb) && (v > 0.0);
+            const uint32_t msk = __ballot_sync(FULL_MASK, pos);
+            if (pos) flips[cnt + __popc(msk & ((1u << lane) - 1u))] = i;
+            cnt += __popc(msk);
+          }
+          warp_amax(gv, gi);
+          if (lane == 0) { misc[S_F] = cnt; misc[S_GBEST] = gi; }
+        }
+      } else if (P.alg == FWBF_ALG_IMWBF) {
+        double v = -dinf();
+        int i = 0x7fffffff;
+        for (int n = tid; n < N; n += T) amax_combine(v, i, Ebuf[n], n);
+        warp_amax(v, i);
+        if (lane == 0) { red_v[warp] = v; red_i[warp] = i; }
+        __syncthreads();
+        if (warp == 0) {
+          v = lane < nwarps ? red_v[lane] : -dinf();
+          i = lane < nwarps ? red_i[lane] : 0x7fffffff;
+          warp_amax(v, i);
+          if (lane == 0) { misc[S_F] = 1; misc[S_GBEST] = i; flips[0] = i; }
+        }
+      } else { // MLP: lambda rounds of CTA argmax with exclusion, then ascending sort
+        // selected indices are marked in the E buffer by overwriting with -inf;
+        // their values are kept in blk_v/blk_i (sized lam on the host).
+        for (int r = 0; r < P.lam; ++r) {
+          double v = -dinf();
+          int i = 0x7fffffff;
+          for (int n = tid; n < N; n += T) amax_combine(v, i, Ebuf[n], n);
+          warp_amax(v, i);
+          if (lane == 0) { red_v[warp] = v; red_i[warp] = i; }
+          __syncthreads();
+          if (warp == 0) {
+            v = lane < nwarps ? red_v[lane] : -dinf();
+            i = lane < nwarps ? red_i[lane] : 0x7fffffff;
+            warp_amax(v, i);
+            if (lane == 0) {
+              blk_v[r] = v;
+              blk_i[r] = i;
+              Ebuf[i] = -dinf();
+              if (r == 0) misc[S_GBEST] = i;
+            }
+          }
+          __syncthreads();
+        }
+        // flips = selected (and positive when thresholded), ascending: mark in a
+        // bitmap over columns (reuse amask-free scratch: the zbits-sized area in
+        // blk_i beyond lam), then compact in index order.
+        uint32_t *sel = reinterpret_cast<uint32_t *>(blk_i + P.lam);
+        for (int w2 = tid; w2 < zw; w2 += T) sel[w2] = 0u;
+        __syncthreads();
+        for (int r = tid; r < P.lam; r += T) {
+          if (!P.mlp_thr || blk_v[r] > 0.0) {
+            const int i = blk_i[r];
+            atomicOr(&sel[i >> 5], 1u << (i & 31));
+          }
+        }
+        __syncthreads();
+        if (warp == 0) {
+          int cnt = 0;
+          for (int base = 0; base < zw; base += 32) {
+            const int w2 = base + lane;
+            const uint32_t word = (w2 < zw) ? sel[w2] : 0u;
+            int c = __popc(word);
+            int incl = c;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+              const int t2 = __shfl_up_sync(FULL_MASK, incl, off);
+              if (lane >= off) incl += t2;
+            }
+            int pos = cnt + incl - c;
+            uint32_t wd = word;
+            while (wd) {
+              const int bit = __ffs(wd) - 1;
+              wd &= wd - 1;
+              flips[pos++] = w2 * 32 + bit;
+            }
+            cnt += __shfl_sync(FULL_MASK, incl, 31);
+          }
+          if (lane == 0) misc[S_F] = cnt;
+        }
+      }
+      __syncthreads();
+
+      int F = misc[S_F];
+      if (F == 0) {
+        stalled = 1;
+        if (P.stall == FWBF_STALL_TERMINATE) {
+          if (tid == 0 && P.fliplog_counts) P.fliplog_counts[f * P.kmax + k] = 0;
+          k += 1;
+          break;
+        }
+        if (tid == 0) flips[0] = misc[S_GBEST];
+        F = 1;
+        __syncthreads();
+      }
+      // flip log
+      if (P.fliplog) {
+        for (int t = tid; t < F; t += T) P.fliplog[f * P.fliplog_stride + logpos + t] = flips[t];
+        if (tid == 0) P.fliplog_counts[f * P.kmax + k] = F;
+      }
+      logpos += F;
+      flips_total += F;
+
+      // ---- apply flips: z and syndrome toggles ----
+      if (tid == 0) misc[S_SWT] = 0;
+      for (int t = tid; t < F; t += T) {
+        const int n = flips[t];
+        atomicXor(&zbits[n >> 5], 1u << (n & 31));
+      }
+      if (CIRC) {
+        const int tot = F * W;
+        for (int t = tid; t < tot; t += T) {
+          const int fi = t / W;
+          const int j = t - fi * W;
+          const int n = flips[fi];
+          int m = n - offs_s[j];
+          if (m < 0) m += N;
+          atomicXor(&sbits[m >> 5], 1u << (m & 31));
+        }
+      } else {
+        const int dv = P.dv_max;
+        const int tot = F * dv;
+        for (int t = tid; t < tot; t += T) {
+          const int fi = t / dv;
+          const int j = t - fi * dv;
+          const int n = flips[fi];
+          const int e0 = __ldg(P.col_ptr + n), e1 = __ldg(P.col_ptr + n + 1);
+          if (e0 + j < e1) {
+            const int m = __ldg(P.col_idx + e0 + j);
+            atomicXor(&sbits[m >> 5], 1u << (m & 31));
+          }
+        }
+      }
+      __syncthreads();
+
+      // ---- refresh signs from the new syndrome; syndrome weight ----
+      for (int kk = 0; kk < nKm; ++kk) {
+        const int m = tid + kk * T;
+        const bool ok = m < M;
+        const bool s = ok && ((sbits[m >> 5] >> (m & 31)) & 1u);
+        if (ok) {
+          const double a1 = fabs(chk1[m]);
+          const double v1 = s ? a1 : -a1;
+          chk1[m] = v1;
+          if (CIRC && fastp) chk1[m + N] = v1;
+          const double a2 = fabs(chk2[m]);
+          chk2[m] = s ? a2 : -a2;
+        }
+        const uint32_t b = __ballot_sync(FULL_MASK, s);
+        if (lane == 0 && b) atomicAdd(&misc[S_SWT], __popc(b));
+      }
+      k += 1;
+      __syncthreads();
+    }
+
+    // ---------------- outputs ----------------------------------------------------
+    if (tid == 0) misc[S_BITERR] = 0;
+    __syncthreads();
+    {
+      int be = 0;
+      for (int w2 = tid; w2 < zw; w2 += T) {
+        const uint32_t z = zbits[w2];
+        if (P.z_bits) P.z_bits[f * P.z_ld + w2] = z;
+        const uint32_t c = P.codeword_bits ? __ldg(P.codeword_bits + w2) : 0u;
+        be += __popc(z ^ c);
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) be += __shfl_xor_sync(FULL_MASK, be, off);
+      if (lane == 0 && be) atomicAdd(&misc[S_BITERR], be);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const int be = misc[S_BITERR];
+      const int flags = (conv ? FWBF_FLAG_CONVERGED : 0) | (stalled ? FWBF_FLAG_STALLED : 0) |
+                        (fastp ? 0 : FWBF_FLAG_ORDERED) | (misc[S_NONFIN] ? FWBF_FLAG_NONFINITE : 0);
+      if (P.iterations) P.iterations[f] = k;
+      if (P.flags) P.flags[f] = (uint8_t)flags;
+      if (P.flips_total) P.flips_total[f] = (int)flips_total;
+      if (P.bit_errors) P.bit_errors[f] = be;
+      if (P.iter_hist) atomicAdd((unsigned long long *)&P.iter_hist[k], 1ull);
+      if (be && P.batch_word_err) atomicAdd(&P.batch_word_err[f / P.batch_frames], 1);
+      c_frames += 1;
+      c_biterr += be;
+      c_worderr += be ? 1 : 0;
+      c_iters += k;
+      c_flips += flips_total;
+      c_stalls += stalled;
+      c_conv += conv;
+      c_ordered += fastp ? 0 : 1;
+      c_edges += (long long)P.n_edges * k;
+      misc[S_NONFIN] = 0;
+    }
+  }
+
+  if (tid == 0 && P.counters && c_frames) {
+    unsigned long long *c = (unsigned long long *)P.counters;
+    atomicAdd(c + FWBF_CNT_FRAMES, (unsigned long long)c_frames);
+    atomicAdd(c + FWBF_CNT_BIT_ERRORS, (unsigned long long)c_biterr);
+    atomicAdd(c + FWBF_CNT_WORD_ERRORS, (unsigned long long)c_worderr);
+    atomicAdd(c + FWBF_CNT_ITER_SUM, (unsigned long long)c_iters);
+    atomicAdd(c + FWBF_CNT_FLIP_SUM, (unsigned long long)c_flips);
+    atomicAdd(c + FWBF_CNT_STALLS, (unsigned long long)c_stalls);
+    atomicAdd(c + FWBF_CNT_CONVERGED, (unsigned long long)c_conv);
+    atomicAdd(c + FWBF_CNT_ORDERED_FRAMES, (unsigned long long)c_ordered);
+    atomicAdd(c + FWBF_CNT_EDGE_VISITS, (unsigned long long)c_edges);
+  }
+}
+
+// explicit instantiations used by the launcher
+#define FWBF_INST(YT, C, KC, TB) template __global__ void decode_kernel<YT, C, KC, TB>(const __grid_constant__ KParams);
+FWBF_FAST_CONFIGS(FWBF_INST)
+FWBF_INST(double, true, 1, 0)
+FWBF_INST(float, false, 1, 0)
+FWBF_INST(double, false, 1, 0)
+
+} // namespace fwbf

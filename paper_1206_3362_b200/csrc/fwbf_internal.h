@@ -1,0 +1,64 @@
+// fwbf_internal.h -- kernel parameter block shared by the launcher and kernels.
+#pragma once
+#include <stdint.h>
+
+namespace fwbf {
+
+constexpr int kMaxCircWeight = 64; // circulant offsets kept in the parameter block
+
+// Guarded-path kernel shapes (threads TB, columns per thread KC): TB*KC >= n.
+#define FWBF_FAST_CONFIGS(X) \
+  X(float, true, 2, 128)     \
+  X(float, true, 4, 256)     \
+  X(float, true, 4, 512)     \
+  X(float, true, 8, 512)     \
+  X(float, true, 8, 1024)
+
+struct KParams {
+  // ---- code (H) ----
+  int n, m;          // columns (bits), rows (checks)
+  int w;             // circulant weight, 0 for explicit codes
+  int dv_max;        // max column weight
+  long long n_edges;
+  int off[kMaxCircWeight];  // circulant first-row columns c_j, ascending
+  int dneg[kMaxCircWeight]; // sorted (n - c_j) mod n, ascending (ordered column walk)
+  const uint8_t *i0tab;     // circulant: first dneg index of column n's ascending walk
+  const int16_t *offpos;    // circulant: offpos[d] = j if c_j == d else -1
+  const int *row_ptr, *row_idx; // CSR, sorted columns
+  const int *col_ptr, *col_idx; // CSC, ascending checks
+  // ---- decoder config ----
+  int alg, wmode, kmax, lam, p, stall, mlp_thr, force_ordered;
+  double alpha;
+  int nblocks;
+  // ---- input ----
+  const void *y;
+  long long ld;
+  long long batch;
+  // noise (awgn mode)
+  unsigned long long seed;
+  long long first_frame;
+  double sigma;
+  // ---- outputs ----
+  uint32_t *z_bits;
+  long long z_ld;
+  int *iterations;
+  uint8_t *flags;
+  int *flips_total;
+  int *bit_errors;
+  int *fliplog;
+  int *fliplog_counts;
+  long long fliplog_stride;
+  long long *counters;
+  long long *iter_hist;
+  int *batch_word_err;
+  int batch_frames;
+  const uint32_t *codeword_bits;
+  unsigned int *work_counter;
+  // ---- shared memory layout (byte offsets) ----
+  int off_y, off_e, off_chk1, off_chk2, off_amin, off_amask, off_sbits, off_zbits;
+  int off_blkv, off_blki, off_flips, off_offs, off_red, off_misc;
+  int smem_bytes;
+  int alias_y; // metric buffer overlays y; alpha*|y| re-read from global
+};
+
+} // namespace fwbf
