@@ -44,6 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     srcs = [os.path.join(HERE, s) for s in SOURCES if os.path.exists(os.path.join(HERE, s))]
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-cudart", "static", "-fmad=false", "--expt-relaxed-constexpr",
+           "-static-global-template-stub=false",
            "-I", os.path.join(REPO, "include"), "-I", HERE,
            "-Xptxas", "-v" if verbose else "-O3",
            "-o", LIB + ".tmp", *srcs]

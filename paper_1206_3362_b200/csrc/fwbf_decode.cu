@@ -74,7 +74,7 @@ __device__ __forceinline__ YT load_y(const KParams &P, long long f, int n) {
 //   KC   : columns per thread on the guarded path (register accumulators)
 // ---------------------------------------------------------------------------
 template <typename YT, bool CIRC, int KC, int TB>
-__global__ void __launch_bounds__(TB ? TB : 1024, 1)
+__global__ void __launch_bounds__(TB ? TB : 1024, 1024 / (TB ? TB : 1024))
 decode_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
@@ -117,7 +117,6 @@ decode_kernel(const __grid_constant__ KParams P) {
             c_stalls = 0, c_conv = 0, c_ordered = 0, c_edges = 0;
 
   const int zw = (N + 31) >> 5;
-  const int sw = (M + 31) >> 5;
   const int nKy = (N + T - 1) / T; // rounds over columns
   const int nKm = (M + T - 1) / T; // rounds over checks
 

@@ -285,6 +285,8 @@ def decode_batch(h, y, cfg: DecoderConfig, algorithm: str = "fwbf", *, flip_log:
     if y.shape[1] != dc.n and y.stride(0) != y.shape[1]:
         y = y.contiguous()
     B, ld = int(y.shape[0]), int(y.stride(0))
+    if B <= 1:
+        ld = int(y.shape[1])  # a single row may carry any (even zero) row stride
     p = make_params(cfg, algorithm, force_ordered)
     L = nat.lib()
     zw = (dc.n + 31) // 32
