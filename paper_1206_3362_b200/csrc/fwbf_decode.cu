@@ -102,7 +102,7 @@ decode_kernel(const __grid_constant__ KParams P) {
   int *misc = reinterpret_cast<int *>(smem_raw + P.off_misc);
   float *redf = reinterpret_cast<float *>(smem_raw + P.off_misc + 16 * 4);
   // misc slots
-  enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR, S_STOP };
+  enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR, S_NA };
 
   const int W = P.w;                 // circulant weight (0 explicit)
   const int aw = (W > 32) ? 2 : 1;   // amask words per column
@@ -155,7 +155,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     }
     nonfin = __any_sync(FULL_MASK, nonfin);
     if (lane == 0) { redf[warp] = lmin; redf[32 + warp] = lmax; if (nonfin) misc[S_NONFIN] = 1; }
-    if (tid == 0) { misc[S_SWT] = 0; }
+    if (tid == 0) { misc[S_SWT] = 0; misc[S_NA] = 0; }
     __syncthreads();
     if (tid == 0) {
       float mn = INFINITY, mx = 0.f;
@@ -236,6 +236,35 @@ decode_kernel(const __grid_constant__ KParams P) {
     }
     __syncthreads();
 
+    // ---------------- guarded path: columns holding a check's argmin -----------
+    // Column n's metric is sum_j sgn*min1[n - c_j] plus, for every check whose
+    // argmin is n, sgn*(min2 - min1).  Only ~12% of columns hold any argmin
+    // (but those hold many), so the corrections are computed per iteration by
+    // one thread per such column (list `alist`, aliasing the unused amin array)
+    // and parked in Ebuf[n], where the main gather picks them up.
+    int *alist = amin;
+    uint32_t aflag = 0; // bit q: column tid + q*T holds an argmin
+    const bool corr_on = CIRC && fastp && P.wmode == FWBF_WEIGHTS_IMWBF;
+    if (corr_on) {
+      for (int kk = 0; kk < nKy; ++kk) {
+        const int n = tid + kk * T;
+        bool has = false;
+        if (n < N) {
+          uint32_t a = amask[n * aw];
+          if (aw > 1) a |= amask[n * aw + 1];
+          has = a != 0u;
+        }
+        const uint32_t b = __ballot_sync(FULL_MASK, has);
+        int base = 0;
+        if (lane == 0 && b) base = atomicAdd(&misc[S_NA], __popc(b));
+        base = __shfl_sync(FULL_MASK, base, 0);
+        if (has) alist[base + __popc(b & ((1u << lane) - 1u))] = n;
+        if (has && kk < KC) aflag |= 1u << kk;
+      }
+      __syncthreads();
+    }
+    const int nA = corr_on ? misc[S_NA] : 0;
+
     // ---------------- iterations -----------------------------------------------
     int k = 0;
     int conv = 0, stalled = 0;
@@ -246,15 +275,39 @@ decode_kernel(const __grid_constant__ KParams P) {
       if (swt == 0) { conv = 1; break; }
       if (k >= P.kmax) break;
 
+      // ---- argmin corrections (guarded path) ----
+      if (corr_on) {
+        for (int t = tid; t < nA; t += T) {
+          const int n = alist[t];
+          double corr = 0.0;
+          for (int w2 = 0; w2 < aw; ++w2) {
+            uint32_t mk = amask[n * aw + w2];
+            while (mk) {
+              const int j = (__ffs(mk) - 1) + 32 * w2;
+              mk &= mk - 1;
+              int m = n - offs_s[j];
+              if (m < 0) m += N;
+              corr = __dadd_rn(corr, chk2[m]);
+            }
+          }
+          Ebuf[n] = corr;
+        }
+        __syncthreads();
+      }
+
       // ---- Eq.(1) metric for every bit -> Ebuf ----
       if (CIRC && fastp) {
         // chk1 holds sgn*min1 twice ([0,N) and [N,2N)) plus KC*T-N zero pad, so
         // column n reads check (n - c_j) mod N at chk1[n + N - c_j] with no wrap
         // test: one uniform add per j, then KC immediate-offset LDS.64 + DADD.
+        // Exact in any order under the guard, so the argmin correction goes first.
         double acc[KC];
         int nk[KC];
 #pragma unroll
-        for (int q = 0; q < KC; ++q) { nk[q] = tid + q * T; acc[q] = 0.0; }
+        for (int q = 0; q < KC; ++q) {
+          nk[q] = tid + q * T;
+          acc[q] = ((aflag >> q) & 1u) ? Ebuf[nk[q]] : 0.0;
+        }
         const double *src = chk1 + N + tid;
         for (int j = 0; j < W; ++j) {
           const double *sj = src - P.off[j];
@@ -265,16 +318,6 @@ decode_kernel(const __grid_constant__ KParams P) {
         for (int q = 0; q < KC; ++q) {
           const int n = nk[q];
           if (n < N) {
-            for (int w2 = 0; w2 < aw; ++w2) {
-              uint32_t mk = amask[n * aw + w2];
-              while (mk) {
-                const int j = (__ffs(mk) - 1) + 32 * w2;
-                mk &= mk - 1;
-                int m = n - offs_s[j];
-                if (m < 0) m += N;
-                acc[q] = __dadd_rn(acc[q], chk2[m]);
-              }
-            }
             const double ay = P.alias_y ? fabs((double)load_y<YT>(P, f, n)) : fabs((double)ybuf[n]);
             Ebuf[n] = __dsub_rn(acc[q], __dmul_rn(P.alpha, ay));
           }
@@ -462,25 +505,20 @@ decode_kernel(const __grid_constant__ KParams P) {
         atomicXor(&zbits[n >> 5], 1u << (n & 31));
       }
       if (CIRC) {
-        const int tot = F * W;
-        for (int t = tid; t < tot; t += T) {
-          const int fi = t / W;
-          const int j = t - fi * W;
+        for (int fi = warp; fi < F; fi += nwarps) {
           const int n = flips[fi];
-          int m = n - offs_s[j];
-          if (m < 0) m += N;
-          atomicXor(&sbits[m >> 5], 1u << (m & 31));
+          for (int j = lane; j < W; j += 32) {
+            int m = n - offs_s[j];
+            if (m < 0) m += N;
+            atomicXor(&sbits[m >> 5], 1u << (m & 31));
+          }
         }
       } else {
-        const int dv = P.dv_max;
-        const int tot = F * dv;
-        for (int t = tid; t < tot; t += T) {
-          const int fi = t / dv;
-          const int j = t - fi * dv;
+        for (int fi = warp; fi < F; fi += nwarps) {
           const int n = flips[fi];
           const int e0 = __ldg(P.col_ptr + n), e1 = __ldg(P.col_ptr + n + 1);
-          if (e0 + j < e1) {
-            const int m = __ldg(P.col_idx + e0 + j);
+          for (int e = e0 + lane; e < e1; e += 32) {
+            const int m = __ldg(P.col_idx + e);
             atomicXor(&sbits[m >> 5], 1u << (m & 31));
           }
         }
