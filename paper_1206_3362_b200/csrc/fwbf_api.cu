@@ -272,9 +272,20 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
   P.off_y = take(n * ysize);
   P.off_e = take(n * 8);
   // guarded path: doubled signed min1 plus zero pad up to the threads' column cover
-  P.off_chk1 = take((circ ? 2 * n + std::max(0, cover - n) : m) * 8);
-  P.off_chk2 = take(m * 8);
-  P.off_amin = take(m * 4);
+  // check records: guarded path (circulant) = two doubled arrays sgn*min1,
+  // sgn*min2 with a pad up to the threads' column cover; ordered path =
+  // chk1[m], chk2[m], amin[m] inside the same region.
+  if (circ) {
+    const int dbl = 2 * n + std::max(0, cover - n);
+    const int r = take(2 * dbl * 8);
+    P.off_chk1 = r;
+    P.off_chk2 = r + dbl * 8;
+    P.off_amin = P.off_chk2 + align16(m * 8); // ordered path only; inside chk2's upper half
+  } else {
+    P.off_chk1 = take(m * 8);
+    P.off_chk2 = take(m * 8);
+    P.off_amin = take(m * 4);
+  }
   P.off_amask = take(circ ? n * aw * 4 : 4);
   P.off_sbits = take(sw * 4);
   P.off_zbits = take(zw * 4);

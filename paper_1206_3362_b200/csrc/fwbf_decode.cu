@@ -61,6 +61,22 @@ struct Smem {
   template <typename T> __device__ T *at(int off) const { return reinterpret_cast<T *>(base + off); }
 };
 
+// One column-slot step of the guarded gather: select the min1 or min2 array
+// by the argmin mask bit, load with the slot's compile-time offset Q*TB*8.
+template <int Q, int KC, int TB> struct GatherQ {
+  static __device__ __forceinline__ void run(double (&acc)[KC], const uint32_t (&mk)[KC], uint32_t bit,
+                                             uint32_t a1, uint32_t a2) {
+    const uint32_t a = (mk[Q] & bit) ? a2 : a1;
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(Q * TB * 8));
+    acc[Q] = __dadd_rn(acc[Q], v);
+    GatherQ<Q + 1, KC, TB>::run(acc, mk, bit, a1, a2);
+  }
+};
+template <int KC, int TB> struct GatherQ<KC, KC, TB> {
+  static __device__ __forceinline__ void run(double (&)[KC], const uint32_t (&)[KC], uint32_t, uint32_t, uint32_t) {}
+};
+
 template <typename YT>
 __device__ __forceinline__ YT load_y(const KParams &P, long long f, int n) {
   const YT *y = reinterpret_cast<const YT *>(P.y);
@@ -88,7 +104,7 @@ decode_kernel(const __grid_constant__ KParams P) {
   YT *ybuf = reinterpret_cast<YT *>(smem_raw + P.off_y);
   double *Ebuf = reinterpret_cast<double *>(smem_raw + P.off_e);
   double *chk1 = reinterpret_cast<double *>(smem_raw + P.off_chk1); // min1 (signed); doubled on the guarded path
-  double *chk2 = reinterpret_cast<double *>(smem_raw + P.off_chk2); // min2 (ordered) or min2-min1 (guarded), signed
+  double *chk2 = reinterpret_cast<double *>(smem_raw + P.off_chk2); // min2 (signed); doubled on the guarded path
   int *amin = reinterpret_cast<int *>(smem_raw + P.off_amin);        // ordered path argmin column
   uint32_t *amask = reinterpret_cast<uint32_t *>(smem_raw + P.off_amask); // guarded: per-column argmin j-mask
   uint32_t *sbits = reinterpret_cast<uint32_t *>(smem_raw + P.off_sbits);
@@ -102,7 +118,7 @@ decode_kernel(const __grid_constant__ KParams P) {
   int *misc = reinterpret_cast<int *>(smem_raw + P.off_misc);
   float *redf = reinterpret_cast<float *>(smem_raw + P.off_misc + 16 * 4);
   // misc slots
-  enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR, S_NA };
+  enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR };
 
   const int W = P.w;                 // circulant weight (0 explicit)
   const int aw = (W > 32) ? 2 : 1;   // amask words per column
@@ -155,7 +171,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     }
     nonfin = __any_sync(FULL_MASK, nonfin);
     if (lane == 0) { redf[warp] = lmin; redf[32 + warp] = lmax; if (nonfin) misc[S_NONFIN] = 1; }
-    if (tid == 0) { misc[S_SWT] = 0; misc[S_NA] = 0; }
+    if (tid == 0) { misc[S_SWT] = 0; }
     __syncthreads();
     if (tid == 0) {
       float mn = INFINITY, mx = 0.f;
@@ -218,14 +234,14 @@ decode_kernel(const __grid_constant__ KParams P) {
         if (CIRC && fastp) {
           chk1[m] = sg * d1;
           chk1[m + N] = sg * d1;
+          chk2[m] = sg * d2;
+          chk2[m + N] = sg * d2;
           if (P.wmode == FWBF_WEIGHTS_IMWBF) {
-            chk2[m] = sg * __dsub_rn(d2, d1); // exact: float32 operands
+            // column ac reads min2 at its local check index j (m = ac - c_j)
             int d = ac - m;
             if (d < 0) d += N;
             const int j = P.offpos[d];
             atomicOr(&amask[ac * aw + (j >> 5)], 1u << (j & 31));
-          } else {
-            chk2[m] = 0.0;
           }
         } else {
           chk1[m] = sg * d1;
@@ -236,34 +252,18 @@ decode_kernel(const __grid_constant__ KParams P) {
     }
     __syncthreads();
 
-    // ---------------- guarded path: columns holding a check's argmin -----------
-    // Column n's metric is sum_j sgn*min1[n - c_j] plus, for every check whose
-    // argmin is n, sgn*(min2 - min1).  Only ~12% of columns hold any argmin
-    // (but those hold many), so the corrections are computed per iteration by
-    // one thread per such column (list `alist`, aliasing the unused amin array)
-    // and parked in Ebuf[n], where the main gather picks them up.
-    int *alist = amin;
-    uint32_t aflag = 0; // bit q: column tid + q*T holds an argmin
-    const bool corr_on = CIRC && fastp && P.wmode == FWBF_WEIGHTS_IMWBF;
-    if (corr_on) {
-      for (int kk = 0; kk < nKy; ++kk) {
-        const int n = tid + kk * T;
-        bool has = false;
-        if (n < N) {
-          uint32_t a = amask[n * aw];
-          if (aw > 1) a |= amask[n * aw + 1];
-          has = a != 0u;
-        }
-        const uint32_t b = __ballot_sync(FULL_MASK, has);
-        int base = 0;
-        if (lane == 0 && b) base = atomicAdd(&misc[S_NA], __popc(b));
-        base = __shfl_sync(FULL_MASK, base, 0);
-        if (has) alist[base + __popc(b & ((1u << lane) - 1u))] = n;
-        if (has && kk < KC) aflag |= 1u << kk;
+    // ---------------- guarded path: per-column argmin masks into registers -----
+    // Bit j of am[q] says column tid + q*T is the argmin of its j-th check
+    // (m = n - c_j), i.e. reads min2 there instead of min1 (decoders.py:80-84).
+    uint32_t am[KC][2];
+    if (CIRC && fastp) {
+#pragma unroll
+      for (int q = 0; q < KC; ++q) {
+        const int n = tid + q * T;
+        am[q][0] = (n < N) ? amask[n * aw] : 0u;
+        am[q][1] = (n < N && aw > 1) ? amask[n * aw + 1] : 0u;
       }
-      __syncthreads();
     }
-    const int nA = corr_on ? misc[S_NA] : 0;
 
     // ---------------- iterations -----------------------------------------------
     int k = 0;
@@ -275,48 +275,39 @@ decode_kernel(const __grid_constant__ KParams P) {
       if (swt == 0) { conv = 1; break; }
       if (k >= P.kmax) break;
 
-      // ---- argmin corrections (guarded path) ----
-      if (corr_on) {
-        for (int t = tid; t < nA; t += T) {
-          const int n = alist[t];
-          double corr = 0.0;
-          for (int w2 = 0; w2 < aw; ++w2) {
-            uint32_t mk = amask[n * aw + w2];
-            while (mk) {
-              const int j = (__ffs(mk) - 1) + 32 * w2;
-              mk &= mk - 1;
-              int m = n - offs_s[j];
-              if (m < 0) m += N;
-              corr = __dadd_rn(corr, chk2[m]);
-            }
-          }
-          Ebuf[n] = corr;
-        }
-        __syncthreads();
-      }
-
       // ---- Eq.(1) metric for every bit -> Ebuf ----
       if (CIRC && fastp) {
-        // chk1 holds sgn*min1 twice ([0,N) and [N,2N)) plus KC*T-N zero pad, so
-        // column n reads check (n - c_j) mod N at chk1[n + N - c_j] with no wrap
-        // test: one uniform add per j, then KC immediate-offset LDS.64 + DADD.
-        // Exact in any order under the guard, so the argmin correction goes first.
+        // chk1/chk2 hold sgn*min1 / sgn*min2 twice ([0,N) and [N,2N)) plus a
+        // KC*T-N pad, so column n reads check (n - c_j) mod N at index
+        // n + N - c_j with no wrap test: per j one uniform offset, then per
+        // column a mask test, an address select, one LDS.64 and one DADD.
+        // The sum is exact in any order under the guard.
         double acc[KC];
-        int nk[KC];
+#pragma unroll
+        for (int q = 0; q < KC; ++q) acc[q] = 0.0;
+        const uint32_t s1 = (uint32_t)__cvta_generic_to_shared(chk1 + N + tid);
+        const uint32_t d21 = (uint32_t)(P.off_chk2 - P.off_chk1);
+        uint32_t mk[KC];
+#pragma unroll
+        for (int q = 0; q < KC; ++q) mk[q] = am[q][0];
+        const int w0 = W < 32 ? W : 32;
+#pragma unroll 2
+        for (int j = 0; j < w0; ++j) {
+          const uint32_t a1 = s1 - 8u * (uint32_t)P.off[j];
+          GatherQ<0, KC, TB>::run(acc, mk, 1u << j, a1, a1 + d21);
+        }
+        if (W > 32) {
+#pragma unroll
+          for (int q = 0; q < KC; ++q) mk[q] = am[q][1];
+#pragma unroll 2
+          for (int j = 32; j < W; ++j) {
+            const uint32_t a1 = s1 - 8u * (uint32_t)P.off[j];
+            GatherQ<0, KC, TB>::run(acc, mk, 1u << (j - 32), a1, a1 + d21);
+          }
+        }
 #pragma unroll
         for (int q = 0; q < KC; ++q) {
-          nk[q] = tid + q * T;
-          acc[q] = ((aflag >> q) & 1u) ? Ebuf[nk[q]] : 0.0;
-        }
-        const double *src = chk1 + N + tid;
-        for (int j = 0; j < W; ++j) {
-          const double *sj = src - P.off[j];
-#pragma unroll
-          for (int q = 0; q < KC; ++q) acc[q] = __dadd_rn(acc[q], sj[q * T]);
-        }
-#pragma unroll
-        for (int q = 0; q < KC; ++q) {
-          const int n = nk[q];
+          const int n = tid + q * T;
           if (n < N) {
             const double ay = P.alias_y ? fabs((double)load_y<YT>(P, f, n)) : fabs((double)ybuf[n]);
             Ebuf[n] = __dsub_rn(acc[q], __dmul_rn(P.alpha, ay));
@@ -534,9 +525,10 @@ decode_kernel(const __grid_constant__ KParams P) {
           const double a1 = fabs(chk1[m]);
           const double v1 = s ? a1 : -a1;
           chk1[m] = v1;
-          if (CIRC && fastp) chk1[m + N] = v1;
           const double a2 = fabs(chk2[m]);
-          chk2[m] = s ? a2 : -a2;
+          const double v2 = s ? a2 : -a2;
+          chk2[m] = v2;
+          if (CIRC && fastp) { chk1[m + N] = v1; chk2[m + N] = v2; }
         }
         const uint32_t b = __ballot_sync(FULL_MASK, s);
         if (lane == 0 && b) atomicAdd(&misc[S_SWT], __popc(b));
