@@ -387,6 +387,14 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
                            : (const void *)fwbf::decode_kernel<double, false, 1, 0>;
   }
   layout(c, p, (int)sizeof(YT), circ, T * kc, P);
+  {
+    int tpb = 1;
+    int pcap = 1;
+    while (pcap < P.p) pcap <<= 1;
+    while (tpb < 32 && tpb < pcap && (long long)P.nblocks * tpb * 2 <= T) tpb <<= 1;
+    P.log2_tpb = 0;
+    while ((1 << P.log2_tpb) < tpb) ++P.log2_tpb;
+  }
   if (P.smem_bytes > c->smem_optin) {
     // Alias the metric buffer over the y buffer: after init y is only needed
     // for alpha*|y|, which the kernel then re-reads from global memory.

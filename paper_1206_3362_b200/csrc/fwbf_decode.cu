@@ -171,7 +171,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     }
     nonfin = __any_sync(FULL_MASK, nonfin);
     if (lane == 0) { redf[warp] = lmin; redf[32 + warp] = lmax; if (nonfin) misc[S_NONFIN] = 1; }
-    if (tid == 0) { misc[S_SWT] = 0; }
+    if (tid == 0) { misc[S_SWT] = 0; misc[S_F] = 0; }
     __syncthreads();
     if (tid == 0) {
       float mn = INFINITY, mx = 0.f;
@@ -276,6 +276,7 @@ decode_kernel(const __grid_constant__ KParams P) {
       if (k >= P.kmax) break;
 
       // ---- Eq.(1) metric for every bit -> Ebuf ----
+      if (tid == 0) misc[S_F] = 0; // last read before the previous refresh barrier
       if (CIRC && fastp) {
         // chk1/chk2 hold sgn*min1 / sgn*min2 twice ([0,N) and [N,2N)) plus a
         // KC*T-N pad, so column n reads check (n - c_j) mod N at index
@@ -341,58 +342,85 @@ decode_kernel(const __grid_constant__ KParams P) {
       }
       __syncthreads();
 
-      // ---- selection ----
+      // ---- selection (+ fused flips for FWBF) ----
+      if (tid == 0) misc[S_SWT] = 0; // every thread read it at the loop top (before the E barrier)
+      int F = 0;
+      bool applied = false;
       if (P.alg == FWBF_ALG_FWBF) {
+        // Groups of TPB = 2^log2_tpb threads own one p-block each: strided scan
+        // (ascending per thread, strict >), butterfly argmax in the group, then
+        // the group applies its flip when the block maximum is > 0
+        // (decoders.py:156-167, :181-183).  misc[S_F] counts the flips.
         const int p = P.p;
         const int nb = P.nblocks;
-        if (p <= 32) {
-          const int G = 32 / p;
-          const int g = lane / p, o = lane - g * p;
-          const int tasks = (nb + G - 1) / G;
-          for (int t = warp; t < tasks; t += nwarps) {
-            const int b = t * G + g;
-            const int n = b * p + o;
-            const bool ok = (g < G) && (b < nb) && (n < N);
-            double v = ok ? Ebuf[n] : -dinf();
-            int i = ok ? n : 0x7fffffff;
-#pragma unroll
-            for (int off = 16; off; off >>= 1) {
-              const double v2 = __shfl_down_sync(FULL_MASK, v, off);
-              const int i2 = __shfl_down_sync(FULL_MASK, i, off);
-              if (o + off < p) amax_combine(v, i, v2, i2);
+        const int lt = P.log2_tpb;
+        const int TPB = 1 << lt;
+        const int grp = tid >> lt, sub = tid & (TPB - 1), gpc = T >> lt;
+        const int rounds = (nb + gpc - 1) / gpc;
+        for (int r = 0; r < rounds; ++r) {
+          const int b = r * gpc + grp;
+          const bool ok = b < nb;
+          double v = -dinf();
+          int i = 0x7fffffff;
+          if (ok) {
+            const int base = b * p;
+            const int lim = min(p, N - base);
+            for (int o = sub; o < lim; o += TPB) {
+              const double e = Ebuf[base + o];
+              if (e > v) { v = e; i = base + o; }
             }
-            if (o == 0 && g < G && b < nb) { blk_v[b] = v; blk_i[b] = i; }
           }
-        } else {
-          for (int b = warp; b < nb; b += nwarps) {
-            double v = -dinf();
-            int i = 0x7fffffff;
-            for (int j = lane; j < p; j += 32) {
-              const int n = b * p + j;
-              if (n < N) amax_combine(v, i, Ebuf[n], n);
+          for (int off = TPB >> 1; off; off >>= 1) {
+            const double v2 = __shfl_xor_sync(FULL_MASK, v, off);
+            const int i2 = __shfl_xor_sync(FULL_MASK, i, off);
+            amax_combine(v, i, v2, i2);
+          }
+          if (ok) {
+            if (sub == 0) { blk_v[b] = v; blk_i[b] = i; }
+            if (v > 0.0) {
+              if (sub == 0) {
+                atomicXor(&zbits[i >> 5], 1u << (i & 31));
+                atomicAdd(&misc[S_F], 1);
+              }
+              if (CIRC) {
+                for (int j = sub; j < W; j += TPB) {
+                  int m = i - offs_s[j];
+                  if (m < 0) m += N;
+                  atomicXor(&sbits[m >> 5], 1u << (m & 31));
+                }
+              } else {
+                const int e1 = __ldg(P.col_ptr + i + 1);
+                for (int e = __ldg(P.col_ptr + i) + sub; e < e1; e += TPB) {
+                  const int m = __ldg(P.col_idx + e);
+                  atomicXor(&sbits[m >> 5], 1u << (m & 31));
+                }
+              }
             }
-            warp_amax(v, i);
-            if (lane == 0) { blk_v[b] = v; blk_i[b] = i; }
           }
         }
         __syncthreads();
-        if (warp == 0) {
-          int cnt = 0;
-          double gv = -dinf();
-          int gi = 0x7fffffff;
-          for (int base = 0; base < nb; base += 32) {
-            const int b = base + lane;
-            double v = -dinf();
-            int i = 0x7fffffff;
-            if (b < nb) { v = blk_v[b]; i = blk_i[b]; }
-            amax_combine(gv, gi, v, i);
-            const bool pos = (b < nb) && (v > 0.0);
-            const uint32_t msk = __ballot_sync(FULL_MASK, pos);
-            if (pos) flips[cnt + __popc(msk & ((1u << lane) - 1u))] = i;
-            cnt += __popc(msk);
+        F = misc[S_F];
+        if (F > 0) {
+          applied = true;
+          if (P.fliplog && warp == 0) { // ascending = block order
+            int cnt = 0;
+            for (int base = 0; base < nb; base += 32) {
+              const int bb = base + lane;
+              const bool pos = bb < nb && blk_v[bb] > 0.0;
+              const uint32_t msk = __ballot_sync(FULL_MASK, pos);
+              if (pos) P.fliplog[f * P.fliplog_stride + logpos + cnt + __popc(msk & ((1u << lane) - 1u))] = blk_i[bb];
+              cnt += __popc(msk);
+            }
+            if (lane == 0) P.fliplog_counts[f * P.kmax + k] = F;
           }
-          warp_amax(gv, gi);
-          if (lane == 0) { misc[S_F] = cnt; misc[S_GBEST] = gi; }
+        } else {
+          if (warp == 0) {
+            double gv = -dinf();
+            int gi = 0x7fffffff;
+            for (int bb = lane; bb < nb; bb += 32) amax_combine(gv, gi, blk_v[bb], blk_i[bb]);
+            warp_amax(gv, gi);
+            if (lane == 0) { misc[S_GBEST] = gi; flips[0] = gi; }
+          }
         }
       } else if (P.alg == FWBF_ALG_IMWBF) {
         double v = -dinf();
@@ -407,6 +435,8 @@ decode_kernel(const __grid_constant__ KParams P) {
           warp_amax(v, i);
           if (lane == 0) { misc[S_F] = 1; misc[S_GBEST] = i; flips[0] = i; }
         }
+        __syncthreads();
+        F = misc[S_F];
       } else { // MLP: lambda rounds of CTA argmax with exclusion, then ascending sort
         // selected indices are marked in the E buffer by overwriting with -inf;
         // their values are kept in blk_v/blk_i (sized lam on the host).
@@ -425,14 +455,13 @@ decode_kernel(const __grid_constant__ KParams P) {
               blk_v[r] = v;
               blk_i[r] = i;
               Ebuf[i] = -dinf();
-              if (r == 0) misc[S_GBEST] = i;
+              if (r == 0) { misc[S_GBEST] = i; flips[0] = i; }
             }
           }
           __syncthreads();
         }
         // flips = selected (and positive when thresholded), ascending: mark in a
-        // bitmap over columns (reuse amask-free scratch: the zbits-sized area in
-        // blk_i beyond lam), then compact in index order.
+        // bitmap over columns (scratch after blk_i[lam]), then compact in order.
         uint32_t *sel = reinterpret_cast<uint32_t *>(blk_i + P.lam);
         for (int w2 = tid; w2 < zw; w2 += T) sel[w2] = 0u;
         __syncthreads();
@@ -466,55 +495,53 @@ decode_kernel(const __grid_constant__ KParams P) {
           }
           if (lane == 0) misc[S_F] = cnt;
         }
+        __syncthreads();
+        F = misc[S_F];
       }
-      __syncthreads();
 
-      int F = misc[S_F];
       if (F == 0) {
+        // nothing selected while the syndrome is nonzero (decoders.py:214-222)
         stalled = 1;
         if (P.stall == FWBF_STALL_TERMINATE) {
           if (tid == 0 && P.fliplog_counts) P.fliplog_counts[f * P.kmax + k] = 0;
           k += 1;
           break;
         }
-        if (tid == 0) flips[0] = misc[S_GBEST];
-        F = 1;
+        F = 1; // flips[0] = global argmax, written above
         __syncthreads();
       }
-      // flip log
-      if (P.fliplog) {
-        for (int t = tid; t < F; t += T) P.fliplog[f * P.fliplog_stride + logpos + t] = flips[t];
-        if (tid == 0) P.fliplog_counts[f * P.kmax + k] = F;
+      if (!applied) {
+        if (P.fliplog) {
+          for (int t = tid; t < F; t += T) P.fliplog[f * P.fliplog_stride + logpos + t] = flips[t];
+          if (tid == 0) P.fliplog_counts[f * P.kmax + k] = F;
+        }
+        for (int t = tid; t < F; t += T) {
+          const int n = flips[t];
+          atomicXor(&zbits[n >> 5], 1u << (n & 31));
+        }
+        if (CIRC) {
+          for (int fi = warp; fi < F; fi += nwarps) {
+            const int n = flips[fi];
+            for (int j = lane; j < W; j += 32) {
+              int m = n - offs_s[j];
+              if (m < 0) m += N;
+              atomicXor(&sbits[m >> 5], 1u << (m & 31));
+            }
+          }
+        } else {
+          for (int fi = warp; fi < F; fi += nwarps) {
+            const int n = flips[fi];
+            const int e0 = __ldg(P.col_ptr + n), e1 = __ldg(P.col_ptr + n + 1);
+            for (int e = e0 + lane; e < e1; e += 32) {
+              const int m = __ldg(P.col_idx + e);
+              atomicXor(&sbits[m >> 5], 1u << (m & 31));
+            }
+          }
+        }
+        __syncthreads();
       }
       logpos += F;
       flips_total += F;
-
-      // ---- apply flips: z and syndrome toggles ----
-      if (tid == 0) misc[S_SWT] = 0;
-      for (int t = tid; t < F; t += T) {
-        const int n = flips[t];
-        atomicXor(&zbits[n >> 5], 1u << (n & 31));
-      }
-      if (CIRC) {
-        for (int fi = warp; fi < F; fi += nwarps) {
-          const int n = flips[fi];
-          for (int j = lane; j < W; j += 32) {
-            int m = n - offs_s[j];
-            if (m < 0) m += N;
-            atomicXor(&sbits[m >> 5], 1u << (m & 31));
-          }
-        }
-      } else {
-        for (int fi = warp; fi < F; fi += nwarps) {
-          const int n = flips[fi];
-          const int e0 = __ldg(P.col_ptr + n), e1 = __ldg(P.col_ptr + n + 1);
-          for (int e = e0 + lane; e < e1; e += 32) {
-            const int m = __ldg(P.col_idx + e);
-            atomicXor(&sbits[m >> 5], 1u << (m & 31));
-          }
-        }
-      }
-      __syncthreads();
 
       // ---- refresh signs from the new syndrome; syndrome weight ----
       for (int kk = 0; kk < nKm; ++kk) {

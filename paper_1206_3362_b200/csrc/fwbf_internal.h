@@ -30,6 +30,7 @@ struct KParams {
   int alg, wmode, kmax, lam, p, stall, mlp_thr, force_ordered;
   double alpha;
   int nblocks;
+  int log2_tpb; // FWBF: threads per block-argmax group = 2^log2_tpb
   // ---- input ----
   const void *y;
   long long ld;
