@@ -276,7 +276,9 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
   // sgn*min2 with a pad up to the threads' column cover; ordered path =
   // chk1[m], chk2[m], amin[m] inside the same region.
   if (circ) {
-    const int dbl = 2 * n + std::max(0, cover - n);
+    // both doubled arrays; chk2 - chk1 is a multiple of 128 B so a lane that
+    // reads min2 instead of min1 hits the same banks (no extra wavefront)
+    const int dbl = (2 * n + std::max(0, cover - n) + 15) / 16 * 16;
     const int r = take(2 * dbl * 8);
     P.off_chk1 = r;
     P.off_chk2 = r + dbl * 8;
@@ -388,10 +390,12 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   }
   layout(c, p, (int)sizeof(YT), circ, T * kc, P);
   {
+    // FWBF block-argmax groups: odd p -> one thread per block (stride-p reads
+    // across lanes are bank-conflict free); power-of-two p -> min(p, 32)
+    // threads per block reading contiguously; otherwise one thread per block.
     int tpb = 1;
-    int pcap = 1;
-    while (pcap < P.p) pcap <<= 1;
-    while (tpb < 32 && tpb < pcap && (long long)P.nblocks * tpb * 2 <= T) tpb <<= 1;
+    const int pp = P.p;
+    if (pp > 1 && (pp & (pp - 1)) == 0) tpb = std::min(pp, 32);
     P.log2_tpb = 0;
     while ((1 << P.log2_tpb) < tpb) ++P.log2_tpb;
   }
