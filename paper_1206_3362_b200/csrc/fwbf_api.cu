@@ -395,7 +395,17 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     // threads per block reading contiguously; otherwise one thread per block.
     int tpb = 1;
     const int pp = P.p;
-    if (pp > 1 && (pp & (pp - 1)) == 0) tpb = std::min(pp, 32);
+    P.sel_spread = 0;
+    if (pp > 1 && (pp & (pp - 1)) == 0) {
+      tpb = std::min(pp, 32);
+    } else if (pp & 1) {
+      // largest power of two <= min(16, p) with all blocks in one round and
+      // the half-warps of the CTA divisible into groups of tpb
+      const int halfwarps = T / 16;
+      for (int t2 = 16; t2 >= 2; t2 >>= 1)
+        if (t2 <= pp && halfwarps % t2 == 0 && (long long)P.nblocks * t2 <= T) { tpb = t2; break; }
+      P.sel_spread = tpb > 1;
+    }
     P.log2_tpb = 0;
     while ((1 << P.log2_tpb) < tpb) ++P.log2_tpb;
   }

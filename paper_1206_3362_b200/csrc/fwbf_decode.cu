@@ -356,9 +356,17 @@ decode_kernel(const __grid_constant__ KParams P) {
         const int lt = P.log2_tpb;
         const int TPB = 1 << lt;
         const int grp = tid >> lt, sub = tid & (TPB - 1), gpc = T >> lt;
+        // odd p: the 16/TPB groups of a half-warp take blocks TPB apart, so their
+        // lanes' words land in distinct banks (p*TPB*i + s, i < 16/TPB, s < TPB)
+        int slot = grp;
+        if (P.sel_spread) {
+          const int hw = tid >> 4, half = 16 >> lt;
+          const int i = grp & (half - 1);
+          slot = (hw / TPB) * 16 + TPB * i + (hw % TPB);
+        }
         const int rounds = (nb + gpc - 1) / gpc;
         for (int r = 0; r < rounds; ++r) {
-          const int b = r * gpc + grp;
+          const int b = r * gpc + slot;
           const bool ok = b < nb;
           double v = -dinf();
           int i = 0x7fffffff;

@@ -31,6 +31,7 @@ struct KParams {
   double alpha;
   int nblocks;
   int log2_tpb; // FWBF: threads per block-argmax group = 2^log2_tpb
+  int sel_spread; // odd p: half-warp groups take blocks TPB apart (bank-conflict free)
   // ---- input ----
   const void *y;
   long long ld;
