@@ -269,9 +269,9 @@ decode_kernel(const __grid_constant__ KParams P) {
     // (decoders.py:80-84).  The main gather sums sgn*min1 for all columns; the
     // ~12% of columns holding an argmin get sum_j [bit j] sgn*(min2 - min1)
     // from a fixed-length (W) predicated loop, one thread per such column
-    // (compacted list `alist`, aliasing the unused amin array), parked in
+    // (compacted list `alist`), parked in
     // Ebuf[n] before the gather.  All sums are exact under the guard.
-    int *alist = amin;
+    int *alist = reinterpret_cast<int *>(smem_raw + P.off_alist);
     uint32_t aflag = 0; // bit q: column tid + q*T holds an argmin
     const bool corr_on = CIRC && fastp && P.wmode == FWBF_WEIGHTS_IMWBF;
     if (corr_on) {
