@@ -310,24 +310,40 @@ decode_kernel(const __grid_constant__ KParams P) {
       if (corr_on) {
         const uint32_t d21 = (uint32_t)(P.off_chk2 - P.off_chk1);
         const uint32_t c1 = (uint32_t)__cvta_generic_to_shared(chk1 + N);
-        for (int t = tid; t < nA; t += T) {
-          const int n = alist[t];
-          const uint32_t m0 = amask[n * aw];
-          const uint32_t m1 = aw > 1 ? amask[n * aw + 1] : 0u;
+        // two threads per argmin column (adjacent lanes), each W/2 checks,
+        // branch-free predicated loads in groups of 8, combined by one shuffle
+        const int hw = (W + 1) >> 1;
+        const int items = 2 * nA;
+        const int rounds = (items + T - 1) / T;
+        for (int r = 0; r < rounds; ++r) {
+          const int t = r * T + tid;
+          const bool ok = t < items;
+          const int n = ok ? alist[t >> 1] : 0;
+          const int j0 = (t & 1) * hw;
+          const int j1 = min(W, j0 + hw);
+          const uint32_t m0 = ok ? amask[n * aw] : 0u;
+          const uint32_t m1 = (ok && aw > 1) ? amask[n * aw + 1] : 0u;
           const uint32_t base = c1 + 8u * (uint32_t)n;
-          double corr = 0.0;
-#pragma unroll 4
-          for (int j = 0; j < W; ++j) {
-            const uint32_t mk = j < 32 ? m0 : m1;
-            if ((mk >> (j & 31)) & 1u) {
-              const uint32_t a = base - 8u * (uint32_t)P.off[j];
-              double v1, v2;
-              asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v1) : "r"(a));
-              asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v2) : "r"(a + d21));
-              corr = __dadd_rn(corr, __dsub_rn(v2, v1));
+          double ca = 0.0, cb = 0.0;
+          for (int j = j0; j < j1; j += 8) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int jj = j + u;
+              const uint32_t mk = jj < 32 ? m0 : m1;
+              const bool hit = jj < j1 && ((mk >> (jj & 31)) & 1u);
+              double v1 = 0.0, v2 = 0.0;
+              if (hit) {
+                const uint32_t a = base - 8u * (uint32_t)offs_s[jj];
+                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v1) : "r"(a));
+                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v2) : "r"(a + d21));
+              }
+              if (u & 1) cb = __dadd_rn(cb, __dsub_rn(v2, v1));
+              else ca = __dadd_rn(ca, __dsub_rn(v2, v1));
             }
           }
-          Ebuf[n] = corr;
+          double corr = __dadd_rn(ca, cb);
+          corr = __dadd_rn(corr, __shfl_xor_sync(FULL_MASK, corr, 1));
+          if (ok && !(t & 1)) Ebuf[n] = corr;
         }
         __syncthreads();
       }
