@@ -289,7 +289,6 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
     P.off_amin = take(m * 4);
   }
   P.off_amask = take(circ ? n * aw * 4 : 4);
-  P.off_alist = take(circ ? n * 4 : 4);
   P.off_sbits = take(sw * 4);
   P.off_zbits = take(zw * 4);
   P.off_blkv = take(nslots * 8);
@@ -417,7 +416,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     const int delta = (P.off_y + align16(c->n * 8)) - P.off_chk1;
     P.off_e = P.off_y;
     for (int *x : {&P.off_chk1, &P.off_chk2, &P.off_amin, &P.off_amask, &P.off_sbits, &P.off_zbits,
-                   &P.off_blkv, &P.off_blki, &P.off_flips, &P.off_offs, &P.off_red, &P.off_misc, &P.off_alist})
+                   &P.off_blkv, &P.off_blki, &P.off_flips, &P.off_offs, &P.off_red, &P.off_misc})
       *x += delta;
     P.smem_bytes += delta;
   }

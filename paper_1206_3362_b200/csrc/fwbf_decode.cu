@@ -73,18 +73,6 @@ template <int Q, int KC, int TB> struct GatherQ {
     GatherQ<Q + 1, KC, TB>::run(acc, mk, bit, a1, a2);
   }
 };
-// Plain slot step: every column of the thread reads sgn*min1 at its offset.
-template <int Q, int KC, int TB> struct GatherP {
-  static __device__ __forceinline__ void run(double (&acc)[KC], uint32_t a) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(Q * TB * 8));
-    acc[Q] = __dadd_rn(acc[Q], v);
-    GatherP<Q + 1, KC, TB>::run(acc, a);
-  }
-};
-template <int KC, int TB> struct GatherP<KC, KC, TB> {
-  static __device__ __forceinline__ void run(double (&)[KC], uint32_t) {}
-};
 template <int KC, int TB> struct GatherQ<KC, KC, TB> {
   static __device__ __forceinline__ void run(double (&)[KC], const uint32_t (&)[KC], uint32_t, uint32_t, uint32_t) {}
 };
@@ -130,7 +118,7 @@ decode_kernel(const __grid_constant__ KParams P) {
   int *misc = reinterpret_cast<int *>(smem_raw + P.off_misc);
   float *redf = reinterpret_cast<float *>(smem_raw + P.off_misc + 16 * 4);
   // misc slots
-  enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR, S_NA };
+  enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR };
 
   const int W = P.w;                 // circulant weight (0 explicit)
   const int aw = (W > 32) ? 2 : 1;   // amask words per column
@@ -264,37 +252,18 @@ decode_kernel(const __grid_constant__ KParams P) {
     }
     __syncthreads();
 
-    // ---------------- guarded path: columns holding a check's argmin -----------
-    // Column n reads min2 instead of min1 at every check whose argmin it is
-    // (decoders.py:80-84).  The main gather sums sgn*min1 for all columns; the
-    // ~12% of columns holding an argmin get sum_j [bit j] sgn*(min2 - min1)
-    // from a fixed-length (W) predicated loop, one thread per such column
-    // (compacted list `alist`), parked in
-    // Ebuf[n] before the gather.  All sums are exact under the guard.
-    int *alist = reinterpret_cast<int *>(smem_raw + P.off_alist);
-    uint32_t aflag = 0; // bit q: column tid + q*T holds an argmin
-    const bool corr_on = CIRC && fastp && P.wmode == FWBF_WEIGHTS_IMWBF;
-    if (corr_on) {
-      if (tid == 0) misc[S_NA] = 0;
-      __syncthreads();
-      for (int kk = 0; kk < nKy; ++kk) {
-        const int n = tid + kk * T;
-        bool has = false;
-        if (n < N) {
-          uint32_t a = amask[n * aw];
-          if (aw > 1) a |= amask[n * aw + 1];
-          has = a != 0u;
-        }
-        const uint32_t b = __ballot_sync(FULL_MASK, has);
-        int base = 0;
-        if (lane == 0 && b) base = atomicAdd(&misc[S_NA], __popc(b));
-        base = __shfl_sync(FULL_MASK, base, 0);
-        if (has) alist[base + __popc(b & ((1u << lane) - 1u))] = n;
-        if (has && kk < KC) aflag |= 1u << kk;
+    // ---------------- guarded path: per-column argmin masks into registers -----
+    // Bit j of am[q] says column tid + q*T is the argmin of its j-th check
+    // (m = n - c_j), i.e. reads min2 there instead of min1 (decoders.py:80-84).
+    uint32_t am[KC][2];
+    if (CIRC && fastp) {
+#pragma unroll
+      for (int q = 0; q < KC; ++q) {
+        const int n = tid + q * T;
+        am[q][0] = (n < N) ? amask[n * aw] : 0u;
+        am[q][1] = (n < N && aw > 1) ? amask[n * aw + 1] : 0u;
       }
-      __syncthreads();
     }
-    const int nA = corr_on ? misc[S_NA] : 0;
 
     // ---------------- iterations -----------------------------------------------
     int k = 0;
@@ -306,61 +275,37 @@ decode_kernel(const __grid_constant__ KParams P) {
       if (swt == 0) { conv = 1; break; }
       if (k >= P.kmax) break;
 
-      // ---- argmin corrections (guarded path) -> Ebuf[n] of argmin columns ----
-      if (corr_on) {
-        const uint32_t d21 = (uint32_t)(P.off_chk2 - P.off_chk1);
-        const uint32_t c1 = (uint32_t)__cvta_generic_to_shared(chk1 + N);
-        // two threads per argmin column (adjacent lanes), each W/2 checks,
-        // branch-free predicated loads in groups of 8, combined by one shuffle
-        const int hw = (W + 1) >> 1;
-        const int items = 2 * nA;
-        const int rounds = (items + T - 1) / T;
-        for (int r = 0; r < rounds; ++r) {
-          const int t = r * T + tid;
-          const bool ok = t < items;
-          const int n = ok ? alist[t >> 1] : 0;
-          const int j0 = (t & 1) * hw;
-          const int j1 = min(W, j0 + hw);
-          const uint32_t m0 = ok ? amask[n * aw] : 0u;
-          const uint32_t m1 = (ok && aw > 1) ? amask[n * aw + 1] : 0u;
-          const uint32_t base = c1 + 8u * (uint32_t)n;
-          double ca = 0.0, cb = 0.0;
-          for (int j = j0; j < j1; j += 8) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int jj = j + u;
-              const uint32_t mk = jj < 32 ? m0 : m1;
-              const bool hit = jj < j1 && ((mk >> (jj & 31)) & 1u);
-              double v1 = 0.0, v2 = 0.0;
-              if (hit) {
-                const uint32_t a = base - 8u * (uint32_t)offs_s[jj];
-                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v1) : "r"(a));
-                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v2) : "r"(a + d21));
-              }
-              if (u & 1) cb = __dadd_rn(cb, __dsub_rn(v2, v1));
-              else ca = __dadd_rn(ca, __dsub_rn(v2, v1));
-            }
-          }
-          double corr = __dadd_rn(ca, cb);
-          corr = __dadd_rn(corr, __shfl_xor_sync(FULL_MASK, corr, 1));
-          if (ok && !(t & 1)) Ebuf[n] = corr;
-        }
-        __syncthreads();
-      }
-
       // ---- Eq.(1) metric for every bit -> Ebuf ----
       if (tid == 0) misc[S_F] = 0; // last read before the previous refresh barrier
       if (CIRC && fastp) {
-        // chk1 holds sgn*min1 twice ([0,N) and [N,2N)) plus a KC*T-N pad, so
-        // column n reads check (n - c_j) mod N at index n + N - c_j with no
-        // wrap test: per j one uniform offset, then per column one
-        // immediate-offset LDS.64 and one DADD.  Exact in any order (guard).
+        // chk1/chk2 hold sgn*min1 / sgn*min2 twice ([0,N) and [N,2N)) plus a
+        // KC*T-N pad, so column n reads check (n - c_j) mod N at index
+        // n + N - c_j with no wrap test: per j one uniform offset, then per
+        // column a mask test, an address select, one LDS.64 and one DADD.
+        // The sum is exact in any order under the guard.
         double acc[KC];
 #pragma unroll
-        for (int q = 0; q < KC; ++q) acc[q] = ((aflag >> q) & 1u) ? Ebuf[tid + q * T] : 0.0;
+        for (int q = 0; q < KC; ++q) acc[q] = 0.0;
         const uint32_t s1 = (uint32_t)__cvta_generic_to_shared(chk1 + N + tid);
-#pragma unroll 4
-        for (int j = 0; j < W; ++j) GatherP<0, KC, TB>::run(acc, s1 - 8u * (uint32_t)P.off[j]);
+        const uint32_t d21 = (uint32_t)(P.off_chk2 - P.off_chk1);
+        uint32_t mk[KC];
+#pragma unroll
+        for (int q = 0; q < KC; ++q) mk[q] = am[q][0];
+        const int w0 = W < 32 ? W : 32;
+#pragma unroll 2
+        for (int j = 0; j < w0; ++j) {
+          const uint32_t a1 = s1 - 8u * (uint32_t)P.off[j];
+          GatherQ<0, KC, TB>::run(acc, mk, 1u << j, a1, a1 + d21);
+        }
+        if (W > 32) {
+#pragma unroll
+          for (int q = 0; q < KC; ++q) mk[q] = am[q][1];
+#pragma unroll 2
+          for (int j = 32; j < W; ++j) {
+            const uint32_t a1 = s1 - 8u * (uint32_t)P.off[j];
+            GatherQ<0, KC, TB>::run(acc, mk, 1u << (j - 32), a1, a1 + d21);
+          }
+        }
 #pragma unroll
         for (int q = 0; q < KC; ++q) {
           const int n = tid + q * T;

@@ -58,7 +58,7 @@ struct KParams {
   unsigned int *work_counter;
   // ---- shared memory layout (byte offsets) ----
   int off_y, off_e, off_chk1, off_chk2, off_amin, off_amask, off_sbits, off_zbits;
-  int off_blkv, off_blki, off_flips, off_offs, off_red, off_misc, off_alist;
+  int off_blkv, off_blki, off_flips, off_offs, off_red, off_misc;
   int smem_bytes;
   int alias_y; // metric buffer overlays y; alpha*|y| re-read from global
 };
