@@ -202,6 +202,7 @@ def main():
     import torch.distributed as dist
     from paper_1206_3362_b200 import DecoderConfig, _native as nat
     from paper_1206_3362_b200.decoders import device_code, make_params, BatchResult, _outputs
+    from paper_1206_3362_b200.sharding import reduce_counters
     from tests.golden.codebook import build_code, code_rate
     import ctypes as C
 
@@ -239,8 +240,7 @@ def main():
         res.counters.zero_()
         nat.check(L.fwbf_decode_f32(dc.handle, C.byref(prm), C.c_void_p(y.data_ptr()), B, ld,
                                     C.byref(out), C.c_void_p(stream.cuda_stream)), "decode")
-        if world > 1:
-            dist.all_reduce(res.counters)
+        reduce_counters(res.counters)
 
     for _ in range(a.warmup):
         step()
