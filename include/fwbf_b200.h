@@ -114,6 +114,9 @@ typedef struct {
   int32_t *batch_word_err; /* [ceil(B / batch_frames)], accumulated */
   int32_t batch_frames;    /* harness BATCH_FRAMES (harness.py:24), e.g. 128 */
   const uint32_t *codeword_bits; /* [ceil(n/32)] transmitted word; NULL = all-zero */
+  void *y_out;             /* fwbf_decode_awgn only: [B][y_out_ld] generated channel
+                              values (double for NUMPY_F64, float for NUMPY_F32) */
+  int64_t y_out_ld;
 } fwbf_outputs;
 
 int fwbf_abi_version(void);

@@ -47,7 +47,8 @@ class Outputs(C.Structure):
                 ("fliplog", C.c_void_p), ("fliplog_counts", C.c_void_p),
                 ("fliplog_stride", C.c_int64), ("counters", C.c_void_p),
                 ("iter_hist", C.c_void_p), ("batch_word_err", C.c_void_p),
-                ("batch_frames", C.c_int32), ("codeword_bits", C.c_void_p)]
+                ("batch_frames", C.c_int32), ("codeword_bits", C.c_void_p),
+                ("y_out", C.c_void_p), ("y_out_ld", C.c_int64)]
 
 
 class FwbfError(RuntimeError):

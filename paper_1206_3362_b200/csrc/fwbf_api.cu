@@ -20,7 +20,7 @@
 #include "fwbf_internal.h"
 
 namespace fwbf {
-template <typename YT, bool CIRC, int KC, int TB> __global__ void decode_kernel(const __grid_constant__ KParams P);
+template <typename YT, bool CIRC, int KC, int TB, bool NOISE> __global__ void decode_kernel(const __grid_constant__ KParams P);
 }
 
 using fwbf::KParams;
@@ -300,15 +300,24 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
   P.smem_bytes = o;
 }
 
+struct NoiseSpec {
+  unsigned long long seed;
+  long long first;
+  double sigma;
+};
+
 template <typename YT>
 static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long long batch,
-                         long long ld, const fwbf_outputs *out, cudaStream_t stream) {
+                         long long ld, const fwbf_outputs *out, cudaStream_t stream,
+                         const NoiseSpec *noise = nullptr) {
   int rc = validate(c, p);
   if (rc) return rc;
   if (batch < 0) return fail(FWBF_EINVAL, "batch must be nonnegative");
   if (batch == 0) return FWBF_OK;
-  if (!y) return fail(FWBF_EINVAL, "y is null");
-  if (ld < c->n) return fail(FWBF_EINVAL, "expected a length-%d frame (ld=%lld)", c->n, ld);
+  if (!noise) {
+    if (!y) return fail(FWBF_EINVAL, "y is null");
+    if (ld < c->n) return fail(FWBF_EINVAL, "expected a length-%d frame (ld=%lld)", c->n, ld);
+  }
   if (batch > 0x7fffffffLL) return fail(FWBF_EINVAL, "batch too large for one call");
   fwbf_outputs o = out ? *out : fwbf_outputs{};
   const long long maxf = fwbf_max_flips_per_iter(c, p);
@@ -349,6 +358,12 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   P.y = y;
   P.ld = ld;
   P.batch = batch;
+  if (noise) {
+    P.seed = noise->seed;
+    P.first_frame = noise->first;
+    P.sigma = noise->sigma;
+  }
+  const bool nz = noise != nullptr;
   P.z_bits = o.z_bits;
   P.z_ld = o.z_ld;
   P.iterations = o.iterations;
@@ -363,6 +378,8 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   P.batch_word_err = o.batch_word_err;
   P.batch_frames = o.batch_frames;
   P.codeword_bits = o.codeword_bits;
+  P.y_out = noise ? o.y_out : nullptr;
+  P.y_out_ld = o.y_out_ld;
   const unsigned slot = c->work_slot.fetch_add(1) % kWorkRing;
   P.work_counter = c->d_work + slot;
 
@@ -372,21 +389,34 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   int kc = 1;
   if (circ) {
     if (sizeof(YT) == 4) {
-      static const struct { int kc, tb; const void *fn; } shapes[] = {
-#define FWBF_SHAPE(YT_, C_, KC_, TB_) {KC_, TB_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_>},
+      struct Shape { int kc, tb; const void *fn; };
+      static const Shape shapes[] = {
+#define FWBF_SHAPE(YT_, C_, KC_, TB_) {KC_, TB_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, false>},
           FWBF_FAST_CONFIGS(FWBF_SHAPE)
 #undef FWBF_SHAPE
       };
-      for (const auto &s : shapes)
-        if (s.kc * s.tb >= c->n) { kern = s.fn; T = s.tb; kc = s.kc; break; }
+      static const Shape shapes_nz[] = {
+#define FWBF_SHAPE(YT_, C_, KC_, TB_) {KC_, TB_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, true>},
+          FWBF_FAST_CONFIGS(FWBF_SHAPE)
+#undef FWBF_SHAPE
+      };
+      const Shape *tab = nz ? shapes_nz : shapes;
+      const int ntab = (int)(sizeof(shapes) / sizeof(shapes[0]));
+      for (int i = 0; i < ntab; ++i)
+        if (tab[i].kc * tab[i].tb >= c->n) { kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc; break; }
     } else {
       T = c->n <= 2048 ? 256 : (c->n <= 8192 ? 512 : 1024);
-      kern = (const void *)fwbf::decode_kernel<double, true, 1, 0>;
+      kern = nz ? (const void *)fwbf::decode_kernel<double, true, 1, 0, true>
+                : (const void *)fwbf::decode_kernel<double, true, 1, 0, false>;
     }
   } else {
     T = c->n <= 2048 ? 256 : (c->n <= 8192 ? 512 : 1024);
-    kern = sizeof(YT) == 4 ? (const void *)fwbf::decode_kernel<float, false, 1, 0>
-                           : (const void *)fwbf::decode_kernel<double, false, 1, 0>;
+    if (sizeof(YT) == 4)
+      kern = nz ? (const void *)fwbf::decode_kernel<float, false, 1, 0, true>
+                : (const void *)fwbf::decode_kernel<float, false, 1, 0, false>;
+    else
+      kern = nz ? (const void *)fwbf::decode_kernel<double, false, 1, 0, true>
+                : (const void *)fwbf::decode_kernel<double, false, 1, 0, false>;
   }
   layout(c, p, (int)sizeof(YT), circ, T * kc, P);
   {
@@ -409,7 +439,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     P.log2_tpb = 0;
     while ((1 << P.log2_tpb) < tpb) ++P.log2_tpb;
   }
-  if (P.smem_bytes > c->smem_optin) {
+  if (P.smem_bytes > c->smem_optin && !nz) {
     // Alias the metric buffer over the y buffer: after init y is only needed
     // for alpha*|y|, which the kernel then re-reads from global memory.
     P.alias_y = 1;
@@ -423,6 +453,14 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   if (P.smem_bytes > c->smem_optin)
     return fail(FWBF_EUNSUPPORTED, "frame state needs %d B of shared memory (device max %d)",
                 P.smem_bytes, c->smem_optin);
+  if (nz) {
+    // raw-draw scratch aliases Ebuf and the check records (unused during init);
+    // about N(1 + 1/16) + 64 draws cover a frame, the rest is computed on demand
+    const int avail = (P.off_amask - P.off_e) / 8;
+    int pm = c->n + c->n / 16 + 64;
+    pm = std::min(pm, avail) & ~3;
+    P.noise_pm = std::max(pm, 0);
+  }
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P.smem_bytes));
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, P.smem_bytes));
@@ -448,8 +486,14 @@ extern "C" int fwbf_decode_f64(fwbf_code *c, const fwbf_params *p, const double 
 extern "C" int fwbf_decode_awgn(fwbf_code *c, const fwbf_params *p, uint64_t seed, int64_t first,
                                 int64_t count, double sigma, int32_t mode, const fwbf_outputs *out,
                                 void *stream) {
-  (void)c; (void)p; (void)seed; (void)first; (void)count; (void)sigma; (void)mode; (void)out; (void)stream;
-  return fail(FWBF_EUNSUPPORTED, "on-device noise is not built into this library version");
+  if (first < 0) return fail(FWBF_EINVAL, "seed and frame index must be nonnegative");
+  if (!(sigma >= 0)) return fail(FWBF_EINVAL, "sigma must be nonnegative");
+  NoiseSpec ns{seed, first, sigma};
+  if (mode == FWBF_NOISE_NUMPY_F64)
+    return launch_decode<double>(c, p, nullptr, count, 0, out, (cudaStream_t)stream, &ns);
+  if (mode == FWBF_NOISE_NUMPY_F32)
+    return launch_decode<float>(c, p, nullptr, count, 0, out, (cudaStream_t)stream, &ns);
+  return fail(FWBF_EINVAL, "unknown noise mode %d", mode);
 }
 
 // ---------------------------------------------------------------------------

@@ -40,6 +40,7 @@ struct KParams {
   unsigned long long seed;
   long long first_frame;
   double sigma;
+  int noise_pm; // raw draws prefetched into shared scratch per frame
   // ---- outputs ----
   uint32_t *z_bits;
   long long z_ld;
@@ -55,6 +56,8 @@ struct KParams {
   int *batch_word_err;
   int batch_frames;
   const uint32_t *codeword_bits;
+  void *y_out;
+  long long y_out_ld;
   unsigned int *work_counter;
   // ---- shared memory layout (byte offsets) ----
   int off_y, off_e, off_chk1, off_chk2, off_amin, off_amask, off_sbits, off_zbits;

@@ -318,6 +318,69 @@ def decode_batch(h, y, cfg: DecoderConfig, algorithm: str = "fwbf", *, flip_log:
     return res
 
 
+def decode_awgn(h, cfg: DecoderConfig, algorithm: str, seed: int, first_frame: int, count: int,
+                sigma: float, *, codeword=None, noise: str = "f64", flip_log: bool = False,
+                device=None, force_ordered: bool = False, stream=None,
+                batch_frames: int = 128, return_y: bool = False) -> BatchResult:
+    """Decode frames [first_frame, first_frame + count) of the reference channel.
+
+    The device draws y_n = (1 - 2 c_n) + sigma * g_n with g from numpy's
+    Philox(key=seed, counter=frame << 128) + standard_normal stream
+    (channel.py:29-50), i.e. the frames harness._run_batch would decode.
+    noise="f64" keeps y in float64 (the reference's own values); "f32" rounds
+    y to float32 first (the float32-input configs of BASELINE.json).
+    Per-batch word errors (batch_frames frames each, harness.py:24) are
+    returned in `res.batch_word_err`."""
+    torch = _torch()
+    if algorithm == "fwbf" and cfg.block_len_p is None:
+        raise ValueError("block_len_p is required for block-parallel decoding")
+    if seed < 0 or first_frame < 0:
+        raise ValueError("seed and frame index must be nonnegative")
+    if sigma < 0:
+        raise ValueError("sigma must be nonnegative")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    dc = device_code(h, dev.index if dev.index is not None else 0)
+    p = make_params(cfg, algorithm, force_ordered)
+    L = nat.lib()
+    B = int(count)
+    zw = (dc.n + 31) // 32
+    kw = dict(device=dev)
+    res = BatchResult(
+        n=dc.n,
+        z_bits=torch.zeros((B, zw), dtype=torch.int32, **kw),
+        iterations=torch.zeros(B, dtype=torch.int32, **kw),
+        flags=torch.zeros(B, dtype=torch.uint8, **kw),
+        flips_total=torch.zeros(B, dtype=torch.int32, **kw),
+        bit_errors=torch.zeros(B, dtype=torch.int32, **kw),
+        counters=torch.zeros(nat.NCOUNTERS, dtype=torch.int64, **kw))
+    stride = 0
+    if flip_log:
+        maxf = int(L.fwbf_max_flips_per_iter(dc.handle, C.byref(p)))
+        stride = max(1, cfg.k_max * maxf)
+        res.fliplog = torch.full((B, stride), -1, dtype=torch.int32, **kw)
+        res.fliplog_counts = torch.zeros((B, cfg.k_max), dtype=torch.int32, **kw)
+    cw_t = None
+    if codeword is not None:
+        cw_t = torch.from_numpy(pack_bits(codeword, dc.n).view(np.int32)).to(dev)
+    res.batch_word_err = torch.zeros(max(1, -(-B // batch_frames)), dtype=torch.int32, **kw)
+    out = _outputs(res, stride, cw_t)
+    out.batch_word_err = res.batch_word_err.data_ptr()
+    out.batch_frames = int(batch_frames)
+    res.y = None
+    if return_y:  # the generated channel values (testing / inspection)
+        res.y = torch.empty((B, dc.n), dtype=torch.float64 if noise == "f64" else torch.float32, **kw)
+        out.y_out = res.y.data_ptr()
+        out.y_out_ld = dc.n
+    mode = {"f64": nat.NOISE_NUMPY_F64, "f32": nat.NOISE_NUMPY_F32}[noise]
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        nat.check(L.fwbf_decode_awgn(dc.handle, C.byref(p), C.c_uint64(int(seed)), int(first_frame), B,
+                                     float(sigma), mode, C.byref(out), C.c_void_p(st.cuda_stream)),
+                  "decode_awgn")
+    res._inputs = (cw_t,)
+    return res
+
+
 # ---------------------------------------------------------------------------
 # Per-frame entry points (reference decoders.py:232-259)
 # ---------------------------------------------------------------------------
