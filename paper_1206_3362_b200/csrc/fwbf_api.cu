@@ -9,6 +9,7 @@
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <atomic>
@@ -402,7 +403,13 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
       };
       const Shape *tab = nz ? shapes_nz : shapes;
       const int ntab = (int)(sizeof(shapes) / sizeof(shapes[0]));
-      for (int i = 0; i < ntab; ++i)
+      int want_kc = 0, want_tb = 0; // FWBF_SHAPE="KCxTB" forces a shape (tuning)
+      if (const char *e = getenv("FWBF_SHAPE")) sscanf(e, "%dx%d", &want_kc, &want_tb);
+      for (int i = 0; i < ntab && want_kc; ++i)
+        if (tab[i].kc == want_kc && tab[i].tb == want_tb && tab[i].kc * tab[i].tb >= c->n) {
+          kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc;
+        }
+      for (int i = 0; i < ntab && !kern; ++i)
         if (tab[i].kc * tab[i].tb >= c->n) { kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc; break; }
     } else {
       T = c->n <= 2048 ? 256 : (c->n <= 8192 ? 512 : 1024);

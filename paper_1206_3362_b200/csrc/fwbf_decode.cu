@@ -129,6 +129,19 @@ decode_kernel(const __grid_constant__ KParams P) {
   }
   if (tid == 0) misc[S_NONFIN] = 0;
 
+  // FWBF block-argmax group geometry (fixed for the launch).  Odd p: the
+  // 16/TPB groups of a half-warp take blocks TPB apart, so their lanes' words
+  // land in distinct banks (p*TPB*i + s, i < 16/TPB, s < TPB).
+  const int sel_lt = P.log2_tpb;
+  const int sel_sub = tid & ((1 << sel_lt) - 1);
+  const int sel_gpc = T >> sel_lt;
+  int sel_slot = tid >> sel_lt;
+  if (P.sel_spread) {
+    const int hw = tid >> 4, half = 16 >> sel_lt, tpb = 1 << sel_lt;
+    sel_slot = (hw / tpb) * 16 + tpb * (sel_slot & (half - 1)) + (hw % tpb);
+  }
+  const int sel_rounds = (P.nblocks + sel_gpc - 1) / sel_gpc;
+
   // per-CTA counter accumulation (thread 0)
   long long c_frames = 0, c_biterr = 0, c_worderr = 0, c_iters = 0, c_flips = 0,
             c_stalls = 0, c_conv = 0, c_ordered = 0, c_edges = 0;
@@ -200,6 +213,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     const bool fastp = misc[S_FAST] != 0;
 
     // ---------------- init 2: per-check minima, syndrome, signed weights --------
+    uint32_t sprev = 0; // syndrome bits of this thread's checks tid + k*T
     for (int k = 0; k < nKm; ++k) {
       const int m = tid + k * T;
       const bool ok = m < M;
@@ -229,6 +243,7 @@ decode_kernel(const __grid_constant__ KParams P) {
           }
         }
       }
+      if (ok && par) sprev |= 1u << k;
       const uint32_t b = __ballot_sync(FULL_MASK, ok && par);
       if (lane == 0 && (k * T + warp * 32) < M) {
         sbits[(k * T + warp * 32) >> 5] = b;
@@ -359,18 +374,8 @@ decode_kernel(const __grid_constant__ KParams P) {
         // (decoders.py:156-167, :181-183).  misc[S_F] counts the flips.
         const int p = P.p;
         const int nb = P.nblocks;
-        const int lt = P.log2_tpb;
-        const int TPB = 1 << lt;
-        const int grp = tid >> lt, sub = tid & (TPB - 1), gpc = T >> lt;
-        // odd p: the 16/TPB groups of a half-warp take blocks TPB apart, so their
-        // lanes' words land in distinct banks (p*TPB*i + s, i < 16/TPB, s < TPB)
-        int slot = grp;
-        if (P.sel_spread) {
-          const int hw = tid >> 4, half = 16 >> lt;
-          const int i = grp & (half - 1);
-          slot = (hw / TPB) * 16 + TPB * i + (hw % TPB);
-        }
-        const int rounds = (nb + gpc - 1) / gpc;
+        const int TPB = 1 << sel_lt;
+        const int sub = sel_sub, gpc = sel_gpc, slot = sel_slot, rounds = sel_rounds;
         for (int r = 0; r < rounds; ++r) {
           const int b = r * gpc + slot;
           const bool ok = b < nb;
@@ -557,19 +562,23 @@ decode_kernel(const __grid_constant__ KParams P) {
       logpos += F;
       flips_total += F;
 
-      // ---- refresh signs from the new syndrome; syndrome weight ----
+      // ---- refresh signs of the checks that toggled; syndrome weight ----
+      // Thread tid owns checks tid + kk*T in every iteration and remembers
+      // their previous syndrome bits in `sprev`, so only toggled checks are
+      // rewritten (negated; both copies on the guarded path).
       for (int kk = 0; kk < nKm; ++kk) {
         const int m = tid + kk * T;
         const bool ok = m < M;
-        const bool s = ok && ((sbits[m >> 5] >> (m & 31)) & 1u);
-        if (ok) {
-          const double a1 = fabs(chk1[m]);
-          const double v1 = s ? a1 : -a1;
+        const uint32_t word = ok ? sbits[m >> 5] : 0u;
+        const bool s = ok && ((word >> (m & 31)) & 1u);
+        const bool tog = s != (bool)((sprev >> kk) & 1u);
+        if (tog) {
+          const double v1 = -chk1[m];
+          const double v2 = -chk2[m];
           chk1[m] = v1;
-          const double a2 = fabs(chk2[m]);
-          const double v2 = s ? a2 : -a2;
           chk2[m] = v2;
           if (CIRC && fastp) { chk1[m + N] = v1; chk2[m + N] = v2; }
+          sprev ^= 1u << kk;
         }
         const uint32_t b = __ballot_sync(FULL_MASK, s);
         if (lane == 0 && b) atomicAdd(&misc[S_SWT], __popc(b));

@@ -12,7 +12,9 @@ constexpr int kMaxCircWeight = 64; // circulant offsets kept in the parameter bl
   X(float, true, 4, 256)     \
   X(float, true, 4, 512)     \
   X(float, true, 8, 512)     \
-  X(float, true, 8, 1024)
+  X(float, true, 8, 1024)     \
+  X(float, true, 8, 128)      \
+  X(float, true, 2, 512)
 
 struct KParams {
   // ---- code (H) ----
