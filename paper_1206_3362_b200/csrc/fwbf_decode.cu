@@ -285,6 +285,7 @@ decode_kernel(const __grid_constant__ KParams P) {
         am[q][1] = (n < N && aw > 1) ? amask[n * aw + 1] : 0u;
       }
     }
+    if (P.alias_y) __syncthreads(); // amask / ybuf may overlay Ebuf (compact layout)
 
     // ---------------- iterations -----------------------------------------------
     int k = 0;
