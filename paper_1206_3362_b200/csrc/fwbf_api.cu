@@ -21,7 +21,7 @@
 #include "fwbf_internal.h"
 
 namespace fwbf {
-template <typename YT, bool CIRC, int KC, int TB, bool NOISE> __global__ void decode_kernel(const __grid_constant__ KParams P);
+template <typename YT, bool CIRC, int KC, int TB, bool NOISE, int WT> __global__ void decode_kernel(const __grid_constant__ KParams P);
 }
 
 using fwbf::KParams;
@@ -403,14 +403,14 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   int kc = 1;
   if (circ) {
     if (sizeof(YT) == 4) {
-      struct Shape { int kc, tb; const void *fn; };
+      struct Shape { int kc, tb, wt; const void *fn; };
       static const Shape shapes[] = {
-#define FWBF_SHAPE(YT_, C_, KC_, TB_) {KC_, TB_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, false>},
+#define FWBF_SHAPE(YT_, C_, KC_, TB_, WT_) {KC_, TB_, WT_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, false, WT_>},
           FWBF_FAST_CONFIGS(FWBF_SHAPE)
 #undef FWBF_SHAPE
       };
       static const Shape shapes_nz[] = {
-#define FWBF_SHAPE(YT_, C_, KC_, TB_) {KC_, TB_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, true>},
+#define FWBF_SHAPE(YT_, C_, KC_, TB_, WT_) {KC_, TB_, WT_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, true, WT_>},
           FWBF_FAST_CONFIGS(FWBF_SHAPE)
 #undef FWBF_SHAPE
       };
@@ -418,25 +418,33 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
       const int ntab = (int)(sizeof(shapes) / sizeof(shapes[0]));
       int want_kc = 0, want_tb = 0; // FWBF_SHAPE="KCxTB" forces a shape (tuning)
       if (const char *e = getenv("FWBF_SHAPE")) sscanf(e, "%dx%d", &want_kc, &want_tb);
+      const bool generic_only = getenv("FWBF_GENERIC_W") != nullptr;
       for (int i = 0; i < ntab && want_kc; ++i)
-        if (tab[i].kc == want_kc && tab[i].tb == want_tb && tab[i].kc * tab[i].tb >= c->n) {
+        if (tab[i].kc == want_kc && tab[i].tb == want_tb && tab[i].kc * tab[i].tb >= c->n &&
+            (tab[i].wt == 0 || (tab[i].wt == c->w && !generic_only))) {
+          kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc;
+          if (tab[i].wt) break;
+        }
+      // prefer the smallest shape covering n with the weight compiled in
+      for (int i = 0; i < ntab && !kern && !generic_only; ++i)
+        if (tab[i].wt == c->w && tab[i].kc * tab[i].tb >= c->n && tab[i].kc * tab[i].tb < 4 * c->n + 256) {
           kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc;
         }
       for (int i = 0; i < ntab && !kern; ++i)
-        if (tab[i].kc * tab[i].tb >= c->n) { kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc; break; }
+        if (tab[i].wt == 0 && tab[i].kc * tab[i].tb >= c->n) { kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc; break; }
     } else {
       T = c->n <= 2048 ? 256 : (c->n <= 8192 ? 512 : 1024);
-      kern = nz ? (const void *)fwbf::decode_kernel<double, true, 1, 0, true>
-                : (const void *)fwbf::decode_kernel<double, true, 1, 0, false>;
+      kern = nz ? (const void *)fwbf::decode_kernel<double, true, 1, 0, true, 0>
+                : (const void *)fwbf::decode_kernel<double, true, 1, 0, false, 0>;
     }
   } else {
     T = c->n <= 2048 ? 256 : (c->n <= 8192 ? 512 : 1024);
     if (sizeof(YT) == 4)
-      kern = nz ? (const void *)fwbf::decode_kernel<float, false, 1, 0, true>
-                : (const void *)fwbf::decode_kernel<float, false, 1, 0, false>;
+      kern = nz ? (const void *)fwbf::decode_kernel<float, false, 1, 0, true, 0>
+                : (const void *)fwbf::decode_kernel<float, false, 1, 0, false, 0>;
     else
-      kern = nz ? (const void *)fwbf::decode_kernel<double, false, 1, 0, true>
-                : (const void *)fwbf::decode_kernel<double, false, 1, 0, false>;
+      kern = nz ? (const void *)fwbf::decode_kernel<double, false, 1, 0, true, 0>
+                : (const void *)fwbf::decode_kernel<double, false, 1, 0, false, 0>;
   }
   const bool compact = circ && sizeof(YT) == 4 && !nz && c->w <= 32 && !getenv("FWBF_NO_COMPACT");
   layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact);

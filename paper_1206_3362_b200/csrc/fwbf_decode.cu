@@ -90,7 +90,7 @@ __device__ __forceinline__ YT load_y(const KParams &P, long long f, int n) {
 //   CIRC : circulant H (index arithmetic) vs explicit CSR/CSC tables
 //   KC   : columns per thread on the guarded path (register accumulators)
 // ---------------------------------------------------------------------------
-template <typename YT, bool CIRC, int KC, int TB, bool NOISE>
+template <typename YT, bool CIRC, int KC, int TB, bool NOISE, int WT>
 __global__ void __launch_bounds__(TB ? TB : 1024, 1024 / (TB ? TB : 1024))
 decode_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -121,7 +121,7 @@ decode_kernel(const __grid_constant__ KParams P) {
   // misc slots
   enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR };
 
-  const int W = P.w;                 // circulant weight (0 explicit)
+  const int W = WT ? WT : P.w;       // circulant weight (0 explicit); compile-time when WT > 0
   const int aw = (W > 32) ? 2 : 1;   // amask words per column
 
   if (CIRC) {
@@ -310,22 +310,28 @@ decode_kernel(const __grid_constant__ KParams P) {
         for (int q = 0; q < KC; ++q) acc[q] = 0.0;
         const uint32_t s1 = (uint32_t)__cvta_generic_to_shared(chk1 + N + tid);
         const uint32_t d21 = (uint32_t)(P.off_chk2 - P.off_chk1);
-        uint32_t mk[KC];
+        uint32_t mk[KC], mkh[KC];
 #pragma unroll
-        for (int q = 0; q < KC; ++q) mk[q] = am[q][0];
-        const int w0 = W < 32 ? W : 32;
+        for (int q = 0; q < KC; ++q) { mk[q] = am[q][0]; mkh[q] = am[q][1]; }
+        if (WT > 0) {
+          // compile-time weight: fully unrolled, offsets are constant-bank operands
+#pragma unroll
+          for (int j = 0; j < (WT > 0 ? WT : 1); ++j) {
+            const uint32_t a1 = s1 - 8u * (uint32_t)P.off[j];
+            if (j < 32) GatherQ<0, KC, TB>::run(acc, mk, 1u << (j & 31), a1, a1 + d21);
+            else GatherQ<0, KC, TB>::run(acc, mkh, 1u << (j & 31), a1, a1 + d21);
+          }
+        } else {
+          const int w0 = W < 32 ? W : 32;
 #pragma unroll 2
-        for (int j = 0; j < w0; ++j) {
-          const uint32_t a1 = s1 - 8u * (uint32_t)P.off[j];
-          GatherQ<0, KC, TB>::run(acc, mk, 1u << j, a1, a1 + d21);
-        }
-        if (W > 32) {
-#pragma unroll
-          for (int q = 0; q < KC; ++q) mk[q] = am[q][1];
+          for (int j = 0; j < w0; ++j) {
+            const uint32_t a1 = s1 - 8u * (uint32_t)P.off[j];
+            GatherQ<0, KC, TB>::run(acc, mk, 1u << j, a1, a1 + d21);
+          }
 #pragma unroll 2
           for (int j = 32; j < W; ++j) {
             const uint32_t a1 = s1 - 8u * (uint32_t)P.off[j];
-            GatherQ<0, KC, TB>::run(acc, mk, 1u << (j - 32), a1, a1 + d21);
+            GatherQ<0, KC, TB>::run(acc, mkh, 1u << (j - 32), a1, a1 + d21);
           }
         }
 #pragma unroll
@@ -642,12 +648,12 @@ decode_kernel(const __grid_constant__ KParams P) {
 }
 
 // explicit instantiations used by the launcher
-#define FWBF_INST(YT, C, KC, TB)                                                             \
-  template __global__ void decode_kernel<YT, C, KC, TB, false>(const __grid_constant__ KParams); \
-  template __global__ void decode_kernel<YT, C, KC, TB, true>(const __grid_constant__ KParams);
+#define FWBF_INST(YT, C, KC, TB, WT)                                                             \
+  template __global__ void decode_kernel<YT, C, KC, TB, false, WT>(const __grid_constant__ KParams); \
+  template __global__ void decode_kernel<YT, C, KC, TB, true, WT>(const __grid_constant__ KParams);
 FWBF_FAST_CONFIGS(FWBF_INST)
-FWBF_INST(double, true, 1, 0)
-FWBF_INST(float, false, 1, 0)
-FWBF_INST(double, false, 1, 0)
+FWBF_INST(double, true, 1, 0, 0)
+FWBF_INST(float, false, 1, 0, 0)
+FWBF_INST(double, false, 1, 0, 0)
 
 } // namespace fwbf

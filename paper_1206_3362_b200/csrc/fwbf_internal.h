@@ -7,14 +7,16 @@ namespace fwbf {
 constexpr int kMaxCircWeight = 64; // circulant offsets kept in the parameter block
 
 // Guarded-path kernel shapes (threads TB, columns per thread KC): TB*KC >= n.
-#define FWBF_FAST_CONFIGS(X) \
-  X(float, true, 2, 128)     \
-  X(float, true, 4, 256)     \
-  X(float, true, 4, 512)     \
-  X(float, true, 8, 512)     \
-  X(float, true, 8, 1024)     \
-  X(float, true, 8, 128)      \
-  X(float, true, 2, 512)
+// WT > 0: circulant weight fixed at compile time (fully unrolled gather).
+#define FWBF_FAST_CONFIGS(X)    \
+  X(float, true, 2, 128, 16)    \
+  X(float, true, 4, 256, 32)    \
+  X(float, true, 8, 512, 64)    \
+  X(float, true, 2, 128, 0)     \
+  X(float, true, 4, 256, 0)     \
+  X(float, true, 4, 512, 0)     \
+  X(float, true, 8, 512, 0)     \
+  X(float, true, 8, 1024, 0)
 
 struct KParams {
   // ---- code (H) ----
