@@ -572,23 +572,48 @@ decode_kernel(const __grid_constant__ KParams P) {
       // ---- refresh signs of the checks that toggled; syndrome weight ----
       // Thread tid owns checks tid + kk*T in every iteration and remembers
       // their previous syndrome bits in `sprev`, so only toggled checks are
-      // rewritten (negated; both copies on the guarded path).
-      for (int kk = 0; kk < nKm; ++kk) {
-        const int m = tid + kk * T;
-        const bool ok = m < M;
-        const uint32_t word = ok ? sbits[m >> 5] : 0u;
-        const bool s = ok && ((word >> (m & 31)) & 1u);
-        const bool tog = s != (bool)((sprev >> kk) & 1u);
-        if (tog) {
-          const double v1 = -chk1[m];
-          const double v2 = -chk2[m];
-          chk1[m] = v1;
-          chk2[m] = v2;
-          if (CIRC && fastp) { chk1[m + N] = v1; chk2[m + N] = v2; }
-          sprev ^= 1u << kk;
+      // rewritten (negated; both copies on the guarded path).  With T a
+      // multiple of 32, check tid + kk*T is bit `lane` of one warp-uniform word.
+      if (TB > 0) {
+        int pc = 0;
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+          const int m = tid + kk * TB;
+          if (kk * TB < M) { // warp-uniform
+            const uint32_t word = sbits[(kk * TB + warp * 32) >> 5];
+            const bool ok = m < M;
+            const bool s = (word >> lane) & 1u;
+            const bool tog = ok && (s != (bool)((sprev >> kk) & 1u));
+            if (tog) {
+              const double v1 = -chk1[m];
+              const double v2 = -chk2[m];
+              chk1[m] = v1;
+              chk2[m] = v2;
+              if (CIRC && fastp) { chk1[m + N] = v1; chk2[m + N] = v2; }
+            }
+            sprev ^= (tog ? 1u : 0u) << kk;
+            pc += __popc(word);
+          }
         }
-        const uint32_t b = __ballot_sync(FULL_MASK, s);
-        if (lane == 0 && b) atomicAdd(&misc[S_SWT], __popc(b));
+        if (lane == 0 && pc) atomicAdd(&misc[S_SWT], pc);
+      } else {
+        for (int kk = 0; kk < nKm; ++kk) {
+          const int m = tid + kk * T;
+          const bool ok = m < M;
+          const uint32_t word = ok ? sbits[m >> 5] : 0u;
+          const bool s = ok && ((word >> (m & 31)) & 1u);
+          const bool tog = s != (bool)((sprev >> kk) & 1u);
+          if (tog) {
+            const double v1 = -chk1[m];
+            const double v2 = -chk2[m];
+            chk1[m] = v1;
+            chk2[m] = v2;
+            if (CIRC && fastp) { chk1[m + N] = v1; chk2[m + N] = v2; }
+            sprev ^= 1u << kk;
+          }
+          const uint32_t b = __ballot_sync(FULL_MASK, s);
+          if (lane == 0 && b) atomicAdd(&misc[S_SWT], __popc(b));
+        }
       }
       k += 1;
       __syncthreads();
