@@ -579,7 +579,7 @@ decode_kernel(const __grid_constant__ KParams P) {
 #pragma unroll
         for (int kk = 0; kk < KC; ++kk) {
           const int m = tid + kk * TB;
-          if (kk * TB < M) { // warp-uniform
+          if (kk * TB + warp * 32 < M) { // warp-uniform: this warp's word exists
             const uint32_t word = sbits[(kk * TB + warp * 32) >> 5];
             const bool ok = m < M;
             const bool s = (word >> lane) & 1u;
