@@ -55,6 +55,7 @@ extern "C" {
 #define FWBF_FLAG_STALLED 2
 #define FWBF_FLAG_ORDERED 4   /* decoded on the ordered (non-guarded) metric path */
 #define FWBF_FLAG_NONFINITE 8 /* y held NaN/inf; result follows IEEE comparisons */
+#define FWBF_FLAG_SPLIT32 16  /* decoded on the split-fp32 guarded metric path */
 
 /* counters vector layout (int64) */
 enum {
@@ -95,7 +96,7 @@ typedef struct {
   int32_t block_len_p;   /* >= 1 (FWBF) */
   int32_t stall;         /* FWBF_STALL_* */
   int32_t mlp_threshold; /* 0/1 */
-  int32_t force_ordered; /* 1: never use the guarded fast metric path (testing) */
+  int32_t force_ordered; /* testing: 1 = ordered path only, 2 = no split-fp32 path */
 } fwbf_params;
 
 /* Output buffers (device memory, caller-owned, all optional). */

@@ -18,7 +18,7 @@ FWBF_OK, FWBF_EINVAL, FWBF_ECUDA, FWBF_EUNSUPPORTED = 0, -1, -2, -3
 ALG = {"fwbf": 0, "imwbf": 1, "mlp": 2}
 WEIGHTS = {"imwbf": 0, "mwbf": 1}
 STALL = {"flip-global-max": 0, "terminate": 1}
-FLAG_CONVERGED, FLAG_STALLED, FLAG_ORDERED, FLAG_NONFINITE = 1, 2, 4, 8
+FLAG_CONVERGED, FLAG_STALLED, FLAG_ORDERED, FLAG_NONFINITE, FLAG_SPLIT32 = 1, 2, 4, 8, 16
 NOISE_NUMPY_F64, NOISE_NUMPY_F32 = 0, 1
 (CNT_FRAMES, CNT_BIT_ERRORS, CNT_WORD_ERRORS, CNT_ITER_SUM, CNT_FLIP_SUM, CNT_STALLS,
  CNT_CONVERGED, CNT_ORDERED_FRAMES, CNT_EDGE_VISITS, NCOUNTERS) = range(10)

@@ -289,10 +289,11 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
   if (circ) {
     // both doubled arrays; chk2 - chk1 is a multiple of 128 B so a lane that
     // reads min2 instead of min1 hits the same banks (no extra wavefront)
-    const int dbl = (2 * n + std::max(0, cover - n) + 15) / 16 * 16;
+    const int dbl = (2 * n + std::max(0, cover - n) + 31) / 32 * 32;
     const int r = take(2 * dbl * 8);
     P.off_chk1 = r;
     P.off_chk2 = r + dbl * 8;
+    P.d21f = dbl * 4; // split-fp32 path: float arrays at r and r + dbl*4 (128 B multiple)
     P.off_amin = P.off_chk2 + align16(m * 8); // ordered path only; inside chk2's upper half
   } else {
     P.off_chk1 = take(m * 8);
@@ -366,7 +367,8 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   P.p = p->block_len_p;
   P.stall = p->stall;
   P.mlp_thr = p->mlp_threshold ? 1 : 0;
-  P.force_ordered = p->force_ordered ? 1 : 0;
+  P.force_ordered = (p->force_ordered & 1) ? 1 : 0;
+  P.no_split = (p->force_ordered & 2) || getenv("FWBF_NO_SPLIT") ? 1 : 0;
   P.alpha = p->alpha;
   P.nblocks = p->algorithm == FWBF_ALG_FWBF ? (c->n + p->block_len_p - 1) / p->block_len_p : 1;
   P.y = y;

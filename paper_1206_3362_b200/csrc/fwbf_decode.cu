@@ -78,6 +78,58 @@ template <int KC, int TB> struct GatherQ<KC, KC, TB> {
   static __device__ __forceinline__ void run(double (&)[KC], const uint32_t (&)[KC], uint32_t, uint32_t, uint32_t) {}
 };
 
+// Packed fp32x2 helpers (sm_100 FADD2); always round-to-nearest, no FTZ.
+__device__ __forceinline__ unsigned long long f2pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2unpack(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long fsub2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// Split-fp32 gather step for a pair of column slots (Q, Q+1): select min1 or
+// min2 per column, load float32, split v = h + l exactly on the grid G
+// (t = v + C, h = t - C, l = v - h with C = 1.5 * 2^23 * G), accumulate h and
+// l in separate fp32 accumulators.  Exact under the float32 guard (see kernel).
+template <int KC> struct SplitPairs { static constexpr int value = KC / 2 > 0 ? KC / 2 : 1; };
+
+template <int Q, int KC, int TB, bool GO = (Q + 1 < KC)> struct GatherS {
+  static __device__ __forceinline__ void run(unsigned long long (&hi)[SplitPairs<KC>::value],
+                                             unsigned long long (&lo)[SplitPairs<KC>::value],
+                                             const uint32_t (&mk)[KC], uint32_t bit, uint32_t a1,
+                                             uint32_t a2, unsigned long long cc) {
+    const uint32_t p0 = (mk[Q] & bit) ? a2 : a1;
+    const uint32_t p1 = (mk[Q + 1] & bit) ? a2 : a1;
+    float v0, v1;
+    asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v0) : "r"(p0), "n"(Q * TB * 4));
+    asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v1) : "r"(p1), "n"((Q + 1) * TB * 4));
+    const unsigned long long v = f2pack(v0, v1);
+    const unsigned long long h = fsub2(fadd2(v, cc), cc);
+    hi[Q / 2] = fadd2(hi[Q / 2], h);
+    lo[Q / 2] = fadd2(lo[Q / 2], fsub2(v, h));
+    GatherS<Q + 2, KC, TB>::run(hi, lo, mk, bit, a1, a2, cc);
+  }
+};
+template <int Q, int KC, int TB> struct GatherS<Q, KC, TB, false> {
+  static __device__ __forceinline__ void run(unsigned long long (&)[SplitPairs<KC>::value],
+                                             unsigned long long (&)[SplitPairs<KC>::value],
+                                             const uint32_t (&)[KC], uint32_t, uint32_t, uint32_t,
+                                             unsigned long long) {}
+};
+
 template <typename YT>
 __device__ __forceinline__ YT load_y(const KParams &P, long long f, int n) {
   const YT *y = reinterpret_cast<const YT *>(P.y);
@@ -195,7 +247,9 @@ decode_kernel(const __grid_constant__ KParams P) {
     if (tid == 0) {
       float mn = INFINITY, mx = 0.f;
       for (int w2 = 0; w2 < nwarps; ++w2) { mn = fminf(mn, redf[w2]); mx = fmaxf(mx, redf[32 + w2]); }
+      // path: 0 ordered, 1 guarded fp64, 2 guarded split-fp32 (compile-time W)
       int fast = 0;
+      float cmag = 0.f;
       if (CIRC && sizeof(YT) == 4 && !P.force_ordered && !misc[S_NONFIN]) {
         if (!(mn < INFINITY)) {
           fast = 1; // all |y| == 0: every weight is 0, sums trivially exact
@@ -205,12 +259,24 @@ decode_kernel(const __grid_constant__ KParams P) {
           // quantum q = 2^(e-23); need 2*dv*max|y| < 2^53 * q = 2^(30+e)
           double lhs = 2.0 * (double)W * (double)mx;
           fast = lhs < ldexp(1.0, 30 + e);
+          // split-fp32: grid G = 2^20 q = 2^(e-3); every column sum of |w| must
+          // stay below 2^(20+e) so hi (multiples of G) and lo (multiples of q,
+          // |lo| <= 16G) sums are exact in fp32; C = 1.5 * 2^23 * G
+          if (fast && WT > 0 && (KC % 2) == 0 && e >= -100 && !P.no_split &&
+              (double)W * (double)mx <= ldexp(1.0, 20 + e)) {
+            fast = 2;
+            cmag = ldexpf(1.5f, 20 + e);
+          }
         }
       }
+      redf[0] = cmag;
       misc[S_FAST] = fast;
     }
     __syncthreads();
-    const bool fastp = misc[S_FAST] != 0;
+    const int fpath = misc[S_FAST];
+    const bool fastp = fpath != 0;
+    const bool split = fpath == 2;
+    const float cmag = redf[0];
 
     // ---------------- init 2: per-check minima, syndrome, signed weights --------
     uint32_t sprev = 0; // syndrome bits of this thread's checks tid + k*T
@@ -252,7 +318,22 @@ decode_kernel(const __grid_constant__ KParams P) {
       if (ok) {
         const double sg = par ? 1.0 : -1.0;
         const double d1 = (double)min1, d2 = (double)min2;
-        if (CIRC && fastp) {
+        if (CIRC && split) {
+          float *f1 = reinterpret_cast<float *>(chk1);
+          float *f2 = reinterpret_cast<float *>(smem_raw + P.off_chk1 + P.d21f);
+          const float s1v = par ? (float)min1 : -(float)min1;
+          const float s2v = par ? (float)min2 : -(float)min2;
+          f1[m] = s1v;
+          f1[m + N] = s1v;
+          f2[m] = s2v;
+          f2[m + N] = s2v;
+          if (P.wmode == FWBF_WEIGHTS_IMWBF) {
+            int d = ac - m;
+            if (d < 0) d += N;
+            const int j = P.offpos[d];
+            atomicOr(&amask[ac * aw + (j >> 5)], 1u << (j & 31));
+          }
+        } else if (CIRC && fastp) {
           chk1[m] = sg * d1;
           chk1[m + N] = sg * d1;
           chk2[m] = sg * d2;
@@ -299,7 +380,42 @@ decode_kernel(const __grid_constant__ KParams P) {
 
       // ---- Eq.(1) metric for every bit -> Ebuf ----
       if (tid == 0) misc[S_F] = 0; // last read before the previous refresh barrier
-      if (CIRC && fastp) {
+      if (WT > 0 && CIRC && split && (KC % 2) == 0) {
+        // Split-fp32 gather (4 B per edge instead of 8): float32 signed min1 /
+        // min2 in doubled arrays; each value v = h + l with h on the grid G and
+        // l = v - h, both exact; hi = sum h (multiples of G, |hi| < 2^24 G) and
+        // lo = sum l (multiples of q, |lo| <= 16 G <= 2^24 q) are exact in fp32,
+        // so hi + lo in fp64 is the exact column sum (= the reference's).
+        unsigned long long hi[SplitPairs<KC>::value], lo[SplitPairs<KC>::value];
+#pragma unroll
+        for (int qp = 0; qp < KC / 2; ++qp) { hi[qp] = 0ull; lo[qp] = 0ull; }
+        const unsigned long long cc = f2pack(cmag, cmag);
+        const uint32_t s1 = (uint32_t)__cvta_generic_to_shared(reinterpret_cast<float *>(chk1) + N + tid);
+        const uint32_t d21 = (uint32_t)P.d21f;
+        uint32_t mk[KC], mkh[KC];
+#pragma unroll
+        for (int q = 0; q < KC; ++q) { mk[q] = am[q][0]; mkh[q] = am[q][1]; }
+#pragma unroll
+        for (int j = 0; j < (WT > 0 ? WT : 1); ++j) {
+          const uint32_t a1 = s1 - 4u * (uint32_t)P.off[j];
+          if (j < 32) GatherS<0, KC, TB>::run(hi, lo, mk, 1u << (j & 31), a1, a1 + d21, cc);
+          else GatherS<0, KC, TB>::run(hi, lo, mkh, 1u << (j & 31), a1, a1 + d21, cc);
+        }
+#pragma unroll
+        for (int qp = 0; qp < KC / 2; ++qp) {
+          const float2 h = f2unpack(hi[qp]);
+          const float2 l = f2unpack(lo[qp]);
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int n = tid + (2 * qp + u) * T;
+            if (n < N) {
+              const double acc = __dadd_rn((double)(u ? h.y : h.x), (double)(u ? l.y : l.x));
+              const double ay = P.alias_y ? fabs((double)load_y<YT>(P, f, n)) : fabs((double)ybuf[n]);
+              Ebuf[n] = __dsub_rn(acc, __dmul_rn(P.alpha, ay));
+            }
+          }
+        }
+      } else if (CIRC && fastp) {
         // chk1/chk2 hold sgn*min1 / sgn*min2 twice ([0,N) and [N,2N)) plus a
         // KC*T-N pad, so column n reads check (n - c_j) mod N at index
         // n + N - c_j with no wrap test: per j one uniform offset, then per
@@ -585,11 +701,21 @@ decode_kernel(const __grid_constant__ KParams P) {
             const bool s = (word >> lane) & 1u;
             const bool tog = ok && (s != (bool)((sprev >> kk) & 1u));
             if (tog) {
-              const double v1 = -chk1[m];
-              const double v2 = -chk2[m];
-              chk1[m] = v1;
-              chk2[m] = v2;
-              if (CIRC && fastp) { chk1[m + N] = v1; chk2[m + N] = v2; }
+              if (CIRC && split) {
+                float *f1 = reinterpret_cast<float *>(chk1);
+                float *f2 = reinterpret_cast<float *>(smem_raw + P.off_chk1 + P.d21f);
+                const float v1 = -f1[m], v2 = -f2[m];
+                f1[m] = v1;
+                f1[m + N] = v1;
+                f2[m] = v2;
+                f2[m + N] = v2;
+              } else {
+                const double v1 = -chk1[m];
+                const double v2 = -chk2[m];
+                chk1[m] = v1;
+                chk2[m] = v2;
+                if (CIRC && fastp) { chk1[m + N] = v1; chk2[m + N] = v2; }
+              }
             }
             sprev ^= (tog ? 1u : 0u) << kk;
             pc += __popc(word);
@@ -638,7 +764,8 @@ decode_kernel(const __grid_constant__ KParams P) {
     if (tid == 0) {
       const int be = misc[S_BITERR];
       const int flags = (conv ? FWBF_FLAG_CONVERGED : 0) | (stalled ? FWBF_FLAG_STALLED : 0) |
-                        (fastp ? 0 : FWBF_FLAG_ORDERED) | (misc[S_NONFIN] ? FWBF_FLAG_NONFINITE : 0);
+                        (fastp ? 0 : FWBF_FLAG_ORDERED) | (misc[S_NONFIN] ? FWBF_FLAG_NONFINITE : 0) |
+                        (split ? FWBF_FLAG_SPLIT32 : 0);
       if (P.iterations) P.iterations[f] = k;
       if (P.flags) P.flags[f] = (uint8_t)flags;
       if (P.flips_total) P.flips_total[f] = (int)flips_total;

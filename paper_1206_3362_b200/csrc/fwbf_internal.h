@@ -68,6 +68,8 @@ struct KParams {
   int off_blkv, off_blki, off_flips, off_offs, off_red, off_misc;
   int smem_bytes;
   int alias_y; // metric buffer overlays y; alpha*|y| re-read from global
+  int d21f;    // split-fp32 path: byte offset of the float min2 array from chk1
+  int no_split; // disable the split-fp32 path (testing)
 };
 
 } // namespace fwbf

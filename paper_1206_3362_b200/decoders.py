@@ -156,7 +156,7 @@ def device_code(h, device: int = 0) -> DeviceCode:
     return dc
 
 
-def make_params(cfg: DecoderConfig, algorithm: str, force_ordered: bool = False) -> nat.Params:
+def make_params(cfg: DecoderConfig, algorithm: str, force_ordered=False) -> nat.Params:
     if algorithm not in nat.ALG:
         raise ValueError(f"unknown algorithm {algorithm!r}")
     p = nat.Params()
@@ -168,7 +168,7 @@ def make_params(cfg: DecoderConfig, algorithm: str, force_ordered: bool = False)
     p.block_len_p = int(cfg.block_len_p) if cfg.block_len_p is not None else 0
     p.stall = nat.STALL[cfg.stall_policy]
     p.mlp_threshold = 1 if cfg.mlp_threshold else 0
-    p.force_ordered = 1 if force_ordered else 0
+    p.force_ordered = int(force_ordered)  # True/1: ordered path; 2: no split-fp32 path
     return p
 
 

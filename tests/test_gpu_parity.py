@@ -36,7 +36,7 @@ def assert_batch_equal(res, z, iters, conv, stalled, flips_total, logs, tag):
             assert a == b, f"{tag}: flip log of frame {i} differs"
 
 
-@pytest.mark.parametrize("ordered", [False, True], ids=["default", "ordered"])
+@pytest.mark.parametrize("ordered", [0, 1, 2], ids=["default", "ordered", "fp64guard"])
 @pytest.mark.parametrize("name", case_names())
 def test_golden_fixture(cuda_device, name, ordered):
     c = load_case(name)
@@ -145,6 +145,18 @@ def test_guarded_equals_ordered_full_size(big_b):
     assert cnt[nat.CNT_WORD_ERRORS] == (a.bit_errors.cpu().numpy() > 0).sum()
     # the guard is rare to fail: at most a few in 1e4 frames take the ordered path
     assert cnt[nat.CNT_ORDERED_FRAMES] < y.shape[0] * 1e-3
+
+
+def test_split_fp32_equals_fp64_guarded_full_size(big_b):
+    h, y = big_b
+    cfg = DecoderConfig(block_len_p=31, k_max=100)
+    a = decode_batch(h, y, cfg, "fwbf")
+    b = decode_batch(h, y, cfg, "fwbf", force_ordered=2)
+    for u, v in zip(_summary(a), _summary(b)):
+        assert np.array_equal(u, v)
+    fl = a.flags.cpu().numpy()
+    assert (fl & nat.FLAG_SPLIT32).mean() > 0.9      # most frames take the split-fp32 path
+    assert not np.any(b.flags.cpu().numpy() & nat.FLAG_SPLIT32)
 
 
 def test_scale_invariance_full_size(big_b):
