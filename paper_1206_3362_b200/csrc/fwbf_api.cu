@@ -290,10 +290,19 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
     // both doubled arrays; chk2 - chk1 is a multiple of 128 B so a lane that
     // reads min2 instead of min1 hits the same banks (no extra wavefront)
     const int dbl = (2 * n + std::max(0, cover - n) + 31) / 32 * 32;
-    const int r = take(2 * dbl * 8);
+    // split-fp32 path (same region): signed min1 as float32 twice (second copy
+    // shifted by one element for 8-byte pair loads), |min2|, argmin column,
+    // and the per-column (lo, hi) correction limbs
+    const int dblf = (2 * n + std::max(0, cover - n) + 2 + 31) / 32 * 32;
+    const int split_bytes = 2 * dblf * 4 + align16(m * 4) * 2 + align16(n * 8);
+    const int r = take(std::max(2 * dbl * 8, split_bytes));
     P.off_chk1 = r;
     P.off_chk2 = r + dbl * 8;
-    P.d21f = dbl * 4; // split-fp32 path: float arrays at r and r + dbl*4 (128 B multiple)
+    P.off_fa = r;
+    P.off_fb = r + dblf * 4;
+    P.off_m2s = r + 2 * dblf * 4;
+    P.off_a2m = P.off_m2s + align16(m * 4);
+    P.off_corr = P.off_a2m + align16(m * 4);
     P.off_amin = P.off_chk2 + align16(m * 8); // ordered path only; inside chk2's upper half
   } else {
     P.off_chk1 = take(m * 8);
@@ -477,9 +486,18 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     const int delta = (P.off_y + align16(c->n * 8)) - P.off_chk1;
     P.off_e = P.off_y;
     for (int *x : {&P.off_chk1, &P.off_chk2, &P.off_amin, &P.off_amask, &P.off_sbits, &P.off_zbits,
-                   &P.off_blkv, &P.off_blki, &P.off_flips, &P.off_offs, &P.off_red, &P.off_misc})
+                   &P.off_blkv, &P.off_blki, &P.off_flips, &P.off_offs, &P.off_red, &P.off_misc,
+                   &P.off_fa, &P.off_fb, &P.off_m2s, &P.off_a2m, &P.off_corr})
       *x += delta;
     P.smem_bytes += delta;
+  }
+  if (circ) {
+    // column n (even) reads check (n - c_j) mod N at float index n + N - c_j of
+    // the min1 copy whose pairs are 8-byte aligned for that parity
+    for (int j = 0; j < c->w; ++j) {
+      const int d = c->n - c->off[j];
+      P.uoff[j] = ((d & 1) ? P.off_fb + 4 : P.off_fa) + 4 * d;
+    }
   }
   if (P.smem_bytes > c->smem_optin)
     return fail(FWBF_EUNSUPPORTED, "frame state needs %d B of shared memory (device max %d)",

@@ -100,35 +100,36 @@ __device__ __forceinline__ unsigned long long fsub2(unsigned long long a, unsign
   return r;
 }
 
-// Split-fp32 gather step for a pair of column slots (Q, Q+1): select min1 or
-// min2 per column, load float32, split v = h + l exactly on the grid G
-// (t = v + C, h = t - C, l = v - h with C = 1.5 * 2^23 * G), accumulate h and
-// l in separate fp32 accumulators.  Exact under the float32 guard (see kernel).
 template <int KC> struct SplitPairs { static constexpr int value = KC / 2 > 0 ? KC / 2 : 1; };
 
-template <int Q, int KC, int TB, bool GO = (Q + 1 < KC)> struct GatherS {
-  static __device__ __forceinline__ void run(unsigned long long (&hi)[SplitPairs<KC>::value],
-                                             unsigned long long (&lo)[SplitPairs<KC>::value],
-                                             const uint32_t (&mk)[KC], uint32_t bit, uint32_t a1,
-                                             uint32_t a2, unsigned long long cc) {
-    const uint32_t p0 = (mk[Q] & bit) ? a2 : a1;
-    const uint32_t p1 = (mk[Q + 1] & bit) ? a2 : a1;
-    float v0, v1;
-    asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v0) : "r"(p0), "n"(Q * TB * 4));
-    asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v1) : "r"(p1), "n"((Q + 1) * TB * 4));
-    const unsigned long long v = f2pack(v0, v1);
+// Split-fp32 gather step for column pair slot QP: one 8-byte load brings the
+// float32 signed min1 of two adjacent columns (n, n+1); each value v is split
+// exactly as v = h + l on the grid G (t = v + C, h = t - C, l = v - h, with
+// C = 1.5 * 2^23 * G), and h, l are accumulated in separate fp32x2 sums.
+template <int QP, int NP, int TB, bool GO = (QP < NP)> struct GatherP2 {
+  static __device__ __forceinline__ void run(unsigned long long (&hi)[NP], unsigned long long (&lo)[NP],
+                                             uint32_t a, unsigned long long cc) {
+    unsigned long long v;
+    asm volatile("ld.shared.b64 %0, [%1+%2];" : "=l"(v) : "r"(a), "n"(QP * TB * 8));
     const unsigned long long h = fsub2(fadd2(v, cc), cc);
-    hi[Q / 2] = fadd2(hi[Q / 2], h);
-    lo[Q / 2] = fadd2(lo[Q / 2], fsub2(v, h));
-    GatherS<Q + 2, KC, TB>::run(hi, lo, mk, bit, a1, a2, cc);
+    hi[QP] = fadd2(hi[QP], h);
+    lo[QP] = fadd2(lo[QP], fsub2(v, h));
+    GatherP2<QP + 1, NP, TB>::run(hi, lo, a, cc);
   }
 };
-template <int Q, int KC, int TB> struct GatherS<Q, KC, TB, false> {
-  static __device__ __forceinline__ void run(unsigned long long (&)[SplitPairs<KC>::value],
-                                             unsigned long long (&)[SplitPairs<KC>::value],
-                                             const uint32_t (&)[KC], uint32_t, uint32_t, uint32_t,
+template <int QP, int NP, int TB> struct GatherP2<QP, NP, TB, false> {
+  static __device__ __forceinline__ void run(unsigned long long (&)[NP], unsigned long long (&)[NP], uint32_t,
                                              unsigned long long) {}
 };
+
+// Exact argmin corrections as two int32 limbs: D = lo + hi * 2^24 with
+// lo in [0, 2^24) (D an integer multiple of the frame quantum q).
+__device__ __forceinline__ void corr_add(int *corr, int col, long long D, int sign) {
+  const int lo = (int)(D & 0xffffffll);
+  const int hi = (int)(D >> 24);
+  atomicAdd(&corr[2 * col], sign * lo);
+  atomicAdd(&corr[2 * col + 1], sign * hi);
+}
 
 template <typename YT>
 __device__ __forceinline__ YT load_y(const KParams &P, long long f, int n) {
@@ -171,7 +172,7 @@ decode_kernel(const __grid_constant__ KParams P) {
   int *misc = reinterpret_cast<int *>(smem_raw + P.off_misc);
   float *redf = reinterpret_cast<float *>(smem_raw + P.off_misc + 16 * 4);
   // misc slots
-  enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR };
+  enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR, S_EQ };
 
   const int W = WT ? WT : P.w;       // circulant weight (0 explicit); compile-time when WT > 0
   const int aw = (W > 32) ? 2 : 1;   // amask words per column
@@ -231,6 +232,11 @@ decode_kernel(const __grid_constant__ KParams P) {
         lmax = fmaxf(lmax, a);
         if (CIRC) {
           for (int q = 0; q < aw; ++q) amask[n * aw + q] = 0u;
+          if (WT > 0 && sizeof(YT) == 4) {
+            int *cz = reinterpret_cast<int *>(smem_raw + P.off_corr);
+            cz[2 * n] = 0;
+            cz[2 * n + 1] = 0;
+          }
         }
       }
     }
@@ -267,6 +273,7 @@ decode_kernel(const __grid_constant__ KParams P) {
             fast = 2;
             cmag = ldexpf(1.5f, 20 + e);
           }
+          misc[S_EQ] = e - 23; // quantum q = 2^(e-23)
         }
       }
       redf[0] = cmag;
@@ -277,6 +284,13 @@ decode_kernel(const __grid_constant__ KParams P) {
     const bool fastp = fpath != 0;
     const bool split = fpath == 2;
     const float cmag = redf[0];
+    const double qexp = split ? ldexp(1.0, misc[S_EQ]) : 0.0;      // q
+    const double qinv = split ? ldexp(1.0, -misc[S_EQ]) : 0.0;     // 1/q
+    float *sFA = reinterpret_cast<float *>(smem_raw + P.off_fa);   // split: signed min1, 8B-aligned at even n
+    float *sFB = reinterpret_cast<float *>(smem_raw + P.off_fb);   // split: same, shifted by one element
+    float *sM2 = reinterpret_cast<float *>(smem_raw + P.off_m2s);  // split: |min2| per check
+    int *sA2 = reinterpret_cast<int *>(smem_raw + P.off_a2m);      // split: argmin column per check
+    int *sCorr = reinterpret_cast<int *>(smem_raw + P.off_corr);   // split: per column (lo, hi) limbs
 
     // ---------------- init 2: per-check minima, syndrome, signed weights --------
     uint32_t sprev = 0; // syndrome bits of this thread's checks tid + k*T
@@ -319,19 +333,16 @@ decode_kernel(const __grid_constant__ KParams P) {
         const double sg = par ? 1.0 : -1.0;
         const double d1 = (double)min1, d2 = (double)min2;
         if (CIRC && split) {
-          float *f1 = reinterpret_cast<float *>(chk1);
-          float *f2 = reinterpret_cast<float *>(smem_raw + P.off_chk1 + P.d21f);
           const float s1v = par ? (float)min1 : -(float)min1;
-          const float s2v = par ? (float)min2 : -(float)min2;
-          f1[m] = s1v;
-          f1[m + N] = s1v;
-          f2[m] = s2v;
-          f2[m + N] = s2v;
-          if (P.wmode == FWBF_WEIGHTS_IMWBF) {
-            int d = ac - m;
-            if (d < 0) d += N;
-            const int j = P.offpos[d];
-            atomicOr(&amask[ac * aw + (j >> 5)], 1u << (j & 31));
+          sFA[m] = s1v;
+          sFA[m + N] = s1v;
+          sFB[m + 1] = s1v;
+          sFB[m + N + 1] = s1v;
+          sM2[m] = (float)min2;
+          sA2[m] = ac;
+          if (P.wmode == FWBF_WEIGHTS_IMWBF) { // column ac reads min2: + sgn*(min2-min1)
+            const long long D = (long long)__dmul_rn(__dsub_rn(d2, d1), qinv);
+            corr_add(sCorr, ac, par ? D : -D, 1);
           }
         } else if (CIRC && fastp) {
           chk1[m] = sg * d1;
@@ -381,35 +392,37 @@ decode_kernel(const __grid_constant__ KParams P) {
       // ---- Eq.(1) metric for every bit -> Ebuf ----
       if (tid == 0) misc[S_F] = 0; // last read before the previous refresh barrier
       if (WT > 0 && CIRC && split && (KC % 2) == 0) {
-        // Split-fp32 gather (4 B per edge instead of 8): float32 signed min1 /
-        // min2 in doubled arrays; each value v = h + l with h on the grid G and
-        // l = v - h, both exact; hi = sum h (multiples of G, |hi| < 2^24 G) and
-        // lo = sum l (multiples of q, |lo| <= 16 G <= 2^24 q) are exact in fp32,
-        // so hi + lo in fp64 is the exact column sum (= the reference's).
-        unsigned long long hi[SplitPairs<KC>::value], lo[SplitPairs<KC>::value];
+        // Split-fp32 gather, 4 B per edge and no per-edge argmin select:
+        // thread tid owns column pairs (2 tid + 2 T qp, +1).  Column n reads
+        // check (n - c_j) mod N; for even n the pair's two values are adjacent,
+        // loaded with one 8-byte LDS from sFA (N - c_j even) or from the
+        // one-element-shifted copy sFB (N - c_j odd).  v = h + l exactly on the
+        // grid G; hi = sum h (multiples of G, |hi| < 2^24 G) and lo = sum l
+        // (multiples of q, |lo| <= 16 G <= 2^24 q) are exact in fp32.  The
+        // argmin columns' min2 - min1 terms come from exact integer limbs
+        // (sCorr).  Every sum is exact, hence equal to the reference's.
+        constexpr int NP = SplitPairs<KC>::value;
+        unsigned long long hi[NP], lo[NP];
 #pragma unroll
-        for (int qp = 0; qp < KC / 2; ++qp) { hi[qp] = 0ull; lo[qp] = 0ull; }
+        for (int qp = 0; qp < NP; ++qp) { hi[qp] = 0ull; lo[qp] = 0ull; }
         const unsigned long long cc = f2pack(cmag, cmag);
-        const uint32_t s1 = (uint32_t)__cvta_generic_to_shared(reinterpret_cast<float *>(chk1) + N + tid);
-        const uint32_t d21 = (uint32_t)P.d21f;
-        uint32_t mk[KC], mkh[KC];
+        // per-thread part of the address, plus a warp-uniform part per j
+        const uint32_t baseT = (uint32_t)__cvta_generic_to_shared(smem_raw) + 8u * (uint32_t)tid;
 #pragma unroll
-        for (int q = 0; q < KC; ++q) { mk[q] = am[q][0]; mkh[q] = am[q][1]; }
+        for (int j = 0; j < (WT > 0 ? WT : 1); ++j) // P.uoff[j]: host-computed uniform part
+          GatherP2<0, NP, TB>::run(hi, lo, baseT + (uint32_t)P.uoff[j], cc);
 #pragma unroll
-        for (int j = 0; j < (WT > 0 ? WT : 1); ++j) {
-          const uint32_t a1 = s1 - 4u * (uint32_t)P.off[j];
-          if (j < 32) GatherS<0, KC, TB>::run(hi, lo, mk, 1u << (j & 31), a1, a1 + d21, cc);
-          else GatherS<0, KC, TB>::run(hi, lo, mkh, 1u << (j & 31), a1, a1 + d21, cc);
-        }
-#pragma unroll
-        for (int qp = 0; qp < KC / 2; ++qp) {
+        for (int qp = 0; qp < NP; ++qp) {
           const float2 h = f2unpack(hi[qp]);
           const float2 l = f2unpack(lo[qp]);
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            const int n = tid + (2 * qp + u) * T;
+            const int n = 2 * tid + 2 * T * qp + u;
             if (n < N) {
-              const double acc = __dadd_rn((double)(u ? h.y : h.x), (double)(u ? l.y : l.x));
+              double acc = __dadd_rn((double)(u ? h.y : h.x), (double)(u ? l.y : l.x));
+              const int2 cv = reinterpret_cast<const int2 *>(sCorr)[n];
+              if (cv.x | cv.y)
+                acc = __dadd_rn(acc, __dmul_rn((double)(((long long)cv.y << 24) + cv.x), qexp));
               const double ay = P.alias_y ? fabs((double)load_y<YT>(P, f, n)) : fabs((double)ybuf[n]);
               Ebuf[n] = __dsub_rn(acc, __dmul_rn(P.alpha, ay));
             }
@@ -702,13 +715,22 @@ decode_kernel(const __grid_constant__ KParams P) {
             const bool tog = ok && (s != (bool)((sprev >> kk) & 1u));
             if (tog) {
               if (CIRC && split) {
-                float *f1 = reinterpret_cast<float *>(chk1);
-                float *f2 = reinterpret_cast<float *>(smem_raw + P.off_chk1 + P.d21f);
-                const float v1 = -f1[m], v2 = -f2[m];
-                f1[m] = v1;
-                f1[m + N] = v1;
-                f2[m] = v2;
-                f2[m + N] = v2;
+                const float v1 = -sFA[m];
+                sFA[m] = v1;
+                sFA[m + N] = v1;
+                sFB[m + 1] = v1;
+                sFB[m + N + 1] = v1;
+                if (P.wmode == FWBF_WEIGHTS_IMWBF) { // correction sign flips with s_m
+                  const double dm = __dsub_rn((double)sM2[m], fabs((double)v1));
+                  const long long D = (long long)__dmul_rn(dm, qinv);
+                  const long long dn = s ? D : -D; // new sgn*(min2-min1)/q
+                  const int a2 = sA2[m];
+                  // limbs(dn) - limbs(-dn): the old contribution was -dn
+                  const int dlo = (int)(dn & 0xffffffll) - (int)((-dn) & 0xffffffll);
+                  const int dhi = (int)(dn >> 24) - (int)((-dn) >> 24);
+                  atomicAdd(&sCorr[2 * a2], dlo);
+                  atomicAdd(&sCorr[2 * a2 + 1], dhi);
+                }
               } else {
                 const double v1 = -chk1[m];
                 const double v2 = -chk2[m];

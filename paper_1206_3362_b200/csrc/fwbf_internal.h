@@ -68,7 +68,9 @@ struct KParams {
   int off_blkv, off_blki, off_flips, off_offs, off_red, off_misc;
   int smem_bytes;
   int alias_y; // metric buffer overlays y; alpha*|y| re-read from global
-  int d21f;    // split-fp32 path: byte offset of the float min2 array from chk1
+  int d21f;    // (unused)
+  int off_fa, off_fb, off_m2s, off_a2m, off_corr; // split-fp32 path arrays (inside the chk region)
+  int uoff[kMaxCircWeight]; // split-fp32 gather: byte offset of check (n - c_j) for even n, minus 4n
   int no_split; // disable the split-fp32 path (testing)
 };
 
