@@ -288,7 +288,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     const double qinv = split ? ldexp(1.0, -misc[S_EQ]) : 0.0;     // 1/q
     float *sFA = reinterpret_cast<float *>(smem_raw + P.off_fa);   // split: signed min1, 8B-aligned at even n
     float *sFB = reinterpret_cast<float *>(smem_raw + P.off_fb);   // split: same, shifted by one element
-    float *sM2 = reinterpret_cast<float *>(smem_raw + P.off_m2s);  // split: |min2| per check
+    int *sM2 = reinterpret_cast<int *>(smem_raw + P.off_m2s);      // split: correction limb deltas per check
     int *sA2 = reinterpret_cast<int *>(smem_raw + P.off_a2m);      // split: argmin column per check
     int *sCorr = reinterpret_cast<int *>(smem_raw + P.off_corr);   // split: per column (lo, hi) limbs
 
@@ -338,11 +338,15 @@ decode_kernel(const __grid_constant__ KParams P) {
           sFA[m + N] = s1v;
           sFB[m + 1] = s1v;
           sFB[m + N + 1] = s1v;
-          sM2[m] = (float)min2;
           sA2[m] = ac;
           if (P.wmode == FWBF_WEIGHTS_IMWBF) { // column ac reads min2: + sgn*(min2-min1)
-            const long long D = (long long)__dmul_rn(__dsub_rn(d2, d1), qinv);
+            const long long D = (long long)__dmul_rn(__dsub_rn(d2, d1), qinv); // exact integer
             corr_add(sCorr, ac, par ? D : -D, 1);
+            // limb change when s_m goes 0 -> 1 (negated for 1 -> 0)
+            int2 dl;
+            dl.x = (int)(D & 0xffffffll) - (int)((-D) & 0xffffffll);
+            dl.y = (int)(D >> 24) - (int)((-D) >> 24);
+            reinterpret_cast<int2 *>(sM2)[m] = dl;
           }
         } else if (CIRC && fastp) {
           chk1[m] = sg * d1;
@@ -721,15 +725,10 @@ decode_kernel(const __grid_constant__ KParams P) {
                 sFB[m + 1] = v1;
                 sFB[m + N + 1] = v1;
                 if (P.wmode == FWBF_WEIGHTS_IMWBF) { // correction sign flips with s_m
-                  const double dm = __dsub_rn((double)sM2[m], fabs((double)v1));
-                  const long long D = (long long)__dmul_rn(dm, qinv);
-                  const long long dn = s ? D : -D; // new sgn*(min2-min1)/q
+                  const int2 dl = reinterpret_cast<const int2 *>(sM2)[m];
                   const int a2 = sA2[m];
-                  // limbs(dn) - limbs(-dn): the old contribution was -dn
-                  const int dlo = (int)(dn & 0xffffffll) - (int)((-dn) & 0xffffffll);
-                  const int dhi = (int)(dn >> 24) - (int)((-dn) >> 24);
-                  atomicAdd(&sCorr[2 * a2], dlo);
-                  atomicAdd(&sCorr[2 * a2 + 1], dhi);
+                  atomicAdd(&sCorr[2 * a2], s ? dl.x : -dl.x);
+                  atomicAdd(&sCorr[2 * a2 + 1], s ? dl.y : -dl.y);
                 }
               } else {
                 const double v1 = -chk1[m];
