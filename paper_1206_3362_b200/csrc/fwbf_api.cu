@@ -516,9 +516,28 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   if (per_sm < 1) return fail(FWBF_EUNSUPPORTED, "kernel does not fit on an SM");
   const long long grid = std::min<long long>(batch, (long long)per_sm * c->sm_count);
   CUDA_TRY(cudaMemsetAsync(P.work_counter, 0, sizeof(unsigned), stream));
+  static long long *phase_buf = nullptr;
+  const bool phases = getenv("FWBF_PHASES") != nullptr;
+  if (phases) {
+    if (!phase_buf) CUDA_TRY(cudaMalloc((void **)&phase_buf, 8 * sizeof(long long)));
+    CUDA_TRY(cudaMemsetAsync(phase_buf, 0, 8 * sizeof(long long), stream));
+    P.phase_cycles = phase_buf;
+  }
   void *args[] = {&P};
   CUDA_TRY(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(T), args, P.smem_bytes, stream));
   CUDA_TRY(cudaGetLastError());
+  if (phases) {
+    long long h[8];
+    CUDA_TRY(cudaMemcpyAsync(h, phase_buf, sizeof h, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    long long tot = 0;
+    for (int i = 0; i < 8; ++i) tot += h[i];
+    static const char *names[8] = {"outputs+fetch", "init1", "init2", "gather", "select+apply",
+                                   "post+refresh", "-", "-"};
+    fprintf(stderr, "[fwbf phases] grid=%lld T=%d smem=%d:", grid, T, P.smem_bytes);
+    for (int i = 0; i < 6; ++i) fprintf(stderr, " %s %.1f%%", names[i], tot ? 100.0 * h[i] / tot : 0.0);
+    fprintf(stderr, "\n");
+  }
   return FWBF_OK;
 }
 

@@ -195,6 +195,16 @@ decode_kernel(const __grid_constant__ KParams P) {
   }
   const int sel_rounds = (P.nblocks + sel_gpc - 1) / sel_gpc;
 
+  // optional per-phase cycle accounting (thread 0, at CTA-wide barriers)
+  long long ph_t = 0;
+  long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define FWBF_PH(i)                                              \
+  if (P.phase_cycles && tid == 0) {                             \
+    const long long t_ = clock64();                             \
+    if (ph_t) ph_acc[i] += t_ - ph_t;                           \
+    ph_t = t_;                                                  \
+  }
+
   // per-CTA counter accumulation (thread 0)
   long long c_frames = 0, c_biterr = 0, c_worderr = 0, c_iters = 0, c_flips = 0,
             c_stalls = 0, c_conv = 0, c_ordered = 0, c_edges = 0;
@@ -207,6 +217,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     __syncthreads();
     if (tid == 0) misc[S_FRAME] = (int)atomicAdd(P.work_counter, 1u);
     __syncthreads();
+    FWBF_PH(0)
     const long long f = misc[S_FRAME];
     if (f >= P.batch) break;
 
@@ -250,6 +261,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     if (lane == 0) { redf[warp] = lmin; redf[32 + warp] = lmax; if (nonfin) misc[S_NONFIN] = 1; }
     if (tid == 0) { misc[S_SWT] = 0; misc[S_F] = 0; }
     __syncthreads();
+    FWBF_PH(1)
     if (tid == 0) {
       float mn = INFINITY, mx = 0.f;
       for (int w2 = 0; w2 < nwarps; ++w2) { mn = fminf(mn, redf[w2]); mx = fmaxf(mx, redf[32 + w2]); }
@@ -368,6 +380,7 @@ decode_kernel(const __grid_constant__ KParams P) {
       }
     }
     __syncthreads();
+    FWBF_PH(2)
 
     // ---------------- guarded path: per-column argmin masks into registers -----
     // Bit j of am[q] says column tid + q*T is the argmin of its j-th check
@@ -502,6 +515,7 @@ decode_kernel(const __grid_constant__ KParams P) {
         }
       }
       __syncthreads();
+      FWBF_PH(3)
 
       // ---- selection (+ fused flips for FWBF) ----
       if (tid == 0) misc[S_SWT] = 0; // every thread read it at the loop top (before the E barrier)
@@ -558,6 +572,7 @@ decode_kernel(const __grid_constant__ KParams P) {
           }
         }
         __syncthreads();
+        FWBF_PH(4)
         F = misc[S_F];
         if (F > 0) {
           applied = true;
@@ -764,6 +779,7 @@ decode_kernel(const __grid_constant__ KParams P) {
       }
       k += 1;
       __syncthreads();
+      FWBF_PH(5)
     }
 
     // ---------------- outputs ----------------------------------------------------
@@ -806,6 +822,9 @@ decode_kernel(const __grid_constant__ KParams P) {
     }
   }
 
+  if (P.phase_cycles && tid == 0)
+    for (int i = 0; i < 8; ++i) atomicAdd((unsigned long long *)&P.phase_cycles[i], (unsigned long long)ph_acc[i]);
+#undef FWBF_PH
   if (tid == 0 && P.counters && c_frames) {
     unsigned long long *c = (unsigned long long *)P.counters;
     atomicAdd(c + FWBF_CNT_FRAMES, (unsigned long long)c_frames);

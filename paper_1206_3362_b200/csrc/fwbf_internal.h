@@ -63,6 +63,7 @@ struct KParams {
   void *y_out;
   long long y_out_ld;
   unsigned int *work_counter;
+  long long *phase_cycles; // optional [8] per-phase cycle sums (FWBF_PHASES=1)
   // ---- shared memory layout (byte offsets) ----
   int off_y, off_e, off_chk1, off_chk2, off_amin, off_amask, off_sbits, off_zbits;
   int off_blkv, off_blki, off_flips, off_offs, off_red, off_misc;
