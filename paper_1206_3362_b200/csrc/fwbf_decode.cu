@@ -196,13 +196,13 @@ decode_kernel(const __grid_constant__ KParams P) {
   const int sel_rounds = (P.nblocks + sel_gpc - 1) / sel_gpc;
 
   // optional per-phase cycle accounting (thread 0, at CTA-wide barriers)
-  long long ph_t = 0;
-  long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  __shared__ long long ph_acc[9]; // [8] = last timestamp
+  if (tid < 9) ph_acc[tid] = 0;
 #define FWBF_PH(i)                                              \
   if (P.phase_cycles && tid == 0) {                             \
     const long long t_ = clock64();                             \
-    if (ph_t) ph_acc[i] += t_ - ph_t;                           \
-    ph_t = t_;                                                  \
+    if (ph_acc[8]) ph_acc[i] += t_ - ph_acc[8];                 \
+    ph_acc[8] = t_;                                             \
   }
 
   // per-CTA counter accumulation (thread 0)
