@@ -538,17 +538,9 @@ decode_kernel(const __grid_constant__ KParams P) {
           if (ok) {
             const int base = b * p;
             const int lim = min(p, N - base);
-            // 8 independent loads per chunk, then the ascending compare chain
-            for (int o0 = sub; o0 < lim; o0 += 8 * TPB) {
-              double e[8];
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                const int o = o0 + u * TPB;
-                e[u] = o < lim ? Ebuf[base + o] : -dinf();
-              }
-#pragma unroll
-              for (int u = 0; u < 8; ++u)
-                if (e[u] > v) { v = e[u]; i = base + o0 + u * TPB; }
+            for (int o = sub; o < lim; o += TPB) {
+              const double e = Ebuf[base + o];
+              if (e > v) { v = e; i = base + o; }
             }
           }
           for (int off = TPB >> 1; off; off >>= 1) {
@@ -564,7 +556,6 @@ decode_kernel(const __grid_constant__ KParams P) {
                 atomicAdd(&misc[S_F], 1);
               }
               if (CIRC) {
-#pragma unroll 8
                 for (int j = sub; j < W; j += TPB) {
                   int m = i - offs_s[j];
                   if (m < 0) m += N;
