@@ -32,6 +32,10 @@
 #include "fwbf_internal.h"
 #include "fwbf_noise.cuh"
 
+#ifndef FWBF_MINB_256
+#define FWBF_MINB_256 5
+#endif
+
 namespace fwbf {
 
 #define FULL_MASK 0xffffffffu
@@ -144,7 +148,7 @@ __device__ __forceinline__ YT load_y(const KParams &P, long long f, int n) {
 //   KC   : columns per thread on the guarded path (register accumulators)
 // ---------------------------------------------------------------------------
 template <typename YT, bool CIRC, int KC, int TB, bool NOISE, int WT>
-__global__ void __launch_bounds__(TB ? TB : 1024, 1024 / (TB ? TB : 1024))
+__global__ void __launch_bounds__(TB ? TB : 1024, TB == 256 ? FWBF_MINB_256 : 1024 / (TB ? TB : 1024))
 decode_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
@@ -301,7 +305,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     float *sFA = reinterpret_cast<float *>(smem_raw + P.off_fa);   // split: signed min1, 8B-aligned at even n
     float *sFB = reinterpret_cast<float *>(smem_raw + P.off_fb);   // split: same, shifted by one element
     int *sM2 = reinterpret_cast<int *>(smem_raw + P.off_m2s);      // split: correction limb deltas per check
-    int *sA2 = reinterpret_cast<int *>(smem_raw + P.off_a2m);      // split: argmin column per check
+    uint16_t *sA2 = reinterpret_cast<uint16_t *>(smem_raw + P.off_a2m); // split: argmin column per check
     int *sCorr = reinterpret_cast<int *>(smem_raw + P.off_corr);   // split: per column (lo, hi) limbs
 
     // ---------------- init 2: per-check minima, syndrome, signed weights --------
@@ -350,7 +354,7 @@ decode_kernel(const __grid_constant__ KParams P) {
           sFA[m + N] = s1v;
           sFB[m + 1] = s1v;
           sFB[m + N + 1] = s1v;
-          sA2[m] = ac;
+          sA2[m] = (uint16_t)ac;
           if (P.wmode == FWBF_WEIGHTS_IMWBF) { // column ac reads min2: + sgn*(min2-min1)
             const long long D = (long long)__dmul_rn(__dsub_rn(d2, d1), qinv); // exact integer
             corr_add(sCorr, ac, par ? D : -D, 1);
