@@ -33,7 +33,7 @@
 #include "fwbf_noise.cuh"
 
 #ifndef FWBF_MINB_256
-#define FWBF_MINB_256 5
+#define FWBF_MINB_256 4
 #endif
 
 namespace fwbf {
