@@ -198,9 +198,6 @@ decode_kernel(const __grid_constant__ KParams P) {
     sel_slot = (hw / tpb) * 16 + tpb * (sel_slot & (half - 1)) + (hw % tpb);
   }
   const int sel_rounds = (P.nblocks + sel_gpc - 1) / sel_gpc;
-  // circulant: this lane's check offsets c_lane, c_{lane+32} (flip toggles)
-  const int my_off0 = (CIRC && lane < P.w) ? P.off[lane] : 0;
-  const int my_off1 = (CIRC && lane + 32 < P.w) ? P.off[lane + 32] : 0;
 
   // optional per-phase cycle accounting (thread 0, at CTA-wide barriers)
   __shared__ long long ph_acc[9]; // [8] = last timestamp
@@ -555,37 +552,26 @@ decode_kernel(const __grid_constant__ KParams P) {
             const int i2 = __shfl_xor_sync(FULL_MASK, i, off);
             amax_combine(v, i, v2, i2);
           }
-          if (ok && sub == 0) { blk_v[b] = v; blk_i[b] = i; }
-          if (CIRC) {
-            // the warp applies its groups' flips one at a time, lane j toggling
-            // check i - c_j (offset held in a register): one atomic per lane
-            uint32_t fm = __ballot_sync(FULL_MASK, ok && sub == 0 && v > 0.0);
-            if (lane == 0 && fm) atomicAdd(&misc[S_F], __popc(fm));
-            while (fm) {
-              const int src = __ffs(fm) - 1;
-              fm &= fm - 1;
-              const int fi = __shfl_sync(FULL_MASK, i, src);
-              if (lane == src) atomicXor(&zbits[fi >> 5], 1u << (fi & 31));
-              if (lane < W) {
-                int m = fi - my_off0;
-                if (m < 0) m += N;
-                atomicXor(&sbits[m >> 5], 1u << (m & 31));
+          if (ok) {
+            if (sub == 0) { blk_v[b] = v; blk_i[b] = i; }
+            if (v > 0.0) {
+              if (sub == 0) {
+                atomicXor(&zbits[i >> 5], 1u << (i & 31));
+                atomicAdd(&misc[S_F], 1);
               }
-              if (lane + 32 < W) {
-                int m = fi - my_off1;
-                if (m < 0) m += N;
-                atomicXor(&sbits[m >> 5], 1u << (m & 31));
+              if (CIRC) {
+                for (int j = sub; j < W; j += TPB) {
+                  int m = i - offs_s[j];
+                  if (m < 0) m += N;
+                  atomicXor(&sbits[m >> 5], 1u << (m & 31));
+                }
+              } else {
+                const int e1 = __ldg(P.col_ptr + i + 1);
+                for (int e = __ldg(P.col_ptr + i) + sub; e < e1; e += TPB) {
+                  const int m = __ldg(P.col_idx + e);
+                  atomicXor(&sbits[m >> 5], 1u << (m & 31));
+                }
               }
-            }
-          } else if (ok && v > 0.0) {
-            if (sub == 0) {
-              atomicXor(&zbits[i >> 5], 1u << (i & 31));
-              atomicAdd(&misc[S_F], 1);
-            }
-            const int e1 = __ldg(P.col_ptr + i + 1);
-            for (int e = __ldg(P.col_ptr + i) + sub; e < e1; e += TPB) {
-              const int m = __ldg(P.col_idx + e);
-              atomicXor(&sbits[m >> 5], 1u << (m & 31));
             }
           }
         }
