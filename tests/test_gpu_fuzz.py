@@ -1,0 +1,71 @@
+"""Randomised parity: random small codes (regular, irregular, circulant), random
+decoder knobs, random inputs (including ties and zeros) -- CUDA vs oracle, bit-exact."""
+
+import numpy as np
+import pytest
+
+from oracle import wbf_oracle as O
+from paper_1206_3362_b200 import DecoderConfig, ParityCheckMatrix, decode_batch, eg_ldpc, gallager_rc
+
+pytestmark = pytest.mark.gpu
+
+
+def random_code(rng):
+    kind = rng.integers(0, 4)
+    if kind == 0:
+        return eg_ldpc(int(rng.integers(2, 5)))
+    if kind == 1:
+        dv = int(rng.choice([2, 3, 4]))
+        dc = int(rng.choice([4, 6, 8]))
+        n = dc * int(rng.integers(4, 20))
+        try:
+            return gallager_rc(n, dv, dc, seed=int(rng.integers(1 << 30)))
+        except RuntimeError:
+            return eg_ldpc(3)
+    if kind == 2:  # irregular random rows (weights 2..7), possibly with 4-cycles
+        n = int(rng.integers(10, 120))
+        m = int(rng.integers(3, n))
+        rows = [np.sort(rng.choice(n, size=int(rng.integers(2, min(8, n) + 1)), replace=False))
+                for _ in range(m)]
+        return ParityCheckMatrix(rows, n)
+    # circulant from a random offset set (not necessarily RC-free)
+    n = int(rng.integers(20, 300))
+    w = int(rng.integers(2, 12))
+    first = np.sort(rng.choice(n, size=w, replace=False))
+    return ParityCheckMatrix([(first + i) % n for i in range(n)], n)
+
+
+def random_y(rng, n, frames):
+    sigma = float(rng.uniform(0.3, 0.9))
+    y = 1.0 + sigma * rng.standard_normal((frames, n))
+    mode = rng.integers(0, 3)
+    if mode == 1:
+        y = np.round(y * 4) / 4  # ties and exact zeros
+    y = y.astype(np.float32 if rng.integers(0, 2) else np.float64)
+    return y
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_parity(cuda_device, seed):
+    rng = np.random.default_rng(1000 + seed)
+    h = random_code(rng)
+    n = h.n_cols
+    alg = ["fwbf", "imwbf", "mlp"][int(rng.integers(0, 3))]
+    cfg = DecoderConfig(alpha=float(rng.choice([0.0, 0.2, 0.7, 1.5])), k_max=int(rng.integers(1, 40)),
+                        lam=int(rng.integers(1, min(12, n) + 1)), block_len_p=int(rng.integers(1, n + 8)),
+                        stall_policy=["flip-global-max", "terminate"][int(rng.integers(0, 2))],
+                        mlp_threshold=bool(rng.integers(0, 2)),
+                        weight_mode=["imwbf", "mwbf"][int(rng.integers(0, 2))])
+    y = random_y(rng, n, int(rng.integers(1, 40)))
+    res = decode_batch(h, y, cfg, alg, flip_log=True)
+    z = res.z()
+    its = res.iterations.cpu().numpy()
+    logs = res.flip_logs()
+    g = O.Graph.of(h)
+    for i in range(y.shape[0]):
+        r = O.decode(g, y[i], alg, alpha=cfg.alpha, k_max=cfg.k_max, lam=cfg.lam, p=cfg.block_len_p,
+                     stall=cfg.stall_policy, mlp_threshold=cfg.mlp_threshold, weight_mode=cfg.weight_mode)
+        assert its[i] == r.iterations, (seed, i)
+        assert logs[i] == r.flip_log, (seed, i)
+        assert np.array_equal(z[i], r.z), (seed, i)
+        assert res.converged[i] == r.converged and res.stalled[i] == r.stalled
