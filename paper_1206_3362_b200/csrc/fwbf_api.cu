@@ -532,10 +532,10 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     CUDA_TRY(cudaStreamSynchronize(stream));
     long long tot = 0;
     for (int i = 0; i < 8; ++i) tot += h[i];
-    static const char *names[8] = {"outputs+fetch", "init1", "init2", "gather", "apply",
-                                   "post+refresh", "select", "-"};
+    static const char *names[8] = {"outputs+fetch", "init1", "init2", "gather", "select+apply",
+                                   "post+refresh", "-", "-"};
     fprintf(stderr, "[fwbf phases] grid=%lld T=%d smem=%d:", grid, T, P.smem_bytes);
-    for (int i = 0; i < 7; ++i) fprintf(stderr, " %s %.1f%%", names[i], tot ? 100.0 * h[i] / tot : 0.0);
+    for (int i = 0; i < 6; ++i) fprintf(stderr, " %s %.1f%%", names[i], tot ? 100.0 * h[i] / tot : 0.0);
     fprintf(stderr, "\n");
   }
   return FWBF_OK;

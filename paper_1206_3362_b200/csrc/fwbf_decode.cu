@@ -198,9 +198,6 @@ decode_kernel(const __grid_constant__ KParams P) {
     sel_slot = (hw / tpb) * 16 + tpb * (sel_slot & (half - 1)) + (hw % tpb);
   }
   const int sel_rounds = (P.nblocks + sel_gpc - 1) / sel_gpc;
-  // circulant: this lane's check offsets c_lane, c_{lane+32} (flip toggles)
-  const int my_off0 = (CIRC && lane < P.w) ? P.off[lane] : 0;
-  const int my_off1 = (CIRC && lane + 32 < P.w) ? P.off[lane + 32] : 0;
 
   // optional per-phase cycle accounting (thread 0, at CTA-wide barriers)
   __shared__ long long ph_acc[9]; // [8] = last timestamp
@@ -556,48 +553,33 @@ decode_kernel(const __grid_constant__ KParams P) {
             amax_combine(v, i, v2, i2);
           }
           if (ok) {
-            if (sub == 0) {
-              blk_v[b] = v;
-              blk_i[b] = i;
-              if (v > 0.0) atomicAdd(&misc[S_F], 1);
-            }
-            if (!CIRC && v > 0.0) {
-              if (sub == 0) atomicXor(&zbits[i >> 5], 1u << (i & 31));
-              const int e1 = __ldg(P.col_ptr + i + 1);
-              for (int e = __ldg(P.col_ptr + i) + sub; e < e1; e += TPB) {
-                const int m = __ldg(P.col_idx + e);
-                atomicXor(&sbits[m >> 5], 1u << (m & 31));
+            if (sub == 0) { blk_v[b] = v; blk_i[b] = i; }
+            if (v > 0.0) {
+              if (sub == 0) {
+                atomicXor(&zbits[i >> 5], 1u << (i & 31));
+                atomicAdd(&misc[S_F], 1);
+              }
+              if (CIRC) {
+                for (int j = sub; j < W; j += TPB) {
+                  int m = i - offs_s[j];
+                  if (m < 0) m += N;
+                  atomicXor(&sbits[m >> 5], 1u << (m & 31));
+                }
+              } else {
+                const int e1 = __ldg(P.col_ptr + i + 1);
+                for (int e = __ldg(P.col_ptr + i) + sub; e < e1; e += TPB) {
+                  const int m = __ldg(P.col_idx + e);
+                  atomicXor(&sbits[m >> 5], 1u << (m & 31));
+                }
               }
             }
           }
         }
         __syncthreads();
-        FWBF_PH(6)
+        FWBF_PH(4)
         F = misc[S_F];
         if (F > 0) {
           applied = true;
-          if (CIRC) {
-            // every warp applies whole flips: block b -> warp b % nwarps, lane j
-            // toggles check i - c_j with its register-held offset
-            for (int bb = warp; bb < nb; bb += nwarps) {
-              if (blk_v[bb] > 0.0) { // warp-uniform
-                const int fi = blk_i[bb];
-                if (lane == 0) atomicXor(&zbits[fi >> 5], 1u << (fi & 31));
-                if (lane < W) {
-                  int m = fi - my_off0;
-                  if (m < 0) m += N;
-                  atomicXor(&sbits[m >> 5], 1u << (m & 31));
-                }
-                if (lane + 32 < W) {
-                  int m = fi - my_off1;
-                  if (m < 0) m += N;
-                  atomicXor(&sbits[m >> 5], 1u << (m & 31));
-                }
-              }
-            }
-            __syncthreads();
-          }
-          FWBF_PH(4)
           if (P.fliplog && warp == 0) { // ascending = block order
             int cnt = 0;
             for (int base = 0; base < nb; base += 32) {
