@@ -1,0 +1,64 @@
+"""Parity at scale: every BASELINE config, tens of thousands of frames, CUDA vs
+the C oracle (oracle/wbf_oracle.c, itself pinned to the reference fixtures).
+Bit-exact per frame: hard decisions, iterations, converged/stalled, flip count."""
+
+import numpy as np
+import pytest
+
+from oracle import wbf_oracle as O
+from oracle.c_oracle import COracle
+from paper_1206_3362_b200 import DecoderConfig, decode_batch
+from paper_1206_3362_b200.decoders import decode_awgn
+from tests.golden.codebook import build_code, code_rate
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # (code, alg, decoder kwargs, Eb/N0, frames)
+    ("eg5", "fwbf", dict(block_len_p=31, k_max=100), 4.0, 1 << 15),
+    ("eg5", "fwbf", dict(block_len_p=31, k_max=100), 3.0, 1 << 12),
+    ("eg5", "fwbf", dict(block_len_p=93, k_max=100), 3.5, 1 << 13),
+    ("eg5", "imwbf", dict(k_max=100, weight_mode="mwbf", alpha=0.0), 4.0, 1 << 11),
+    ("eg5", "mlp", dict(lam=10, k_max=100), 4.0, 1 << 13),
+    ("eg6", "fwbf", dict(block_len_p=128, k_max=100), 4.5, 1 << 11),
+    ("gal504", "fwbf", dict(block_len_p=24, k_max=50), 4.0, 10000),
+    ("qc4x32", "fwbf", dict(block_len_p=256, k_max=50), 5.0, 1 << 8),
+]
+
+
+def _cmp(res, z, its, fl, ft, tag):
+    gz = res.z()
+    git = res.iterations.cpu().numpy()
+    gfl = res.flags.cpu().numpy() & 3
+    gft = res.flips_total.cpu().numpy()
+    bad = np.nonzero((git != its) | (gfl != fl) | (gft != ft) | np.any(gz != z, axis=1))[0]
+    assert bad.size == 0, f"{tag}: {bad.size} frames differ, first {bad[:8]}"
+
+
+@pytest.mark.parametrize("code,alg,kw,ebn0,frames", CASES)
+def test_scale_parity_vs_c_oracle(cuda_device, code, alg, kw, ebn0, frames):
+    import torch
+    h = build_code(code)
+    sigma = O.ebn0_to_sigma(ebn0, code_rate(code))
+    g = torch.Generator(device="cuda").manual_seed(hash((code, ebn0, frames)) & 0xffffffff)
+    y = (1.0 + sigma * torch.randn((frames, h.n_cols), generator=g, device="cuda")).float()
+    cfg = DecoderConfig(**kw)
+    res = decode_batch(h, y, cfg, alg)
+    p = kw.get("block_len_p")
+    z, its, fl, ft = COracle(h).decode_batch(y.cpu().numpy(), algorithm=alg, alpha=cfg.alpha,
+                                             k_max=cfg.k_max, lam=cfg.lam, p=p,
+                                             weight_mode=cfg.weight_mode)
+    _cmp(res, z, its, fl, ft, f"{code}/{alg}/{ebn0}")
+
+
+@pytest.mark.parametrize("noise", ["f32", "f64"])
+def test_scale_parity_device_noise(cuda_device, noise):
+    """Config E path: the device draws the reference channel; the C oracle
+    decodes the very same values (returned by the kernel)."""
+    h = build_code("eg5")
+    sigma = O.ebn0_to_sigma(4.0, code_rate("eg5"))
+    cfg = DecoderConfig(block_len_p=31, k_max=100)
+    res = decode_awgn(h, cfg, "fwbf", 11, 1 << 20, 1 << 13, sigma, noise=noise, return_y=True)
+    z, its, fl, ft = COracle(h).decode_batch(res.y.cpu().numpy(), algorithm="fwbf", alpha=0.2,
+                                             k_max=100, p=31)
+    _cmp(res, z, its, fl, ft, f"awgn-{noise}")

@@ -58,3 +58,16 @@ def test_weights_spec_example():
     m1, m2, a = O.check_minima(g, np.array([0.5, 0.2, 0.9]))
     w = O.edge_weights(g, m1, m2, a)
     assert w.tolist() == [0.2, 0.5, 0.2]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_c_oracle_matches_reference_fixture(name):
+    from oracle.c_oracle import COracle
+    c = load_case(name)
+    co = COracle(build_code(c.meta["code"]))
+    z, its, fl, ft = co.decode_batch(c.y, algorithm=c.meta["algorithm"], **c.decoder_kwargs)
+    assert np.array_equal(z, c.z), name
+    assert np.array_equal(its, c.iterations), name
+    assert np.array_equal((fl & 1).astype(bool), c.converged)
+    assert np.array_equal((fl & 2).astype(bool), c.stalled)
+    assert np.array_equal(ft, c.flips_total)
