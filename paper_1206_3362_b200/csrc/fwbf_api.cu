@@ -57,6 +57,8 @@ struct fwbf_code {
   int16_t *d_offpos = nullptr;
   unsigned int *d_work = nullptr; // ring of per-launch work counters
   std::atomic<unsigned> work_slot{0};
+  int qc_z = 0, qc_jb = 0, qc_kb = 0;
+  short qc_shift[fwbf::kMaxQcBlocks];
   int sm_count = 0;
   int smem_optin = 0;
   // host pipeline scratch
@@ -169,6 +171,32 @@ extern "C" int fwbf_code_create(const fwbf_code_desc *desc, int device, fwbf_cod
     }
     offpos.assign(n, (int16_t)-1);
     for (int j = 0; j < w; ++j) offpos[desc->offsets[j]] = (int16_t)j;
+  }
+  if (!desc->circulant) {
+    // quasi-cyclic detection: every Z x Z block zero or one shifted identity
+    // (row i -> column (i + s) mod Z); Z a power of two, at most 256 blocks
+    for (int Z = 1024; Z >= 16 && !c->qc_z; Z >>= 1) {
+      if (n % Z || m % Z || (long long)(n / Z) * (m / Z) > fwbf::kMaxQcBlocks) continue;
+      const int jb = m / Z, kb = n / Z;
+      std::vector<int> sh(jb * kb, -2), cnt(jb * kb, 0);
+      bool okq = true;
+      for (int r = 0; r < m && okq; ++r)
+        for (int e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+          const int col = row_idx[e];
+          const int b = (r / Z) * kb + col / Z;
+          const int s = ((col % Z) - (r % Z) + Z) % Z;
+          if (sh[b] == -2) sh[b] = s;
+          else if (sh[b] != s) { okq = false; break; }
+          cnt[b]++;
+        }
+      for (int b = 0; b < jb * kb && okq; ++b)
+        if (cnt[b] != 0 && cnt[b] != Z) okq = false;
+      if (!okq) continue;
+      c->qc_z = Z;
+      c->qc_jb = jb;
+      c->qc_kb = kb;
+      for (int b = 0; b < jb * kb; ++b) c->qc_shift[b] = (short)(cnt[b] ? sh[b] : -1);
+    }
   }
   int rc;
   cudaError_t ce = cudaSetDevice(device);
@@ -369,6 +397,10 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   P.row_idx = c->d_row_idx;
   P.col_ptr = c->d_col_ptr;
   P.col_idx = c->d_col_idx;
+  P.qc_z = getenv("FWBF_NO_QC") ? 0 : c->qc_z;
+  P.qc_jb = c->qc_jb;
+  P.qc_kb = c->qc_kb;
+  memcpy(P.qc_shift, c->qc_shift, sizeof P.qc_shift);
   P.alg = p->algorithm;
   P.wmode = p->weight_mode;
   P.kmax = p->k_max;

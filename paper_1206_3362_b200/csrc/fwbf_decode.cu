@@ -327,6 +327,19 @@ decode_kernel(const __grid_constant__ KParams P) {
             if (a < min1 || (a == min1 && c < ac)) { min2 = min1; min1 = a; ac = c; }
             else if (a < min2) min2 = a;
           }
+        } else if (P.qc_z) {
+          // quasi-cyclic: row r*Z + i holds column cb*Z + ((i + s[r][cb]) mod Z)
+          const int Z = P.qc_z, r = m / Z, ii = m - r * Z;
+          for (int cb = 0; cb < P.qc_kb; ++cb) {
+            const int sh = P.qc_shift[r * P.qc_kb + cb];
+            if (sh < 0) continue;
+            const int c = cb * Z + ((ii + sh) & (Z - 1));
+            const YT yv = ybuf[c];
+            par ^= (yv < YT(0));
+            const YT a = fabs(yv);
+            if (a < min1 || (a == min1 && c < ac)) { min2 = min1; min1 = a; ac = c; }
+            else if (a < min2) min2 = a;
+          }
         } else {
           const int e0 = __ldg(P.row_ptr + m), e1 = __ldg(P.row_ptr + m + 1);
           for (int e = e0; e < e1; ++e) {
@@ -506,6 +519,17 @@ decode_kernel(const __grid_constant__ KParams P) {
               acc = __dadd_rn(acc, w);
               if (++ii == W) ii = 0;
             }
+          } else if (P.qc_z) {
+            // column cb*Z + o meets row block r at check r*Z + ((o - s) mod Z):
+            // ascending in r, i.e. the reference's ascending check order
+            const int Z = P.qc_z, cb = n / Z, o = n - cb * Z;
+            for (int r = 0; r < P.qc_jb; ++r) {
+              const int sh = P.qc_shift[r * P.qc_kb + cb];
+              if (sh < 0) continue;
+              const int m = r * Z + ((o - sh) & (Z - 1));
+              const double w = (amin[m] == n) ? chk2[m] : chk1[m];
+              acc = __dadd_rn(acc, w);
+            }
           } else {
             const int e0 = __ldg(P.col_ptr + n), e1 = __ldg(P.col_ptr + n + 1);
             for (int e = e0; e < e1; ++e) {
@@ -563,6 +587,14 @@ decode_kernel(const __grid_constant__ KParams P) {
                 for (int j = sub; j < W; j += TPB) {
                   int m = i - offs_s[j];
                   if (m < 0) m += N;
+                  atomicXor(&sbits[m >> 5], 1u << (m & 31));
+                }
+              } else if (P.qc_z) {
+                const int Z = P.qc_z, cb = i / Z, o = i - cb * Z;
+                for (int r = sub; r < P.qc_jb; r += TPB) {
+                  const int sh = P.qc_shift[r * P.qc_kb + cb];
+                  if (sh < 0) continue;
+                  const int m = r * Z + ((o - sh) & (Z - 1));
                   atomicXor(&sbits[m >> 5], 1u << (m & 31));
                 }
               } else {
@@ -703,6 +735,17 @@ decode_kernel(const __grid_constant__ KParams P) {
             for (int j = lane; j < W; j += 32) {
               int m = n - offs_s[j];
               if (m < 0) m += N;
+              atomicXor(&sbits[m >> 5], 1u << (m & 31));
+            }
+          }
+        } else if (P.qc_z) {
+          for (int fi = warp; fi < F; fi += nwarps) {
+            const int n = flips[fi];
+            const int Z = P.qc_z, cb = n / Z, o = n - cb * Z;
+            for (int r = lane; r < P.qc_jb; r += 32) {
+              const int sh = P.qc_shift[r * P.qc_kb + cb];
+              if (sh < 0) continue;
+              const int m = r * Z + ((o - sh) & (Z - 1));
               atomicXor(&sbits[m >> 5], 1u << (m & 31));
             }
           }

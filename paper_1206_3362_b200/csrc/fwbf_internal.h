@@ -5,6 +5,7 @@
 namespace fwbf {
 
 constexpr int kMaxCircWeight = 64; // circulant offsets kept in the parameter block
+constexpr int kMaxQcBlocks = 256;  // quasi-cyclic shift table entries in the parameter block
 
 // Guarded-path kernel shapes (threads TB, columns per thread KC): TB*KC >= n.
 // WT > 0: circulant weight fixed at compile time (fully unrolled gather).
@@ -30,6 +31,8 @@ struct KParams {
   const int16_t *offpos;    // circulant: offpos[d] = j if c_j == d else -1
   const int *row_ptr, *row_idx; // CSR, sorted columns
   const int *col_ptr, *col_idx; // CSC, ascending checks
+  int qc_z, qc_jb, qc_kb;       // quasi-cyclic structure (qc_z = 0: none); Z a power of two
+  short qc_shift[kMaxQcBlocks]; // [jb][kb] circulant shifts, -1 = zero block
   // ---- decoder config ----
   int alg, wmode, kmax, lam, p, stall, mlp_thr, force_ordered;
   double alpha;
