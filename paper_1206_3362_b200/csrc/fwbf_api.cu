@@ -21,7 +21,10 @@
 #include "fwbf_internal.h"
 
 namespace fwbf {
-template <typename YT, bool CIRC, int KC, int TB, bool NOISE, int WT> __global__ void decode_kernel(const __grid_constant__ KParams P);
+template <typename YT, bool CIRC, int KC, int TB, int WT> __global__ void decode_kernel(const __grid_constant__ KParams P);
+template <typename YT>
+__global__ void noise_kernel(unsigned long long seed, long long first, long long count, double sigma,
+                             const uint32_t *codeword, YT *y, long long ld, int n, int pm);
 }
 
 using fwbf::KParams;
@@ -67,6 +70,8 @@ struct fwbf_code {
   void *pipe_buf[2] = {nullptr, nullptr};
   size_t pipe_bytes = 0;
   int64_t *pipe_counters = nullptr;
+  void *noise_buf = nullptr;
+  size_t noise_bytes = 0;
 };
 
 static constexpr int kWorkRing = 1024;
@@ -230,6 +235,7 @@ extern "C" int fwbf_code_destroy(fwbf_code *c) {
     if (c->pipe_buf[i]) cudaFree(c->pipe_buf[i]);
   }
   cudaFree(c->pipe_counters);
+  cudaFree(c->noise_buf);
   delete c;
   return FWBF_OK;
 }
@@ -352,24 +358,15 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
   P.smem_bytes = o;
 }
 
-struct NoiseSpec {
-  unsigned long long seed;
-  long long first;
-  double sigma;
-};
-
 template <typename YT>
 static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long long batch,
-                         long long ld, const fwbf_outputs *out, cudaStream_t stream,
-                         const NoiseSpec *noise = nullptr) {
+                         long long ld, const fwbf_outputs *out, cudaStream_t stream) {
   int rc = validate(c, p);
   if (rc) return rc;
   if (batch < 0) return fail(FWBF_EINVAL, "batch must be nonnegative");
   if (batch == 0) return FWBF_OK;
-  if (!noise) {
-    if (!y) return fail(FWBF_EINVAL, "y is null");
-    if (ld < c->n) return fail(FWBF_EINVAL, "expected a length-%d frame (ld=%lld)", c->n, ld);
-  }
+  if (!y) return fail(FWBF_EINVAL, "y is null");
+  if (ld < c->n) return fail(FWBF_EINVAL, "expected a length-%d frame (ld=%lld)", c->n, ld);
   if (batch > 0x7fffffffLL) return fail(FWBF_EINVAL, "batch too large for one call");
   fwbf_outputs o = out ? *out : fwbf_outputs{};
   const long long maxf = fwbf_max_flips_per_iter(c, p);
@@ -415,12 +412,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   P.y = y;
   P.ld = ld;
   P.batch = batch;
-  if (noise) {
-    P.seed = noise->seed;
-    P.first_frame = noise->first;
-    P.sigma = noise->sigma;
-  }
-  const bool nz = noise != nullptr;
+
   P.z_bits = o.z_bits;
   P.z_ld = o.z_ld;
   P.iterations = o.iterations;
@@ -435,8 +427,6 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   P.batch_word_err = o.batch_word_err;
   P.batch_frames = o.batch_frames;
   P.codeword_bits = o.codeword_bits;
-  P.y_out = noise ? o.y_out : nullptr;
-  P.y_out_ld = o.y_out_ld;
   const unsigned slot = c->work_slot.fetch_add(1) % kWorkRing;
   P.work_counter = c->d_work + slot;
 
@@ -448,16 +438,11 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     if (sizeof(YT) == 4) {
       struct Shape { int kc, tb, wt; const void *fn; };
       static const Shape shapes[] = {
-#define FWBF_SHAPE(YT_, C_, KC_, TB_, WT_) {KC_, TB_, WT_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, false, WT_>},
+#define FWBF_SHAPE(YT_, C_, KC_, TB_, WT_) {KC_, TB_, WT_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, WT_>},
           FWBF_FAST_CONFIGS(FWBF_SHAPE)
 #undef FWBF_SHAPE
       };
-      static const Shape shapes_nz[] = {
-#define FWBF_SHAPE(YT_, C_, KC_, TB_, WT_) {KC_, TB_, WT_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, true, WT_>},
-          FWBF_FAST_CONFIGS(FWBF_SHAPE)
-#undef FWBF_SHAPE
-      };
-      const Shape *tab = nz ? shapes_nz : shapes;
+      const Shape *tab = shapes;
       const int ntab = (int)(sizeof(shapes) / sizeof(shapes[0]));
       int want_kc = 0, want_tb = 0; // FWBF_SHAPE="KCxTB" forces a shape (tuning)
       if (const char *e = getenv("FWBF_SHAPE")) sscanf(e, "%dx%d", &want_kc, &want_tb);
@@ -477,19 +462,14 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
         if (tab[i].wt == 0 && tab[i].kc * tab[i].tb >= c->n) { kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc; break; }
     } else {
       T = c->n <= 2048 ? 256 : (c->n <= 8192 ? 512 : 1024);
-      kern = nz ? (const void *)fwbf::decode_kernel<double, true, 1, 0, true, 0>
-                : (const void *)fwbf::decode_kernel<double, true, 1, 0, false, 0>;
+      kern = (const void *)fwbf::decode_kernel<double, true, 1, 0, 0>;
     }
   } else {
     T = c->n <= 2048 ? 256 : (c->n <= 8192 ? 512 : 1024);
-    if (sizeof(YT) == 4)
-      kern = nz ? (const void *)fwbf::decode_kernel<float, false, 1, 0, true, 0>
-                : (const void *)fwbf::decode_kernel<float, false, 1, 0, false, 0>;
-    else
-      kern = nz ? (const void *)fwbf::decode_kernel<double, false, 1, 0, true, 0>
-                : (const void *)fwbf::decode_kernel<double, false, 1, 0, false, 0>;
+    kern = sizeof(YT) == 4 ? (const void *)fwbf::decode_kernel<float, false, 1, 0, 0>
+                           : (const void *)fwbf::decode_kernel<double, false, 1, 0, 0>;
   }
-  const bool compact = circ && sizeof(YT) == 4 && !nz && c->w <= 32 && !getenv("FWBF_NO_COMPACT");
+  const bool compact = circ && sizeof(YT) == 4 && c->w <= 32 && !getenv("FWBF_NO_COMPACT");
   layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact);
   {
     // FWBF block-argmax groups: odd p -> one thread per block (stride-p reads
@@ -511,7 +491,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     P.log2_tpb = 0;
     while ((1 << P.log2_tpb) < tpb) ++P.log2_tpb;
   }
-  if (P.smem_bytes > c->smem_optin && !nz && !compact) {
+  if (P.smem_bytes > c->smem_optin && !compact) {
     // Alias the metric buffer over the y buffer: after init y is only needed
     // for alpha*|y|, which the kernel then re-reads from global memory.
     P.alias_y = 1;
@@ -534,14 +514,6 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   if (P.smem_bytes > c->smem_optin)
     return fail(FWBF_EUNSUPPORTED, "frame state needs %d B of shared memory (device max %d)",
                 P.smem_bytes, c->smem_optin);
-  if (nz) {
-    // raw-draw scratch aliases Ebuf and the check records (unused during init);
-    // about N(1 + 1/16) + 64 draws cover a frame, the rest is computed on demand
-    const int avail = (P.off_amask - P.off_e) / 8;
-    int pm = c->n + c->n / 16 + 64;
-    pm = std::min(pm, avail) & ~3;
-    P.noise_pm = std::max(pm, 0);
-  }
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P.smem_bytes));
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, P.smem_bytes));
@@ -583,16 +555,77 @@ extern "C" int fwbf_decode_f64(fwbf_code *c, const fwbf_params *p, const double 
   return launch_decode<double>(c, p, y, batch, ld, out, (cudaStream_t)stream);
 }
 
+// Reference-channel decode: per chunk, noise_kernel writes the chunk's
+// channel values (numpy's stream, float64 or rounded to float32) to a scratch
+// buffer (or to out->y_out), then the decode kernel consumes them.
+template <typename YT>
+static int decode_awgn_t(fwbf_code *c, const fwbf_params *p, uint64_t seed, int64_t first, int64_t count,
+                         double sigma, const fwbf_outputs *out, cudaStream_t stream) {
+  int rc = validate(c, p);
+  if (rc) return rc;
+  if (count < 0) return fail(FWBF_EINVAL, "count must be nonnegative");
+  if (count == 0) return FWBF_OK;
+  fwbf_outputs o = out ? *out : fwbf_outputs{};
+  const int n = c->n;
+  const long long ld = o.y_out ? o.y_out_ld : ((n + 3) / 4 * 4);
+  if (o.y_out && ld < n) return fail(FWBF_EINVAL, "y_out_ld too small");
+  long long chunk = std::min<long long>(count, 1 << 18);
+  const int bf = o.batch_word_err ? std::max(1, o.batch_frames) : 1;
+  chunk = std::max<long long>(bf, chunk / bf * bf);
+  CUDA_TRY(cudaSetDevice(c->device));
+  YT *scratch = nullptr;
+  if (!o.y_out) {
+    std::lock_guard<std::mutex> lock(c->pipe_mu);
+    const size_t need = (size_t)chunk * ld * sizeof(YT);
+    if (need > c->noise_bytes) {
+      if (c->noise_buf) cudaFree(c->noise_buf);
+      c->noise_buf = nullptr;
+      c->noise_bytes = 0;
+      CUDA_TRY(cudaMalloc(&c->noise_buf, need));
+      c->noise_bytes = need;
+    }
+    scratch = (YT *)c->noise_buf;
+  }
+  // raw draws prefetched per frame: about N (1 + 1/16) + 64 cover a frame
+  const int pm = ((n + n / 16 + 64) + 3) & ~3;
+  const int smem = pm * 8;
+  auto nk = fwbf::noise_kernel<YT>;
+  CUDA_TRY(cudaFuncSetAttribute((const void *)nk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const long long kmax = p->k_max;
+  const long long maxf = fwbf_max_flips_per_iter(c, p);
+  for (long long s = 0; s < count; s += chunk) {
+    const long long nb = std::min(chunk, count - s);
+    YT *yb = o.y_out ? (YT *)o.y_out + s * ld : scratch;
+    const int grid = (int)std::min<long long>(nb, (long long)c->sm_count * 8);
+    nk<<<grid, 128, smem, stream>>>((unsigned long long)seed, first + s, nb, sigma, o.codeword_bits, yb, ld, n, pm);
+    CUDA_TRY(cudaGetLastError());
+    fwbf_outputs oc = o;
+    if (o.z_bits) oc.z_bits = o.z_bits + s * o.z_ld;
+    if (o.iterations) oc.iterations = o.iterations + s;
+    if (o.flags) oc.flags = o.flags + s;
+    if (o.flips_total) oc.flips_total = o.flips_total + s;
+    if (o.bit_errors) oc.bit_errors = o.bit_errors + s;
+    if (o.fliplog) {
+      oc.fliplog = o.fliplog + s * o.fliplog_stride;
+      oc.fliplog_counts = o.fliplog_counts + s * kmax;
+    }
+    if (o.batch_word_err) oc.batch_word_err = o.batch_word_err + s / bf;
+    (void)maxf;
+    rc = launch_decode<YT>(c, p, yb, nb, ld, &oc, stream);
+    if (rc) return rc;
+  }
+  return FWBF_OK;
+}
+
 extern "C" int fwbf_decode_awgn(fwbf_code *c, const fwbf_params *p, uint64_t seed, int64_t first,
                                 int64_t count, double sigma, int32_t mode, const fwbf_outputs *out,
                                 void *stream) {
   if (first < 0) return fail(FWBF_EINVAL, "seed and frame index must be nonnegative");
   if (!(sigma >= 0)) return fail(FWBF_EINVAL, "sigma must be nonnegative");
-  NoiseSpec ns{seed, first, sigma};
   if (mode == FWBF_NOISE_NUMPY_F64)
-    return launch_decode<double>(c, p, nullptr, count, 0, out, (cudaStream_t)stream, &ns);
+    return decode_awgn_t<double>(c, p, seed, first, count, sigma, out, (cudaStream_t)stream);
   if (mode == FWBF_NOISE_NUMPY_F32)
-    return launch_decode<float>(c, p, nullptr, count, 0, out, (cudaStream_t)stream, &ns);
+    return decode_awgn_t<float>(c, p, seed, first, count, sigma, out, (cudaStream_t)stream);
   return fail(FWBF_EINVAL, "unknown noise mode %d", mode);
 }
 

@@ -30,7 +30,6 @@
 
 #include "fwbf_b200.h"
 #include "fwbf_internal.h"
-#include "fwbf_noise.cuh"
 
 #ifndef FWBF_MINB_256
 #define FWBF_MINB_256 4
@@ -147,7 +146,7 @@ __device__ __forceinline__ YT load_y(const KParams &P, long long f, int n) {
 //   CIRC : circulant H (index arithmetic) vs explicit CSR/CSC tables
 //   KC   : columns per thread on the guarded path (register accumulators)
 // ---------------------------------------------------------------------------
-template <typename YT, bool CIRC, int KC, int TB, bool NOISE, int WT>
+template <typename YT, bool CIRC, int KC, int TB, int WT>
 __global__ void __launch_bounds__(TB ? TB : 1024, TB == 256 ? FWBF_MINB_256 : 1024 / (TB ? TB : 1024))
 decode_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -228,16 +227,11 @@ decode_kernel(const __grid_constant__ KParams P) {
     // ---------------- init 1: y -> smem, hard decisions, guard statistics -------
     float lmin = INFINITY, lmax = 0.f;
     bool nonfin = false;
-    if (NOISE) // the reference channel for global frame first_frame + f (channel.py:29-50)
-      gen_frame<YT>(ybuf, N, P.seed, (unsigned long long)(P.first_frame + f), P.sigma,
-                    P.codeword_bits, reinterpret_cast<unsigned long long *>(smem_raw + P.off_e),
-                    P.noise_pm);
     for (int k = 0; k < nKy; ++k) {
       const int n = tid + k * T;
       const bool ok = n < N;
-      YT v = ok ? (NOISE ? ybuf[n] : load_y<YT>(P, f, n)) : YT(0);
-      if (ok && !NOISE) ybuf[n] = v;
-      if (NOISE && ok && P.y_out) reinterpret_cast<YT *>(P.y_out)[f * P.y_out_ld + n] = v;
+      YT v = ok ? load_y<YT>(P, f, n) : YT(0);
+      if (ok) ybuf[n] = v;
       const uint32_t b = __ballot_sync(FULL_MASK, ok && (v < YT(0)));
       if (lane == 0 && (k * T + warp * 32) < N) zbits[(k * T + warp * 32) >> 5] = b;
       if (ok) {
@@ -887,9 +881,8 @@ decode_kernel(const __grid_constant__ KParams P) {
 }
 
 // explicit instantiations used by the launcher
-#define FWBF_INST(YT, C, KC, TB, WT)                                                             \
-  template __global__ void decode_kernel<YT, C, KC, TB, false, WT>(const __grid_constant__ KParams); \
-  template __global__ void decode_kernel<YT, C, KC, TB, true, WT>(const __grid_constant__ KParams);
+#define FWBF_INST(YT, C, KC, TB, WT) \
+  template __global__ void decode_kernel<YT, C, KC, TB, WT>(const __grid_constant__ KParams);
 FWBF_FAST_CONFIGS(FWBF_INST)
 FWBF_INST(double, true, 1, 0, 0)
 FWBF_INST(float, false, 1, 0, 0)

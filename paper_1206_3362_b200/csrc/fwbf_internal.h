@@ -43,11 +43,6 @@ struct KParams {
   const void *y;
   long long ld;
   long long batch;
-  // noise (awgn mode)
-  unsigned long long seed;
-  long long first_frame;
-  double sigma;
-  int noise_pm; // raw draws prefetched into shared scratch per frame
   // ---- outputs ----
   uint32_t *z_bits;
   long long z_ld;
@@ -63,8 +58,6 @@ struct KParams {
   int *batch_word_err;
   int batch_frames;
   const uint32_t *codeword_bits;
-  void *y_out;
-  long long y_out_ld;
   unsigned int *work_counter;
   long long *phase_cycles; // optional [8] per-phase cycle sums (FWBF_PHASES=1)
   // ---- shared memory layout (byte offsets) ----

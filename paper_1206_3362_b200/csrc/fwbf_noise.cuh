@@ -2,7 +2,7 @@
 // Philox4x64-10 stream keyed (seed, frame << 128) and its 256-level ziggurat
 // standard normal (channel.py:29-50), y = s + sigma * g in float64.
 //
-// One CTA generates one frame's N normals:
+// noise_kernel (fwbf_noise.cu): one CTA generates one frame's N normals:
 //   A. all threads fill raw[p] (the p-th uint64 of the frame's stream) for
 //      p < PM into shared scratch: block b = p / 4 uses counter (b + 1, 0,
 //      frame_lo, frame_hi) -- numpy increments before generating;
@@ -18,9 +18,9 @@
 
 namespace fwbf {
 
-__device__ const double d_zig_w[256] = FWBF_ZIG_W_INIT;
-__device__ const unsigned long long d_zig_k[256] = FWBF_ZIG_K_INIT;
-__device__ const double d_zig_f[256] = FWBF_ZIG_F_INIT;
+static __device__ const double d_zig_w[256] = FWBF_ZIG_W_INIT;
+static __device__ const unsigned long long d_zig_k[256] = FWBF_ZIG_K_INIT;
+static __device__ const double d_zig_f[256] = FWBF_ZIG_F_INIT;
 
 struct U4 { unsigned long long v[4]; };
 
@@ -59,7 +59,7 @@ struct NoiseStream {
 
 // Slow path of one normal whose first draw (already split) failed the fast
 // test; `pos` is the position after that draw.  Returns the value, advances pos.
-__device__ __noinline__ double zig_slow(const NoiseStream &s, long long &pos, int idx,
+__device__ __forceinline__ double zig_slow(const NoiseStream &s, long long &pos, int idx,
                                         unsigned long long rabs, double x) {
   const double R = FWBF_ZIG_R;
   const double inv_r = 1.0 / FWBF_ZIG_R;
