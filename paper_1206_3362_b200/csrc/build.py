@@ -47,6 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-static-global-template-stub=false",
            "-I", os.path.join(REPO, "include"), "-I", HERE,
            "-Xptxas", "-v" if verbose else "-O3",
+           *os.environ.get("FWBF_EXTRA_NVCC", "").split(),
            "-o", LIB + ".tmp", *srcs]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
