@@ -328,7 +328,7 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
     // shifted by one element for 8-byte pair loads), |min2|, argmin column,
     // and the per-column (lo, hi) correction limbs
     const int dblf = (2 * n + std::max(0, cover - n) + 2 + 31) / 32 * 32;
-    const int split_bytes = 2 * dblf * 4 + align16(m * 8) + align16(m * 2) + align16(n * 8);
+    const int split_bytes = 2 * dblf * 4 + align16(m * 8) + align16(m * 2) + 2 * align16(n * 8);
     const int r = take(std::max(2 * dbl * 8, split_bytes));
     P.off_chk1 = r;
     P.off_chk2 = r + dbl * 8;
@@ -337,6 +337,7 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
     P.off_m2s = r + 2 * dblf * 4;
     P.off_a2m = P.off_m2s + align16(m * 8);
     P.off_corr = P.off_a2m + align16(m * 2);
+    P.off_ay = P.off_corr + align16(n * 8);
     P.off_amin = P.off_chk2 + align16(m * 8); // ordered path only; inside chk2's upper half
   } else {
     P.off_chk1 = take(m * 8);
@@ -499,7 +500,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     P.off_e = P.off_y;
     for (int *x : {&P.off_chk1, &P.off_chk2, &P.off_amin, &P.off_amask, &P.off_sbits, &P.off_zbits,
                    &P.off_blkv, &P.off_blki, &P.off_flips, &P.off_offs, &P.off_red, &P.off_misc,
-                   &P.off_fa, &P.off_fb, &P.off_m2s, &P.off_a2m, &P.off_corr})
+                   &P.off_fa, &P.off_fb, &P.off_m2s, &P.off_a2m, &P.off_corr, &P.off_ay})
       *x += delta;
     P.smem_bytes += delta;
   }

@@ -301,6 +301,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     int *sM2 = reinterpret_cast<int *>(smem_raw + P.off_m2s);      // split: correction limb deltas per check
     uint16_t *sA2 = reinterpret_cast<uint16_t *>(smem_raw + P.off_a2m); // split: argmin column per check
     int *sCorr = reinterpret_cast<int *>(smem_raw + P.off_corr);   // split: per column (lo, hi) limbs
+    double *sAY = reinterpret_cast<double *>(smem_raw + P.off_ay); // split: fl(alpha |y_n|)
 
     // ---------------- init 2: per-check minima, syndrome, signed weights --------
     uint32_t sprev = 0; // syndrome bits of this thread's checks tid + k*T
@@ -405,6 +406,9 @@ decode_kernel(const __grid_constant__ KParams P) {
         am[q][1] = (n < N && aw > 1) ? amask[n * aw + 1] : 0u;
       }
     }
+    if (split) { // fl(alpha |y_n|) once per frame (ybuf is still valid here)
+      for (int n = tid; n < N; n += T) sAY[n] = __dmul_rn(P.alpha, fabs((double)ybuf[n]));
+    }
     if (P.alias_y) __syncthreads(); // amask / ybuf may overlay Ebuf (compact layout)
 
     // ---------------- iterations -----------------------------------------------
@@ -451,8 +455,7 @@ decode_kernel(const __grid_constant__ KParams P) {
               const int2 cv = reinterpret_cast<const int2 *>(sCorr)[n];
               if (cv.x | cv.y)
                 acc = __dadd_rn(acc, __dmul_rn((double)(((long long)cv.y << 24) + cv.x), qexp));
-              const double ay = P.alias_y ? fabs((double)load_y<YT>(P, f, n)) : fabs((double)ybuf[n]);
-              Ebuf[n] = __dsub_rn(acc, __dmul_rn(P.alpha, ay));
+              Ebuf[n] = __dsub_rn(acc, sAY[n]);
             }
           }
         }

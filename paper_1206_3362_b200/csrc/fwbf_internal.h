@@ -66,7 +66,7 @@ struct KParams {
   int smem_bytes;
   int alias_y; // metric buffer overlays y; alpha*|y| re-read from global
   int d21f;    // (unused)
-  int off_fa, off_fb, off_m2s, off_a2m, off_corr; // split-fp32 path arrays (inside the chk region)
+  int off_fa, off_fb, off_m2s, off_a2m, off_corr, off_ay; // split-fp32 path arrays (inside the chk region)
   int uoff[kMaxCircWeight]; // split-fp32 gather: byte offset of check (n - c_j) for even n, minus 4n
   int no_split; // disable the split-fp32 path (testing)
 };
