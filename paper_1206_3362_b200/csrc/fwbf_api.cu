@@ -328,7 +328,7 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
     // shifted by one element for 8-byte pair loads), |min2|, argmin column,
     // and the per-column (lo, hi) correction limbs
     const int dblf = (2 * n + std::max(0, cover - n) + 2 + 31) / 32 * 32;
-    const int split_bytes = 2 * dblf * 4 + align16(m * 8) + align16(m * 2) + 2 * align16(n * 8);
+    const int split_bytes = 2 * dblf * 4 + align16(m * 8) + align16(m * 2) + (compact ? 2 : 1) * align16(n * 8);
     const int r = take(std::max(2 * dbl * 8, split_bytes));
     P.off_chk1 = r;
     P.off_chk2 = r + dbl * 8;
@@ -338,6 +338,7 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
     P.off_a2m = P.off_m2s + align16(m * 8);
     P.off_corr = P.off_a2m + align16(m * 2);
     P.off_ay = P.off_corr + align16(n * 8);
+    P.has_ay = compact ? 1 : 0;
     P.off_amin = P.off_chk2 + align16(m * 8); // ordered path only; inside chk2's upper half
   } else {
     P.off_chk1 = take(m * 8);

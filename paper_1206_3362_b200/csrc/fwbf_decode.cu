@@ -406,7 +406,7 @@ decode_kernel(const __grid_constant__ KParams P) {
         am[q][1] = (n < N && aw > 1) ? amask[n * aw + 1] : 0u;
       }
     }
-    if (split) { // fl(alpha |y_n|) once per frame (ybuf is still valid here)
+    if (split && P.has_ay) { // fl(alpha |y_n|) once per frame (ybuf is still valid here)
       for (int n = tid; n < N; n += T) sAY[n] = __dmul_rn(P.alpha, fabs((double)ybuf[n]));
     }
     if (P.alias_y) __syncthreads(); // amask / ybuf may overlay Ebuf (compact layout)
@@ -455,7 +455,10 @@ decode_kernel(const __grid_constant__ KParams P) {
               const int2 cv = reinterpret_cast<const int2 *>(sCorr)[n];
               if (cv.x | cv.y)
                 acc = __dadd_rn(acc, __dmul_rn((double)(((long long)cv.y << 24) + cv.x), qexp));
-              Ebuf[n] = __dsub_rn(acc, sAY[n]);
+              const double aa = P.has_ay ? sAY[n]
+                                         : __dmul_rn(P.alpha, P.alias_y ? fabs((double)load_y<YT>(P, f, n))
+                                                                        : fabs((double)ybuf[n]));
+              Ebuf[n] = __dsub_rn(acc, aa);
             }
           }
         }

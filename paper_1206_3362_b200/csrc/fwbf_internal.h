@@ -67,6 +67,7 @@ struct KParams {
   int alias_y; // metric buffer overlays y; alpha*|y| re-read from global
   int d21f;    // (unused)
   int off_fa, off_fb, off_m2s, off_a2m, off_corr, off_ay; // split-fp32 path arrays (inside the chk region)
+  int has_ay; // split path keeps fl(alpha|y|) per column in shared memory (compact layout)
   int uoff[kMaxCircWeight]; // split-fp32 gather: byte offset of check (n - c_j) for even n, minus 4n
   int no_split; // disable the split-fp32 path (testing)
 };
