@@ -12,7 +12,7 @@ constexpr int kMaxQcBlocks = 256;  // quasi-cyclic shift table entries in the pa
 #define FWBF_FAST_CONFIGS(X)    \
   X(float, true, 2, 128, 16)    \
   X(float, true, 4, 256, 32)    \
-  X(float, true, 8, 512, 64)    \
+  X(float, true, 4, 1024, 64)   \
   X(float, true, 2, 128, 0)     \
   X(float, true, 4, 256, 0)     \
   X(float, true, 4, 512, 0)     \
