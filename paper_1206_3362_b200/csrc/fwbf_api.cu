@@ -482,6 +482,10 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     P.sel_spread = 0;
     if (pp > 1 && (pp & (pp - 1)) == 0) {
       tpb = std::min(pp, 32);
+    } else if (pp > 1 && !(pp & 1)) {
+      // p = 2^k * odd: groups of 2^k (<= 16) threads on consecutive blocks start
+      // at distinct multiples of 2^k modulo 16 banks-of-doubles: conflict free
+      tpb = std::min(16, pp & -pp);
     } else if (pp & 1) {
       // largest power of two <= min(16, p) with all blocks in one round and
       // the half-warps of the CTA divisible into groups of tpb
