@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfwbf_b200.so")
+# FWBF_LIB: development override (A/B builds of the same sources)
+LIB_PATH = os.environ.get("FWBF_LIB") or os.path.join(_HERE, "libfwbf_b200.so")
 
 FWBF_OK, FWBF_EINVAL, FWBF_ECUDA, FWBF_EUNSUPPORTED = 0, -1, -2, -3
 ALG = {"fwbf": 0, "imwbf": 1, "mlp": 2}

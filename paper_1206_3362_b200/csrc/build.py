@@ -38,8 +38,8 @@ def _stale() -> bool:
     return any(os.path.exists(d) and os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB) -> str:
+    if out == LIB and not force and not _stale():
         return LIB
     srcs = [os.path.join(HERE, s) for s in SOURCES if os.path.exists(os.path.join(HERE, s))]
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
@@ -48,16 +48,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-I", os.path.join(REPO, "include"), "-I", HERE,
            "-Xptxas", "-v" if verbose else "-O3",
            *os.environ.get("FWBF_EXTRA_NVCC", "").split(),
-           "-o", LIB + ".tmp", *srcs]
+           "-o", out + ".tmp", *srcs]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libfwbf_b200.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    outs = [a[len("--out="):] for a in sys.argv if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=os.path.abspath(outs[0]) if outs else LIB))

@@ -443,6 +443,37 @@ decode_kernel(const __grid_constant__ KParams P) {
 #pragma unroll
         for (int j = 0; j < (WT > 0 ? WT : 1); ++j) // P.uoff[j]: host-computed uniform part
           GatherP2<0, NP, TB>::run(hi, lo, baseT + (uint32_t)P.uoff[j], cc);
+        if (WT <= 32) {
+#pragma unroll
+        for (int qp = 0; qp < NP; ++qp) {
+          // columns (n, n+1), n even: 16-byte accesses to the per-column arrays
+          const float2 h = f2unpack(hi[qp]);
+          const float2 l = f2unpack(lo[qp]);
+          const int n = 2 * tid + 2 * T * qp;
+          if (n < N) {
+            const int4 cv = *reinterpret_cast<const int4 *>(sCorr + 2 * n);
+            double a0 = __dadd_rn((double)h.x, (double)l.x), a1 = __dadd_rn((double)h.y, (double)l.y);
+            if (cv.x | cv.y) a0 = __dadd_rn(a0, __dmul_rn((double)(((long long)cv.y << 24) + cv.x), qexp));
+            if (cv.z | cv.w) a1 = __dadd_rn(a1, __dmul_rn((double)(((long long)cv.w << 24) + cv.z), qexp));
+            double aa0, aa1;
+            if (P.has_ay) {
+              const double2 ay2 = *reinterpret_cast<const double2 *>(sAY + n);
+              aa0 = ay2.x;
+              aa1 = ay2.y;
+            } else {
+              aa0 = __dmul_rn(P.alpha, P.alias_y ? fabs((double)load_y<YT>(P, f, n)) : fabs((double)ybuf[n]));
+              aa1 = (n + 1 < N) ? __dmul_rn(P.alpha, P.alias_y ? fabs((double)load_y<YT>(P, f, n + 1))
+                                                                 : fabs((double)ybuf[n + 1]))
+                                : 0.0;
+            }
+            if (n + 1 < N) {
+              *reinterpret_cast<double2 *>(Ebuf + n) = make_double2(__dsub_rn(a0, aa0), __dsub_rn(a1, aa1));
+            } else {
+              Ebuf[n] = __dsub_rn(a0, aa0);
+            }
+          }
+        }
+        } else {
 #pragma unroll
         for (int qp = 0; qp < NP; ++qp) {
           const float2 h = f2unpack(hi[qp]);
@@ -461,6 +492,7 @@ decode_kernel(const __grid_constant__ KParams P) {
               Ebuf[n] = __dsub_rn(acc, aa);
             }
           }
+        }
         }
       } else if (CIRC && fastp) {
         // chk1/chk2 hold sgn*min1 / sgn*min2 twice ([0,N) and [N,2N)) plus a
@@ -576,13 +608,14 @@ decode_kernel(const __grid_constant__ KParams P) {
             const int i2 = __shfl_xor_sync(FULL_MASK, i, off);
             amax_combine(v, i, v2, i2);
           }
+          {
+            const uint32_t pm = __ballot_sync(FULL_MASK, ok && sub == 0 && v > 0.0);
+            if (lane == 0 && pm) atomicAdd(&misc[S_F], __popc(pm)); // one count per warp
+          }
           if (ok) {
             if (sub == 0) { blk_v[b] = v; blk_i[b] = i; }
             if (v > 0.0) {
-              if (sub == 0) {
-                atomicXor(&zbits[i >> 5], 1u << (i & 31));
-                atomicAdd(&misc[S_F], 1);
-              }
+              if (sub == 0) atomicXor(&zbits[i >> 5], 1u << (i & 31));
               if (CIRC) {
                 for (int j = sub; j < W; j += TPB) {
                   int m = i - offs_s[j];
