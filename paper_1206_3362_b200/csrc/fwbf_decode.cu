@@ -179,6 +179,7 @@ decode_kernel(const __grid_constant__ KParams P) {
 
   const int W = WT ? WT : P.w;       // circulant weight (0 explicit); compile-time when WT > 0
   const int aw = (W > 32) ? 2 : 1;   // amask words per column
+  const int qlz = P.qc_z ? __ffs(P.qc_z) - 1 : 0; // log2 Z (QC: Z a power of two)
 
   if (CIRC) {
     for (int j = tid; j < W; j += T) { offs_s[j] = P.off[j]; offs_s[64 + j] = P.dneg[j]; }
@@ -324,7 +325,7 @@ decode_kernel(const __grid_constant__ KParams P) {
           }
         } else if (P.qc_z) {
           // quasi-cyclic: row r*Z + i holds column cb*Z + ((i + s[r][cb]) mod Z)
-          const int Z = P.qc_z, r = m / Z, ii = m - r * Z;
+          const int Z = P.qc_z, r = m >> qlz, ii = m & (Z - 1);
           for (int cb = 0; cb < P.qc_kb; ++cb) {
             const int sh = P.qc_shift[r * P.qc_kb + cb];
             if (sh < 0) continue;
@@ -547,26 +548,26 @@ decode_kernel(const __grid_constant__ KParams P) {
             for (int i = 0; i < W; ++i) {
               int m = n + offs_s[64 + ii];
               if (m >= N) m -= N;
-              const double w = (amin[m] == n) ? chk2[m] : chk1[m];
+              const double w = ((amin[m] == n) ? chk2 : chk1)[m]; // one 8-byte load
               acc = __dadd_rn(acc, w);
               if (++ii == W) ii = 0;
             }
           } else if (P.qc_z) {
             // column cb*Z + o meets row block r at check r*Z + ((o - s) mod Z):
             // ascending in r, i.e. the reference's ascending check order
-            const int Z = P.qc_z, cb = n / Z, o = n - cb * Z;
+            const int Z = P.qc_z, cb = n >> qlz, o = n & (Z - 1);
             for (int r = 0; r < P.qc_jb; ++r) {
               const int sh = P.qc_shift[r * P.qc_kb + cb];
               if (sh < 0) continue;
               const int m = r * Z + ((o - sh) & (Z - 1));
-              const double w = (amin[m] == n) ? chk2[m] : chk1[m];
+              const double w = ((amin[m] == n) ? chk2 : chk1)[m]; // one 8-byte load
               acc = __dadd_rn(acc, w);
             }
           } else {
             const int e0 = __ldg(P.col_ptr + n), e1 = __ldg(P.col_ptr + n + 1);
             for (int e = e0; e < e1; ++e) {
               const int m = __ldg(P.col_idx + e);
-              const double w = (amin[m] == n) ? chk2[m] : chk1[m];
+              const double w = ((amin[m] == n) ? chk2 : chk1)[m]; // one 8-byte load
               acc = __dadd_rn(acc, w);
             }
           }
@@ -623,7 +624,7 @@ decode_kernel(const __grid_constant__ KParams P) {
                   atomicXor(&sbits[m >> 5], 1u << (m & 31));
                 }
               } else if (P.qc_z) {
-                const int Z = P.qc_z, cb = i / Z, o = i - cb * Z;
+                const int Z = P.qc_z, cb = i >> qlz, o = i & (Z - 1);
                 for (int r = sub; r < P.qc_jb; r += TPB) {
                   const int sh = P.qc_shift[r * P.qc_kb + cb];
                   if (sh < 0) continue;
@@ -774,7 +775,7 @@ decode_kernel(const __grid_constant__ KParams P) {
         } else if (P.qc_z) {
           for (int fi = warp; fi < F; fi += nwarps) {
             const int n = flips[fi];
-            const int Z = P.qc_z, cb = n / Z, o = n - cb * Z;
+            const int Z = P.qc_z, cb = n >> qlz, o = n & (Z - 1);
             for (int r = lane; r < P.qc_jb; r += 32) {
               const int sh = P.qc_shift[r * P.qc_kb + cb];
               if (sh < 0) continue;
