@@ -539,9 +539,14 @@ decode_kernel(const __grid_constant__ KParams P) {
           }
         }
       } else {
+        // y of the next column is fetched one column ahead (from global memory
+        // when the metric buffer overlays y) so its latency hides behind a gather
+        YT ynext = (tid < N) ? (P.alias_y ? load_y<YT>(P, f, tid) : ybuf[tid]) : YT(0);
         for (int kk = 0; kk < nKy; ++kk) {
           const int n = tid + kk * T;
           if (n >= N) break;
+          const YT ycur = ynext;
+          if (n + T < N) ynext = P.alias_y ? load_y<YT>(P, f, n + T) : ybuf[n + T];
           double acc = 0.0;
           if (CIRC) {
             int ii = P.i0tab[n];
@@ -571,8 +576,7 @@ decode_kernel(const __grid_constant__ KParams P) {
               acc = __dadd_rn(acc, w);
             }
           }
-          const double ay = P.alias_y ? fabs((double)load_y<YT>(P, f, n)) : fabs((double)ybuf[n]);
-          Ebuf[n] = __dsub_rn(acc, __dmul_rn(P.alpha, ay));
+          Ebuf[n] = __dsub_rn(acc, __dmul_rn(P.alpha, fabs((double)ycur)));
         }
       }
       __syncthreads();
