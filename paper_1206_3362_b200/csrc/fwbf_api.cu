@@ -55,6 +55,7 @@ struct fwbf_code {
   int dv_max = 0, dc_max = 0, min_row_w = 0;
   int off[fwbf::kMaxCircWeight] = {0};
   int dneg[fwbf::kMaxCircWeight] = {0};
+  unsigned char jii[fwbf::kMaxCircWeight] = {0};
   int *d_row_ptr = nullptr, *d_row_idx = nullptr, *d_col_ptr = nullptr, *d_col_idx = nullptr;
   uint8_t *d_i0tab = nullptr;
   int16_t *d_offpos = nullptr;
@@ -166,6 +167,8 @@ extern "C" int fwbf_code_create(const fwbf_code_desc *desc, int device, fwbf_cod
     for (int j = 0; j < w; ++j) dn[j] = (n - desc->offsets[j]) % n;
     std::sort(dn.begin(), dn.end());
     for (int j = 0; j < w; ++j) c->dneg[j] = dn[j];
+    for (int j = 0; j < w; ++j) // position of (n - c_j) mod n in the sorted list
+      c->jii[j] = (unsigned char)(std::lower_bound(dn.begin(), dn.end(), (n - desc->offsets[j]) % n) - dn.begin());
     // Column n's checks are (n + dneg[i]) mod n; ascending order starts at the
     // first i with n + dneg[i] >= n (the wrapped, smaller ones).
     i0tab.resize(n);
@@ -306,9 +309,8 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
   int o = 0;
   auto take = [&](int bytes) { int r = o; o = align16(o + bytes); return r; };
   if (compact) {
-    // y (float32) and the argmin masks live only during frame init, so both
-    // overlay the metric buffer; alpha*|y| is then re-read from global y
-    // (L1-resident).  Saves 8 KB per CTA at N = 1023: 5 CTAs/SM instead of 4.
+    // y (float32) lives only during frame init, so it overlays the metric
+    // buffer; alpha*|y| comes from a per-frame table (split path) or global y.
     P.off_y = take(n * 8);
     P.off_e = P.off_y;
     P.alias_y = 1;
@@ -329,7 +331,10 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
     // and the per-column (lo, hi) correction limbs
     const int dblf = (2 * n + std::max(0, cover - n) + 2 + 31) / 32 * 32;
     const int split_bytes = 2 * dblf * 4 + align16(m * 8) + align16(m * 2) + (compact ? 2 : 1) * align16(n * 8);
-    const int r = take(std::max(2 * dbl * 8, split_bytes));
+    // the argmin masks (fp64 paths only) follow the two doubled arrays, inside
+    // the split-path footprint when it is larger
+    const int r = take(std::max(2 * dbl * 8 + n * aw * 4, split_bytes));
+    P.off_amask = r + 2 * dbl * 8;
     P.off_chk1 = r;
     P.off_chk2 = r + dbl * 8;
     P.off_fa = r;
@@ -339,22 +344,21 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
     P.off_corr = P.off_a2m + align16(m * 2);
     P.off_ay = P.off_corr + align16(n * 8);
     P.has_ay = compact ? 1 : 0;
-    P.off_amin = P.off_chk2 + align16(m * 8); // ordered path only; inside chk2's upper half
+    P.off_amin = 0; // unused: the ordered circulant path reads argmin bits from amask
   } else {
     P.off_chk1 = take(m * 8);
     P.off_chk2 = take(m * 8);
     P.off_amin = take(m * 4);
   }
-  if (compact)
-    P.off_amask = P.off_y + align16(n * 4);
-  else
-    P.off_amask = take(circ ? n * aw * 4 : 4);
+  // argmin masks, circulant only (placed above): guarded path bit j = offset
+  // index; ordered path bit i = position in the column's ascending check list
+  if (!circ) P.off_amask = take(4);
   P.off_sbits = take(sw * 4);
   P.off_zbits = take(zw * 4);
   P.off_blkv = take(nslots * 8);
   P.off_blki = take((nslots + zw) * 4);
   P.off_flips = take(maxf * 4);
-  P.off_offs = take(2 * fwbf::kMaxCircWeight * 4);
+  P.off_offs = take(3 * fwbf::kMaxCircWeight * 4); // off[64], dneg doubled [128]
   P.off_red = take(32 * 8 + 32 * 4);
   P.off_misc = take(16 * 4 + 64 * 4);
   P.smem_bytes = o;
@@ -390,6 +394,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   P.n_edges = c->n_edges;
   memcpy(P.off, c->off, sizeof P.off);
   memcpy(P.dneg, c->dneg, sizeof P.dneg);
+  memcpy(P.jii, c->jii, sizeof P.jii);
   P.i0tab = c->d_i0tab;
   P.offpos = c->d_offpos;
   P.row_ptr = c->d_row_ptr;

@@ -182,7 +182,7 @@ decode_kernel(const __grid_constant__ KParams P) {
   const int qlz = P.qc_z ? __ffs(P.qc_z) - 1 : 0; // log2 Z (QC: Z a power of two)
 
   if (CIRC) {
-    for (int j = tid; j < W; j += T) { offs_s[j] = P.off[j]; offs_s[64 + j] = P.dneg[j]; }
+    for (int j = tid; j < W; j += T) { offs_s[j] = P.off[j]; offs_s[64 + j] = P.dneg[j]; offs_s[64 + W + j] = P.dneg[j]; }
   }
   if (tid == 0) misc[S_NONFIN] = 0;
 
@@ -385,6 +385,20 @@ decode_kernel(const __grid_constant__ KParams P) {
             const int j = P.offpos[d];
             atomicOr(&amask[ac * aw + (j >> 5)], 1u << (j & 31));
           }
+        } else if (CIRC) {
+          // ordered path: doubled records as above; the argmin bit sits at the
+          // check's position in column ac's ascending check list
+          chk1[m] = sg * d1;
+          chk1[m + N] = sg * d1;
+          chk2[m] = sg * d2;
+          chk2[m + N] = sg * d2;
+          if (P.wmode == FWBF_WEIGHTS_IMWBF) {
+            int d = ac - m;
+            if (d < 0) d += N;
+            int i = (int)P.jii[P.offpos[d]] - (int)P.i0tab[ac];
+            if (i < 0) i += W;
+            atomicOr(&amask[ac * aw + (i >> 5)], 1u << (i & 31));
+          }
         } else {
           chk1[m] = sg * d1;
           chk2[m] = sg * d2;
@@ -549,13 +563,23 @@ decode_kernel(const __grid_constant__ KParams P) {
           if (n + T < N) ynext = P.alias_y ? load_y<YT>(P, f, n + T) : ybuf[n + T];
           double acc = 0.0;
           if (CIRC) {
-            int ii = P.i0tab[n];
-            for (int i = 0; i < W; ++i) {
-              int m = n + offs_s[64 + ii];
-              if (m >= N) m -= N;
-              const double w = ((amin[m] == n) ? chk2 : chk1)[m]; // one 8-byte load
-              acc = __dadd_rn(acc, w);
-              if (++ii == W) ii = 0;
+            // checks (n + dneg[ii]) mod N for ii = i0, i0+1, ... (ascending),
+            // read from the doubled records at n + dneg[ii] (no wrap); bit i of
+            // the column's mask selects min2 at the i-th check
+            const int *dn = offs_s + 64 + P.i0tab[n];
+            const double *c1 = chk1 + n, *c2 = chk2 + n;
+            const uint32_t mk = amask[n * aw];
+            const int w0 = W < 32 ? W : 32;
+            for (int i = 0; i < w0; ++i) {
+              const int d = dn[i];
+              acc = __dadd_rn(acc, (((mk >> i) & 1u) ? c2 : c1)[d]);
+            }
+            if (W > 32) {
+              const uint32_t mkh = amask[n * aw + 1];
+              for (int i = 32; i < W; ++i) {
+                const int d = dn[i];
+                acc = __dadd_rn(acc, (((mkh >> (i - 32)) & 1u) ? c2 : c1)[d]);
+              }
             }
           } else if (P.qc_z) {
             // column cb*Z + o meets row block r at check r*Z + ((o - s) mod Z):
@@ -835,7 +859,7 @@ decode_kernel(const __grid_constant__ KParams P) {
                 const double v2 = -chk2[m];
                 chk1[m] = v1;
                 chk2[m] = v2;
-                if (CIRC && fastp) { chk1[m + N] = v1; chk2[m + N] = v2; }
+                if (CIRC) { chk1[m + N] = v1; chk2[m + N] = v2; }
               }
             }
             sprev ^= (tog ? 1u : 0u) << kk;
@@ -855,7 +879,7 @@ decode_kernel(const __grid_constant__ KParams P) {
             const double v2 = -chk2[m];
             chk1[m] = v1;
             chk2[m] = v2;
-            if (CIRC && fastp) { chk1[m + N] = v1; chk2[m + N] = v2; }
+            if (CIRC) { chk1[m + N] = v1; chk2[m + N] = v2; }
             sprev ^= 1u << kk;
           }
           const uint32_t b = __ballot_sync(FULL_MASK, s);

@@ -27,6 +27,7 @@ struct KParams {
   long long n_edges;
   int off[kMaxCircWeight];  // circulant first-row columns c_j, ascending
   int dneg[kMaxCircWeight]; // sorted (n - c_j) mod n, ascending (ordered column walk)
+  unsigned char jii[kMaxCircWeight]; // offset index j -> its position in dneg
   const uint8_t *i0tab;     // circulant: first dneg index of column n's ascending walk
   const int16_t *offpos;    // circulant: offpos[d] = j if c_j == d else -1
   const int *row_ptr, *row_idx; // CSR, sorted columns
