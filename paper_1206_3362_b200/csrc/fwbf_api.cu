@@ -468,8 +468,22 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
       for (int i = 0; i < ntab && !kern; ++i)
         if (tab[i].wt == 0 && tab[i].kc * tab[i].tb >= c->n) { kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc; break; }
     } else {
-      T = c->n <= 2048 ? 256 : (c->n <= 8192 ? 512 : 1024);
-      kern = (const void *)fwbf::decode_kernel<double, true, 1, 0, 0>;
+      struct Shape { int kc, tb, wt; const void *fn; };
+      static const Shape shapes[] = {
+#define FWBF_SHAPE(YT_, C_, KC_, TB_, WT_) {KC_, TB_, WT_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, WT_>},
+          FWBF_F64_CONFIGS(FWBF_SHAPE)
+#undef FWBF_SHAPE
+      };
+      if (!getenv("FWBF_GENERIC_W"))
+        for (const Shape &sh : shapes)
+          if (sh.wt == c->w && sh.kc * sh.tb >= c->n && sh.kc * sh.tb < 4 * c->n + 256) {
+            kern = sh.fn; T = sh.tb; kc = sh.kc;
+            break;
+          }
+      if (!kern) {
+        T = c->n <= 2048 ? 256 : (c->n <= 8192 ? 512 : 1024);
+        kern = (const void *)fwbf::decode_kernel<double, true, 1, 0, 0>;
+      }
     }
   } else {
     T = c->n <= 2048 ? 256 : (c->n <= 8192 ? 512 : 1024);

@@ -178,6 +178,7 @@ decode_kernel(const __grid_constant__ KParams P) {
   enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR, S_EQ };
 
   const int W = WT ? WT : P.w;       // circulant weight (0 explicit); compile-time when WT > 0
+  constexpr bool kGuard = CIRC && sizeof(YT) == 4; // guarded paths exist for float32 y only
   const int aw = (W > 32) ? 2 : 1;   // amask words per column
   const int qlz = P.qc_z ? __ffs(P.qc_z) - 1 : 0; // log2 Z (QC: Z a power of two)
 
@@ -357,7 +358,7 @@ decode_kernel(const __grid_constant__ KParams P) {
       if (ok) {
         const double sg = par ? 1.0 : -1.0;
         const double d1 = (double)min1, d2 = (double)min2;
-        if (CIRC && split) {
+        if (kGuard && split) {
           const float s1v = par ? (float)min1 : -(float)min1;
           sFA[m] = s1v;
           sFA[m + N] = s1v;
@@ -373,7 +374,7 @@ decode_kernel(const __grid_constant__ KParams P) {
             dl.y = (int)(D >> 24) - (int)((-D) >> 24);
             reinterpret_cast<int2 *>(sM2)[m] = dl;
           }
-        } else if (CIRC && fastp) {
+        } else if (kGuard && fastp) {
           chk1[m] = sg * d1;
           chk1[m + N] = sg * d1;
           chk2[m] = sg * d2;
@@ -413,7 +414,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     // Bit j of am[q] says column tid + q*T is the argmin of its j-th check
     // (m = n - c_j), i.e. reads min2 there instead of min1 (decoders.py:80-84).
     uint32_t am[KC][2];
-    if (CIRC && fastp) {
+    if (kGuard && fastp) {
 #pragma unroll
       for (int q = 0; q < KC; ++q) {
         const int n = tid + q * T;
@@ -421,7 +422,7 @@ decode_kernel(const __grid_constant__ KParams P) {
         am[q][1] = (n < N && aw > 1) ? amask[n * aw + 1] : 0u;
       }
     }
-    if (split && P.has_ay) { // fl(alpha |y_n|) once per frame (ybuf is still valid here)
+    if (kGuard && split && P.has_ay) { // fl(alpha |y_n|) once per frame (ybuf is still valid here)
       for (int n = tid; n < N; n += T) sAY[n] = __dmul_rn(P.alpha, fabs((double)ybuf[n]));
     }
     if (P.alias_y) __syncthreads(); // amask / ybuf may overlay Ebuf (compact layout)
@@ -438,7 +439,7 @@ decode_kernel(const __grid_constant__ KParams P) {
 
       // ---- Eq.(1) metric for every bit -> Ebuf ----
       if (tid == 0) misc[S_F] = 0; // last read before the previous refresh barrier
-      if (WT > 0 && CIRC && split && (KC % 2) == 0) {
+      if (kGuard && WT > 0 && split && (KC % 2) == 0) {
         // Split-fp32 gather, 4 B per edge and no per-edge argmin select:
         // thread tid owns column pairs (2 tid + 2 T qp, +1).  Column n reads
         // check (n - c_j) mod N; for even n the pair's two values are adjacent,
@@ -509,7 +510,7 @@ decode_kernel(const __grid_constant__ KParams P) {
           }
         }
         }
-      } else if (CIRC && fastp) {
+      } else if (kGuard && fastp) {
         // chk1/chk2 hold sgn*min1 / sgn*min2 twice ([0,N) and [N,2N)) plus a
         // KC*T-N pad, so column n reads check (n - c_j) mod N at index
         // n + N - c_j with no wrap test: per j one uniform offset, then per
@@ -842,7 +843,7 @@ decode_kernel(const __grid_constant__ KParams P) {
             const bool s = (word >> lane) & 1u;
             const bool tog = ok && (s != (bool)((sprev >> kk) & 1u));
             if (tog) {
-              if (CIRC && split) {
+              if (kGuard && split) {
                 const float v1 = -sFA[m];
                 sFA[m] = v1;
                 sFA[m + N] = v1;
@@ -952,6 +953,7 @@ decode_kernel(const __grid_constant__ KParams P) {
 #define FWBF_INST(YT, C, KC, TB, WT) \
   template __global__ void decode_kernel<YT, C, KC, TB, WT>(const __grid_constant__ KParams);
 FWBF_FAST_CONFIGS(FWBF_INST)
+FWBF_F64_CONFIGS(FWBF_INST)
 FWBF_INST(double, true, 1, 0, 0)
 FWBF_INST(float, false, 1, 0, 0)
 FWBF_INST(double, false, 1, 0, 0)
