@@ -298,7 +298,7 @@ struct Plan {
 };
 
 static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool circ, int cover, KParams &P,
-                   bool compact = false) {
+                   bool compact = false, bool fused = false) {
   const int n = c->n, m = c->m;
   const int zw = (n + 31) / 32, sw = (m + 31) / 32;
   int nb = 1;
@@ -316,7 +316,7 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
     P.alias_y = 1;
   } else {
     P.off_y = take(n * ysize);
-    P.off_e = take(n * 8);
+    P.off_e = fused ? P.off_y : take(n * 8); // fused: no metric buffer
   }
   // guarded path: doubled signed min1 plus zero pad up to the threads' column cover
   // check records: guarded path (circulant) = two doubled arrays sgn*min1,
@@ -490,8 +490,16 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     kern = sizeof(YT) == 4 ? (const void *)fwbf::decode_kernel<float, false, 1, 0, 0>
                            : (const void *)fwbf::decode_kernel<double, false, 1, 0, 0>;
   }
+  // explicit/QC FWBF with 32 | p: metric and block argmax in one warp pass (no
+  // metric buffer); 512 threads so two CTAs share an SM on large codes
+  P.fused = !circ && p->algorithm == FWBF_ALG_FWBF && p->block_len_p % 32 == 0 && !getenv("FWBF_NO_FUSED");
+  if (P.fused && T > 512) T = 512;
   const bool compact = circ && sizeof(YT) == 4 && c->w <= 32 && !getenv("FWBF_NO_COMPACT");
-  layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact);
+  layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, P.fused);
+  if (P.fused && P.smem_bytes > c->smem_optin) { // y must stay resident for the fused pass
+    P.fused = 0;
+    layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, false);
+  }
   {
     // FWBF block-argmax groups: odd p -> one thread per block (stride-p reads
     // across lanes are bank-conflict free); power-of-two p -> min(p, 32)

@@ -175,7 +175,11 @@ decode_kernel(const __grid_constant__ KParams P) {
   int *misc = reinterpret_cast<int *>(smem_raw + P.off_misc);
   float *redf = reinterpret_cast<float *>(smem_raw + P.off_misc + 16 * 4);
   // misc slots
-  enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR, S_EQ };
+  enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR, S_EQ, S_FB };
+  // fused metric + block argmax (explicit/QC codes, FWBF, p % 32 == 0): no
+  // metric buffer; the flip counter alternates between S_F and S_FB by
+  // iteration parity because flips are counted during the metric pass
+  const bool fused = !CIRC && P.fused;
 
   const int W = WT ? WT : P.w;       // circulant weight (0 explicit); compile-time when WT > 0
   constexpr bool kGuard = CIRC && sizeof(YT) == 4; // guarded paths exist for float32 y only
@@ -259,7 +263,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     }
     nonfin = __any_sync(FULL_MASK, nonfin);
     if (lane == 0) { redf[warp] = lmin; redf[32 + warp] = lmax; if (nonfin) misc[S_NONFIN] = 1; }
-    if (tid == 0) { misc[S_SWT] = 0; misc[S_F] = 0; }
+    if (tid == 0) { misc[S_SWT] = 0; misc[S_F] = 0; misc[S_FB] = 0; }
     __syncthreads();
     FWBF_PH(1)
     if (tid == 0) {
@@ -438,7 +442,11 @@ decode_kernel(const __grid_constant__ KParams P) {
       if (k >= P.kmax) break;
 
       // ---- Eq.(1) metric for every bit -> Ebuf ----
-      if (tid == 0) misc[S_F] = 0; // last read before the previous refresh barrier
+      const int fs = (fused && (k & 1)) ? S_FB : S_F; // this iteration's flip counter
+      // reset: non-fused, this iteration's counter (last read before the previous
+      // refresh barrier); fused, the next iteration's (it is written during the
+      // metric pass, so it must be zero before this iteration's last barrier)
+      if (tid == 0) misc[fused ? (S_F + S_FB - fs) : S_F] = 0;
       if (kGuard && WT > 0 && split && (KC % 2) == 0) {
         // Split-fp32 gather, 4 B per edge and no per-edge argmin select:
         // thread tid owns column pairs (2 tid + 2 T qp, +1).  Column n reads
@@ -554,6 +562,69 @@ decode_kernel(const __grid_constant__ KParams P) {
           }
         }
       } else {
+        // ordered column sum for explicit / QC codes (ascending checks)
+        auto col_sum = [&](const int n) -> double {
+          double acc = 0.0;
+          if (P.qc_z) {
+            // column cb*Z + o meets row block r at check r*Z + ((o - s) mod Z):
+            // ascending in r, i.e. the reference's ascending check order
+            const int Z = P.qc_z, cb = n >> qlz, o = n & (Z - 1);
+            for (int r = 0; r < P.qc_jb; ++r) {
+              const int sh = P.qc_shift[r * P.qc_kb + cb];
+              if (sh < 0) continue;
+              const int m = r * Z + ((o - sh) & (Z - 1));
+              acc = __dadd_rn(acc, ((amin[m] == n) ? chk2 : chk1)[m]); // one 8-byte load
+            }
+          } else {
+            const int e0 = __ldg(P.col_ptr + n), e1 = __ldg(P.col_ptr + n + 1);
+            for (int e = e0; e < e1; ++e) {
+              const int m = __ldg(P.col_idx + e);
+              acc = __dadd_rn(acc, ((amin[m] == n) ? chk2 : chk1)[m]);
+            }
+          }
+          return acc;
+        };
+        if (fused) {
+          // Warp w owns p-blocks w, w + nwarps, ...: lane l takes the block's
+          // columns l, l + 32, ... (ascending, strict >); a butterfly argmax
+          // with lowest-index ties gives the block's first maximum
+          // (decoders.py:156-167) and the warp applies the flip when it is > 0
+          // (decoders.py:181-183).  The metric never goes to shared memory.
+          const int p = P.p, nb = P.nblocks;
+          for (int b = warp; b < nb; b += nwarps) {
+            double v = -dinf();
+            int i = 0x7fffffff;
+            const int base = b * p, lim = min(p, N - base);
+            for (int o = lane; o < lim; o += 32) {
+              const int n = base + o;
+              const double e = __dsub_rn(col_sum(n), __dmul_rn(P.alpha, fabs((double)ybuf[n])));
+              if (e > v) { v = e; i = n; }
+            }
+            warp_amax(v, i);
+            if (lane == 0) { blk_v[b] = v; blk_i[b] = i; }
+            if (v > 0.0) {
+              if (lane == 0) {
+                atomicXor(&zbits[i >> 5], 1u << (i & 31));
+                atomicAdd(&misc[fs], 1);
+              }
+              if (P.qc_z) {
+                const int Z = P.qc_z, cb = i >> qlz, o = i & (Z - 1);
+                for (int r = lane; r < P.qc_jb; r += 32) {
+                  const int sh = P.qc_shift[r * P.qc_kb + cb];
+                  if (sh < 0) continue;
+                  const int m = r * Z + ((o - sh) & (Z - 1));
+                  atomicXor(&sbits[m >> 5], 1u << (m & 31));
+                }
+              } else {
+                const int e1 = __ldg(P.col_ptr + i + 1);
+                for (int e = __ldg(P.col_ptr + i) + lane; e < e1; e += 32) {
+                  const int m = __ldg(P.col_idx + e);
+                  atomicXor(&sbits[m >> 5], 1u << (m & 31));
+                }
+              }
+            }
+          }
+        } else {
         // y of the next column is fetched one column ahead (from global memory
         // when the metric buffer overlays y) so its latency hides behind a gather
         YT ynext = (tid < N) ? (P.alias_y ? load_y<YT>(P, f, tid) : ybuf[tid]) : YT(0);
@@ -582,26 +653,11 @@ decode_kernel(const __grid_constant__ KParams P) {
                 acc = __dadd_rn(acc, (((mkh >> (i - 32)) & 1u) ? c2 : c1)[d]);
               }
             }
-          } else if (P.qc_z) {
-            // column cb*Z + o meets row block r at check r*Z + ((o - s) mod Z):
-            // ascending in r, i.e. the reference's ascending check order
-            const int Z = P.qc_z, cb = n >> qlz, o = n & (Z - 1);
-            for (int r = 0; r < P.qc_jb; ++r) {
-              const int sh = P.qc_shift[r * P.qc_kb + cb];
-              if (sh < 0) continue;
-              const int m = r * Z + ((o - sh) & (Z - 1));
-              const double w = ((amin[m] == n) ? chk2 : chk1)[m]; // one 8-byte load
-              acc = __dadd_rn(acc, w);
-            }
           } else {
-            const int e0 = __ldg(P.col_ptr + n), e1 = __ldg(P.col_ptr + n + 1);
-            for (int e = e0; e < e1; ++e) {
-              const int m = __ldg(P.col_idx + e);
-              const double w = ((amin[m] == n) ? chk2 : chk1)[m]; // one 8-byte load
-              acc = __dadd_rn(acc, w);
-            }
+            acc = col_sum(n);
           }
           Ebuf[n] = __dsub_rn(acc, __dmul_rn(P.alpha, fabs((double)ycur)));
+        }
         }
       }
       __syncthreads();
@@ -619,7 +675,7 @@ decode_kernel(const __grid_constant__ KParams P) {
         const int p = P.p;
         const int nb = P.nblocks;
         const int TPB = 1 << sel_lt;
-        const int sub = sel_sub, gpc = sel_gpc, slot = sel_slot, rounds = sel_rounds;
+        const int sub = sel_sub, gpc = sel_gpc, slot = sel_slot, rounds = fused ? 0 : sel_rounds;
         for (int r = 0; r < rounds; ++r) {
           const int b = r * gpc + slot;
           const bool ok = b < nb;
@@ -670,9 +726,9 @@ decode_kernel(const __grid_constant__ KParams P) {
             }
           }
         }
-        __syncthreads();
+        if (!fused) __syncthreads(); // fused: block results and flips came with the metric pass
         FWBF_PH(4)
-        F = misc[S_F];
+        F = misc[fs];
         if (F > 0) {
           applied = true;
           if (P.fliplog && warp == 0) { // ascending = block order

@@ -23,6 +23,10 @@ CASES = [
     ("eg6", "fwbf", dict(block_len_p=128, k_max=100), 4.5, 1 << 11),
     ("gal504", "fwbf", dict(block_len_p=24, k_max=50), 4.0, 10000),
     ("qc4x32", "fwbf", dict(block_len_p=256, k_max=50), 5.0, 1 << 8),
+    # explicit / QC codes with 32 | p take the fused metric + block-argmax pass
+    ("gal504", "fwbf", dict(block_len_p=32, k_max=50), 3.5, 4096),
+    ("gal504", "fwbf", dict(block_len_p=64, k_max=50, stall_policy="terminate"), 3.0, 4096),
+    ("qc4x32", "fwbf", dict(block_len_p=32, k_max=30), 4.5, 1 << 7),
 ]
 
 
@@ -47,7 +51,8 @@ def test_scale_parity_vs_c_oracle(cuda_device, code, alg, kw, ebn0, frames):
     p = kw.get("block_len_p")
     z, its, fl, ft = COracle(h).decode_batch(y.cpu().numpy(), algorithm=alg, alpha=cfg.alpha,
                                              k_max=cfg.k_max, lam=cfg.lam, p=p,
-                                             weight_mode=cfg.weight_mode)
+                                             weight_mode=cfg.weight_mode, stall=cfg.stall_policy,
+                                             mlp_threshold=cfg.mlp_threshold)
     _cmp(res, z, its, fl, ft, f"{code}/{alg}/{ebn0}")
 
 
@@ -62,3 +67,24 @@ def test_scale_parity_device_noise(cuda_device, noise):
     z, its, fl, ft = COracle(h).decode_batch(res.y.cpu().numpy(), algorithm="fwbf", alpha=0.2,
                                              k_max=100, p=31)
     _cmp(res, z, its, fl, ft, f"awgn-{noise}")
+
+
+@pytest.mark.parametrize("code,p,stall,dtype", [
+    ("gal504", 32, "flip-global-max", "f32"), ("gal504", 96, "terminate", "f32"),
+    ("gal504", 64, "flip-global-max", "f64"), ("qc4x32", 256, "flip-global-max", "f32"),
+    ("qc4x32", 512, "terminate", "f64")])
+def test_fused_pass_matches_unfused(cuda_device, monkeypatch, code, p, stall, dtype):
+    """The fused metric + block-argmax pass (explicit/QC, 32 | p) gives the same
+    flip sequence as the metric-buffer path, frame by frame."""
+    h = build_code(code)
+    n = h.n_cols
+    rng = np.random.default_rng(p)
+    sigma = 0.62 if code == "gal504" else 0.45
+    y = (1.0 + sigma * rng.standard_normal((256, n))).astype(np.float32 if dtype == "f32" else np.float64)
+    cfg = DecoderConfig(block_len_p=p, k_max=40, stall_policy=stall)
+    a = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+    monkeypatch.setenv("FWBF_NO_FUSED", "1")
+    b = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+    assert np.array_equal(a.iterations.cpu().numpy(), b.iterations.cpu().numpy())
+    assert np.array_equal(a.flags.cpu().numpy(), b.flags.cpu().numpy())
+    assert a.flip_logs() == b.flip_logs()
