@@ -563,17 +563,21 @@ decode_kernel(const __grid_constant__ KParams P) {
         }
       } else {
         // ordered column sum for explicit / QC codes (ascending checks)
-        auto col_sum = [&](const int n) -> double {
+        auto col_sum = [chk1, chk2, amin, qlz, &P](const int n) -> double {
           double acc = 0.0;
           if (P.qc_z) {
             // column cb*Z + o meets row block r at check r*Z + ((o - s) mod Z):
-            // ascending in r, i.e. the reference's ascending check order
+            // ascending in r, i.e. the reference's ascending check order.  An
+            // absent block (s < 0) adds +0.0, which leaves acc unchanged (acc
+            // starts at +0.0 and round-to-nearest never produces -0.0 from it).
             const int Z = P.qc_z, cb = n >> qlz, o = n & (Z - 1);
-            for (int r = 0; r < P.qc_jb; ++r) {
-              const int sh = P.qc_shift[r * P.qc_kb + cb];
-              if (sh < 0) continue;
-              const int m = r * Z + ((o - sh) & (Z - 1));
-              acc = __dadd_rn(acc, ((amin[m] == n) ? chk2 : chk1)[m]); // one 8-byte load
+            const int jb = P.qc_jb, kb = P.qc_kb;
+#pragma unroll 4
+            for (int r = 0; r < jb; ++r) {
+              const int sh = P.qc_shift[r * kb + cb];
+              const int m = (r << qlz) + ((o - sh) & (Z - 1));
+              const double w = ((amin[m] == n) ? chk2 : chk1)[m]; // one 8-byte load
+              acc = __dadd_rn(acc, sh >= 0 ? w : 0.0);
             }
           } else {
             const int e0 = __ldg(P.col_ptr + n), e1 = __ldg(P.col_ptr + n + 1);
