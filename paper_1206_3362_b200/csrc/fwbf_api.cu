@@ -494,6 +494,11 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   // metric buffer); 512 threads so two CTAs share an SM on large codes
   P.fused = !circ && p->algorithm == FWBF_ALG_FWBF && p->block_len_p % 32 == 0 && !getenv("FWBF_NO_FUSED");
   if (P.fused && T > 512) T = 512;
+  // small explicit codes: ~8 columns per thread and more, smaller CTAs per SM
+  // (the per-iteration barriers and serial phases cost less; A: 64 threads +40%)
+  if (!circ && !P.fused && c->n <= 2048) T = std::min(256, std::max(64, ((c->n + 7) / 8 + 31) / 32 * 32));
+  if (!circ)
+    if (const char *e = getenv("FWBF_EXPLICIT_T")) T = atoi(e); // tuning: threads per CTA (multiple of 32)
   const bool compact = circ && sizeof(YT) == 4 && c->w <= 32 && !getenv("FWBF_NO_COMPACT");
   layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, P.fused);
   if (P.fused && P.smem_bytes > c->smem_optin) { // y must stay resident for the fused pass
