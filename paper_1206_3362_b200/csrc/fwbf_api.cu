@@ -58,6 +58,7 @@ struct fwbf_code {
   unsigned char jii[fwbf::kMaxCircWeight] = {0};
   int *d_row_ptr = nullptr, *d_row_idx = nullptr, *d_col_ptr = nullptr, *d_col_idx = nullptr;
   uint8_t *d_i0tab = nullptr;
+  uint8_t *d_jwtab = nullptr;
   int16_t *d_offpos = nullptr;
   unsigned int *d_work = nullptr; // ring of per-launch work counters
   std::atomic<unsigned> work_slot{0};
@@ -156,7 +157,7 @@ extern "C" int fwbf_code_create(const fwbf_code_desc *desc, int device, fwbf_cod
   c->dv_max = dvm;
   c->dc_max = dcm;
   c->min_row_w = minrw;
-  std::vector<uint8_t> i0tab;
+  std::vector<uint8_t> i0tab, jwtab;
   std::vector<int16_t> offpos;
   if (desc->circulant) {
     c->circ = 1;
@@ -176,6 +177,13 @@ extern "C" int fwbf_code_create(const fwbf_code_desc *desc, int device, fwbf_cod
       int i0 = 0;
       while (i0 < w && col + dn[i0] < n) ++i0;
       i0tab[col] = (uint8_t)(i0 == w ? 0 : i0);
+    }
+    // check m's columns m + c_j wrap (>= n) from j = jwtab[m] on
+    jwtab.resize(n);
+    for (int m = 0; m < n; ++m) {
+      int j = 0;
+      while (j < w && m + desc->offsets[j] < n) ++j;
+      jwtab[m] = (uint8_t)j;
     }
     offpos.assign(n, (int16_t)-1);
     for (int j = 0; j < w; ++j) offpos[desc->offsets[j]] = (int16_t)j;
@@ -211,7 +219,7 @@ extern "C" int fwbf_code_create(const fwbf_code_desc *desc, int device, fwbf_cod
   if (ce != cudaSuccess) { delete c; return fail(FWBF_ECUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(ce)); }
   if ((rc = upload(&c->d_row_ptr, row_ptr)) || (rc = upload(&c->d_row_idx, row_idx)) ||
       (rc = upload(&c->d_col_ptr, col_ptr)) || (rc = upload(&c->d_col_idx, col_idx)) ||
-      (rc = upload(&c->d_i0tab, i0tab)) || (rc = upload(&c->d_offpos, offpos))) {
+      (rc = upload(&c->d_i0tab, i0tab)) || (rc = upload(&c->d_jwtab, jwtab)) || (rc = upload(&c->d_offpos, offpos))) {
     fwbf_code_destroy(c);
     return rc;
   }
@@ -231,6 +239,7 @@ extern "C" int fwbf_code_destroy(fwbf_code *c) {
   cudaFree(c->d_col_ptr);
   cudaFree(c->d_col_idx);
   cudaFree(c->d_i0tab);
+  cudaFree(c->d_jwtab);
   cudaFree(c->d_offpos);
   cudaFree(c->d_work);
   for (int i = 0; i < 2; ++i) {
@@ -358,7 +367,7 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
   P.off_blkv = take(nslots * 8);
   P.off_blki = take((nslots + zw) * 4);
   P.off_flips = take(maxf * 4);
-  P.off_offs = take(3 * fwbf::kMaxCircWeight * 4); // off[64], dneg doubled [128]
+  P.off_offs = take(5 * fwbf::kMaxCircWeight * 4); // off[64], dneg doubled [128], rotated offsets [128]
   P.off_red = take(32 * 8 + 32 * 4);
   P.off_misc = take(16 * 4 + 64 * 4);
   P.smem_bytes = o;
@@ -396,6 +405,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   memcpy(P.dneg, c->dneg, sizeof P.dneg);
   memcpy(P.jii, c->jii, sizeof P.jii);
   P.i0tab = c->d_i0tab;
+  P.jwtab = c->d_jwtab;
   P.offpos = c->d_offpos;
   P.row_ptr = c->d_row_ptr;
   P.row_idx = c->d_row_idx;

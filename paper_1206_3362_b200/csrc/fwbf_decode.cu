@@ -187,7 +187,13 @@ decode_kernel(const __grid_constant__ KParams P) {
   const int qlz = P.qc_z ? __ffs(P.qc_z) - 1 : 0; // log2 Z (QC: Z a power of two)
 
   if (CIRC) {
-    for (int j = tid; j < W; j += T) { offs_s[j] = P.off[j]; offs_s[64 + j] = P.dneg[j]; offs_s[64 + W + j] = P.dneg[j]; }
+    for (int j = tid; j < W; j += T) {
+      offs_s[j] = P.off[j];
+      offs_s[64 + j] = P.dneg[j];
+      offs_s[64 + W + j] = P.dneg[j];
+      offs_s[192 + j] = P.off[j] - N; // rotated walk of a check's columns: the
+      offs_s[192 + W + j] = P.off[j]; // wrapped (smaller) ones first, no wrap test
+    }
   }
   if (tid == 0) misc[S_NONFIN] = 0;
 
@@ -310,6 +316,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     double *sAY = reinterpret_cast<double *>(smem_raw + P.off_ay); // split: fl(alpha |y_n|)
 
     // ---------------- init 2: per-check minima, syndrome, signed weights --------
+    const bool nonfin_frame = misc[S_NONFIN] != 0; // NaN/inf: keep the compare-based scan
     uint32_t sprev = 0; // syndrome bits of this thread's checks tid + k*T
     for (int k = 0; k < nKm; ++k) {
       const int m = tid + k * T;
@@ -318,7 +325,22 @@ decode_kernel(const __grid_constant__ KParams P) {
       YT min1 = YT(INFINITY), min2 = YT(INFINITY);
       int ac = 0x7fffffff;
       if (ok) {
-        if (CIRC) {
+        if (kGuard && !nonfin_frame) {
+          // columns in ascending order (m + c_j - N for j >= jw, then m + c_j),
+          // so strict < keeps the lowest column on ties; min2 = second smallest
+          // of the multiset (min(min2, max(min1, a)))
+          const int *orr = offs_s + 192 + __ldg(P.jwtab + m);
+          for (int t = 0; t < W; ++t) {
+            const int c = m + orr[t];
+            const YT yv = ybuf[c];
+            par ^= (yv < YT(0));
+            const YT a = fabs(yv);
+            const bool lt = a < min1;
+            min2 = fminf(min2, fmaxf(min1, a));
+            min1 = fminf(min1, a);
+            ac = lt ? c : ac;
+          }
+        } else if (CIRC) {
           for (int j = 0; j < W; ++j) {
             int c = m + P.off[j];
             if (c >= N) c -= N;

@@ -35,6 +35,7 @@ struct KParams {
   int dneg[kMaxCircWeight]; // sorted (n - c_j) mod n, ascending (ordered column walk)
   unsigned char jii[kMaxCircWeight]; // offset index j -> its position in dneg
   const uint8_t *i0tab;     // circulant: first dneg index of column n's ascending walk
+  const uint8_t *jwtab;     // circulant: first j with m + c_j >= n (check m's wrap point)
   const int16_t *offpos;    // circulant: offpos[d] = j if c_j == d else -1
   const int *row_ptr, *row_idx; // CSR, sorted columns
   const int *col_ptr, *col_idx; // CSC, ascending checks
