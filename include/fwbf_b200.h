@@ -138,6 +138,18 @@ int fwbf_decode_f32(fwbf_code *code, const fwbf_params *params, const float *y,
 int fwbf_decode_f64(fwbf_code *code, const fwbf_params *params, const double *y,
                     int64_t batch, int64_t ld, const fwbf_outputs *out, void *stream);
 
+/* Stage view (tests, diagnostics): the Eq.(1) metric vector each frame's
+ * decode would compute in its first iteration -- all_metrics on the initial
+ * hard decisions (decoders.py:148-153 with the weights of :80-103) -- written
+ * to metric[f * metric_ld + n] (device memory, float64).  flags (nullable)
+ * receive the per-frame metric path (FWBF_FLAG_ORDERED / FWBF_FLAG_SPLIT32).
+ * Same params, validation and path choice as fwbf_decode_*; the metric is
+ * produced even when the initial syndrome is already zero. */
+int fwbf_metric_f32(fwbf_code *code, const fwbf_params *params, const float *y, int64_t batch,
+                    int64_t ld, double *metric, int64_t metric_ld, uint8_t *flags, void *stream);
+int fwbf_metric_f64(fwbf_code *code, const fwbf_params *params, const double *y, int64_t batch,
+                    int64_t ld, double *metric, int64_t metric_ld, uint8_t *flags, void *stream);
+
 /* Noise modes for fwbf_decode_awgn. */
 #define FWBF_NOISE_NUMPY_F64 0 /* the reference stream: numpy Philox(key=seed,
                                   counter=frame<<128) + Generator.standard_normal,

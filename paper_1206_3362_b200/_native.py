@@ -26,7 +26,8 @@ NOISE_NUMPY_F64, NOISE_NUMPY_F32 = 0, 1
 
 EXPORTS = ("fwbf_abi_version", "fwbf_last_error", "fwbf_device_count", "fwbf_code_create",
            "fwbf_code_destroy", "fwbf_code_info", "fwbf_max_flips_per_iter", "fwbf_decode_f32",
-           "fwbf_decode_f64", "fwbf_decode_awgn", "fwbf_decode_host_f32")
+           "fwbf_decode_f64", "fwbf_decode_awgn", "fwbf_decode_host_f32", "fwbf_metric_f32",
+           "fwbf_metric_f64")
 
 
 class CodeDesc(C.Structure):
@@ -87,6 +88,9 @@ def lib() -> C.CDLL:
                                            C.c_double, C.c_int32, C.POINTER(Outputs), vp]
             L.fwbf_decode_host_f32.argtypes = [vp, C.POINTER(Params), vp, C.c_int64, C.c_int64,
                                                vp, C.c_int64, vp, vp, vp, C.c_int64]
+            L.fwbf_metric_f32.argtypes = [vp, C.POINTER(Params), vp, C.c_int64, C.c_int64, vp, C.c_int64,
+                                          vp, vp]
+            L.fwbf_metric_f64.argtypes = L.fwbf_metric_f32.argtypes
             for f in EXPORTS:
                 if f not in ("fwbf_abi_version", "fwbf_last_error", "fwbf_device_count",
                              "fwbf_max_flips_per_iter"):

@@ -375,7 +375,8 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
 
 template <typename YT>
 static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long long batch,
-                         long long ld, const fwbf_outputs *out, cudaStream_t stream) {
+                         long long ld, const fwbf_outputs *out, cudaStream_t stream,
+                         double *metric_out = nullptr, long long metric_ld = 0) {
   int rc = validate(c, p);
   if (rc) return rc;
   if (batch < 0) return fail(FWBF_EINVAL, "batch must be nonnegative");
@@ -502,7 +503,10 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   }
   // explicit/QC FWBF with 32 | p: metric and block argmax in one warp pass (no
   // metric buffer); 512 threads so two CTAs share an SM on large codes
-  P.fused = !circ && p->algorithm == FWBF_ALG_FWBF && p->block_len_p % 32 == 0 && !getenv("FWBF_NO_FUSED");
+  P.fused = !circ && p->algorithm == FWBF_ALG_FWBF && p->block_len_p % 32 == 0 && !getenv("FWBF_NO_FUSED") &&
+            !metric_out;
+  P.metric_out = metric_out;
+  P.metric_ld = metric_ld;
   if (P.fused && T > 512) T = 512;
   // small explicit codes: ~8 columns per thread and more, smaller CTAs per SM
   // (the per-iteration barriers and serial phases cost less; A: 64 threads +40%)
@@ -601,6 +605,27 @@ extern "C" int fwbf_decode_f32(fwbf_code *c, const fwbf_params *p, const float *
 extern "C" int fwbf_decode_f64(fwbf_code *c, const fwbf_params *p, const double *y, int64_t batch,
                                int64_t ld, const fwbf_outputs *out, void *stream) {
   return launch_decode<double>(c, p, y, batch, ld, out, (cudaStream_t)stream);
+}
+
+template <typename YT>
+static int metric_t(fwbf_code *c, const fwbf_params *p, const YT *y, int64_t batch, int64_t ld, double *metric,
+                    int64_t metric_ld, uint8_t *flags, void *stream) {
+  if (!c) return fail(FWBF_EINVAL, "code is null");
+  if (batch > 0 && !metric) return fail(FWBF_EINVAL, "metric is null");
+  if (metric_ld < c->n) return fail(FWBF_EINVAL, "metric_ld must be at least n (%d)", c->n);
+  fwbf_outputs o{};
+  o.flags = flags;
+  return launch_decode<YT>(c, p, y, batch, ld, &o, (cudaStream_t)stream, metric, metric_ld);
+}
+
+extern "C" int fwbf_metric_f32(fwbf_code *c, const fwbf_params *p, const float *y, int64_t batch, int64_t ld,
+                               double *metric, int64_t metric_ld, uint8_t *flags, void *stream) {
+  return metric_t<float>(c, p, y, batch, ld, metric, metric_ld, flags, stream);
+}
+
+extern "C" int fwbf_metric_f64(fwbf_code *c, const fwbf_params *p, const double *y, int64_t batch, int64_t ld,
+                               double *metric, int64_t metric_ld, uint8_t *flags, void *stream) {
+  return metric_t<double>(c, p, y, batch, ld, metric, metric_ld, flags, stream);
 }
 
 // Reference-channel decode: per chunk, noise_kernel writes the chunk's

@@ -287,13 +287,17 @@ decode_kernel(const __grid_constant__ KParams P) {
           // quantum q = 2^(e-23); need 2*dv*max|y| < 2^53 * q = 2^(30+e)
           double lhs = 2.0 * (double)W * (double)mx;
           fast = lhs < ldexp(1.0, 30 + e);
-          // split-fp32: grid G = 2^20 q = 2^(e-3); every column sum of |w| must
-          // stay below 2^(20+e) so hi (multiples of G) and lo (multiples of q,
-          // |lo| <= 16G) sums are exact in fp32; C = 1.5 * 2^23 * G
-          if (fast && WT > 0 && (KC % 2) == 0 && e >= -100 && !P.no_split &&
-              (double)W * (double)mx <= ldexp(1.0, 20 + e)) {
+          // split-fp32: grid G = 2^g q with W * 2^(g-1) <= 2^24 (g = 20 for
+          // W <= 32, 19 for W <= 64), so every partial lo sum (multiples of q,
+          // |l| <= G/2) stays within 2^24 q; every column sum of |w| must stay
+          // below 2^23 G = 2^(g+e) so the hi sums (multiples of G, plus at most
+          // W G/2 of rounding) stay below 2^24 G.  Both exact in fp32.
+          // C = 1.5 * 2^23 * G keeps t = v + C in [2^23 G, 2^24 G].
+          constexpr int kG = (WT > 32) ? 19 : 20;
+          if (fast && WT > 0 && WT <= 64 && (KC % 2) == 0 && e >= -100 && !P.no_split &&
+              (double)W * (double)mx <= ldexp(1.0, kG + e)) {
             fast = 2;
-            cmag = ldexpf(1.5f, 20 + e);
+            cmag = ldexpf(1.5f, kG + e);
           }
           misc[S_EQ] = e - 23; // quantum q = 2^(e-23)
         }
@@ -460,7 +464,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     long long flips_total = 0;
     for (;;) {
       const int swt = misc[S_SWT];
-      if (swt == 0) { conv = 1; break; }
+      if (swt == 0 && !P.metric_out) { conv = 1; break; }
       if (k >= P.kmax) break;
 
       // ---- Eq.(1) metric for every bit -> Ebuf ----
@@ -688,6 +692,10 @@ decode_kernel(const __grid_constant__ KParams P) {
       }
       __syncthreads();
       FWBF_PH(3)
+      if (P.metric_out) { // stage view (fwbf_metric_*): Eq.(1) on the initial state, then stop
+        for (int n = tid; n < N; n += T) P.metric_out[f * P.metric_ld + n] = Ebuf[n];
+        break;
+      }
 
       // ---- selection (+ fused flips for FWBF) ----
       if (tid == 0) misc[S_SWT] = 0; // every thread read it at the loop top (before the E barrier)

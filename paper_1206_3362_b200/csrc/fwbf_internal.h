@@ -77,6 +77,8 @@ struct KParams {
   int off_fa, off_fb, off_m2s, off_a2m, off_corr, off_ay; // split-fp32 path arrays (inside the chk region)
   int has_ay; // split path keeps fl(alpha|y|) per column in shared memory (compact layout)
   int fused;  // explicit/QC FWBF with p % 32 == 0: metric + block argmax in one pass, no metric buffer
+  double *metric_out;       // stage view: first-iteration metric per frame (then stop), or null
+  long long metric_ld;
   int uoff[kMaxCircWeight]; // split-fp32 gather: byte offset of check (n - c_j) for even n, minus 4n
   int no_split; // disable the split-fp32 path (testing)
 };

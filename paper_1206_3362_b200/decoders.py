@@ -318,6 +318,39 @@ def decode_batch(h, y, cfg: DecoderConfig, algorithm: str = "fwbf", *, flip_log:
     return res
 
 
+def metric_batch(h, y, cfg: DecoderConfig = DecoderConfig(), algorithm: str = "fwbf", *,
+                 force_ordered=False, device=None):
+    """Stage view: the Eq.(1) metric of each frame's first iteration (the
+    reference's ``all_metrics`` on the initial hard decisions with the weights
+    of ``compute_weights``/``edge_weights``, decoders.py:80-103,148-153),
+    computed by the decode kernel itself.  Returns (E float64 [B, N] torch
+    tensor on the device, per-frame flags uint8)."""
+    torch = _torch()
+    if not isinstance(y, torch.Tensor):
+        arr = np.asarray(y)
+        if arr.dtype not in (np.float32, np.float64):
+            arr = arr.astype(np.float64)
+        y = torch.from_numpy(np.ascontiguousarray(arr))
+    if y.dim() == 1:
+        y = y.unsqueeze(0)
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    y = y.to(dev).contiguous()
+    dc = device_code(h, dev.index if dev.index is not None else 0)
+    if y.shape[1] != dc.n:
+        raise ValueError(f"expected a length-{dc.n} frame")
+    B = int(y.shape[0])
+    E = torch.empty((B, dc.n), dtype=torch.float64, device=dev)
+    flags = torch.zeros(B, dtype=torch.uint8, device=dev)
+    p = make_params(cfg, algorithm, force_ordered)
+    L = nat.lib()
+    fn = L.fwbf_metric_f32 if y.dtype == torch.float32 else L.fwbf_metric_f64
+    st = torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        nat.check(fn(dc.handle, C.byref(p), C.c_void_p(y.data_ptr()), B, dc.n, C.c_void_p(E.data_ptr()),
+                     dc.n, C.c_void_p(flags.data_ptr()), C.c_void_p(st.cuda_stream)), "metric")
+    return E, flags
+
+
 def decode_awgn(h, cfg: DecoderConfig, algorithm: str, seed: int, first_frame: int, count: int,
                 sigma: float, *, codeword=None, noise: str = "f64", flip_log: bool = False,
                 device=None, force_ordered: bool = False, stream=None,
