@@ -281,6 +281,7 @@ decode_kernel(const __grid_constant__ KParams P) {
       if (CIRC && sizeof(YT) == 4 && !P.force_ordered && !misc[S_NONFIN]) {
         if (!(mn < INFINITY)) {
           fast = 1; // all |y| == 0: every weight is 0, sums trivially exact
+          misc[S_EQ] = -200; // (no quantum: keeps the split re-check below off)
         } else {
           int e = ((__float_as_int(mn) >> 23) & 0xff) - 127;
           if (e < -126) e = -126;
@@ -306,12 +307,12 @@ decode_kernel(const __grid_constant__ KParams P) {
       misc[S_FAST] = fast;
     }
     __syncthreads();
-    const int fpath = misc[S_FAST];
-    const bool fastp = fpath != 0;
-    const bool split = fpath == 2;
-    const float cmag = redf[0];
-    const double qexp = split ? ldexp(1.0, misc[S_EQ]) : 0.0;      // q
-    const double qinv = split ? ldexp(1.0, -misc[S_EQ]) : 0.0;     // 1/q
+    int fpath = misc[S_FAST];
+    bool fastp = fpath != 0;
+    bool split = fpath == 2;
+    float cmag = redf[0];
+    double qexp = split ? ldexp(1.0, misc[S_EQ]) : 0.0;      // q
+    double qinv = split ? ldexp(1.0, -misc[S_EQ]) : 0.0;     // 1/q
     float *sFA = reinterpret_cast<float *>(smem_raw + P.off_fa);   // split: signed min1, 8B-aligned at even n
     float *sFB = reinterpret_cast<float *>(smem_raw + P.off_fb);   // split: same, shifted by one element
     int *sM2 = reinterpret_cast<int *>(smem_raw + P.off_m2s);      // split: correction limb deltas per check
@@ -322,6 +323,169 @@ decode_kernel(const __grid_constant__ KParams P) {
     // ---------------- init 2: per-check minima, syndrome, signed weights --------
     const bool nonfin_frame = misc[S_NONFIN] != 0; // NaN/inf: keep the compare-based scan
     uint32_t sprev = 0; // syndrome bits of this thread's checks tid + k*T
+    // Circulant float32 kernels with compile-time shape keep each check's
+    // (min1, min2, argmin) in registers between the scan and the stores: the
+    // split-fp32 guard can then be re-evaluated on the largest min1 (the
+    // values the split sums actually see) instead of max|y| -- about ten times
+    // looser -- before any path-specific state is written.
+    constexpr bool kTwoPhase = kGuard && TB > 0 && WT > 0 && (KC % 2) == 0 && WT <= 64;
+    constexpr int KR = kTwoPhase ? KC : 1;
+    YT r_min1[KR], r_min2[KR];
+    int r_ac[KR];
+    if (kTwoPhase) {
+      float wmax = 0.f; // largest min1 of this thread's checks
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        const int m = tid + k * T;
+        const bool ok = m < M;
+        int par = 0;
+        YT min1 = YT(INFINITY), min2 = YT(INFINITY);
+        int ac = 0x7fffffff;
+        if (ok) {
+          if (kGuard && !nonfin_frame) {
+            // columns in ascending order (m + c_j - N for j >= jw, then m + c_j),
+            // so strict < keeps the lowest column on ties; min2 = second smallest
+            // of the multiset (min(min2, max(min1, a)))
+            const int *orr = offs_s + 192 + __ldg(P.jwtab + m);
+            for (int t = 0; t < W; ++t) {
+              const int c = m + orr[t];
+              const YT yv = ybuf[c];
+              par ^= (yv < YT(0));
+              const YT a = fabs(yv);
+              const bool lt = a < min1;
+              min2 = fminf(min2, fmaxf(min1, a));
+              min1 = fminf(min1, a);
+              ac = lt ? c : ac;
+            }
+          } else if (CIRC) {
+            for (int j = 0; j < W; ++j) {
+              int c = m + P.off[j];
+              if (c >= N) c -= N;
+              const YT yv = ybuf[c];
+              par ^= (yv < YT(0));
+              const YT a = fabs(yv);
+              if (a < min1 || (a == min1 && c < ac)) { min2 = min1; min1 = a; ac = c; }
+              else if (a < min2) min2 = a;
+            }
+          } else if (P.qc_z) {
+            // quasi-cyclic: row r*Z + i holds column cb*Z + ((i + s[r][cb]) mod Z)
+            const int Z = P.qc_z, r = m >> qlz, ii = m & (Z - 1);
+            for (int cb = 0; cb < P.qc_kb; ++cb) {
+              const int sh = P.qc_shift[r * P.qc_kb + cb];
+              if (sh < 0) continue;
+              const int c = cb * Z + ((ii + sh) & (Z - 1));
+              const YT yv = ybuf[c];
+              par ^= (yv < YT(0));
+              const YT a = fabs(yv);
+              if (a < min1 || (a == min1 && c < ac)) { min2 = min1; min1 = a; ac = c; }
+              else if (a < min2) min2 = a;
+            }
+          } else {
+            const int e0 = __ldg(P.row_ptr + m), e1 = __ldg(P.row_ptr + m + 1);
+            for (int e = e0; e < e1; ++e) {
+              const int c = __ldg(P.row_idx + e);
+              const YT yv = ybuf[c];
+              par ^= (yv < YT(0));
+              const YT a = fabs(yv);
+              if (a < min1 || (a == min1 && c < ac)) { min2 = min1; min1 = a; ac = c; }
+              else if (a < min2) min2 = a;
+            }
+          }
+        }
+        if (ok && par) sprev |= 1u << k;
+        const uint32_t b = __ballot_sync(FULL_MASK, ok && par);
+        if (lane == 0 && (k * T + warp * 32) < M) {
+          sbits[(k * T + warp * 32) >> 5] = b;
+          atomicAdd(&misc[S_SWT], __popc(b));
+        }
+        r_min1[k] = min1;
+        r_min2[k] = min2;
+        r_ac[k] = ac;
+        if (ok) wmax = fmaxf(wmax, (float)min1);
+      }
+      if (fpath == 1 && !P.no_split && misc[S_EQ] >= -123) { // uniform: fp64-guarded, not yet split
+        for (int off = 16; off; off >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(FULL_MASK, wmax, off));
+        if (lane == 0) redf[32 + warp] = wmax; // init1's slots, already consumed
+        __syncthreads();
+        if (tid == 0) {
+          float mx1 = 0.f;
+          for (int w2 = 0; w2 < nwarps; ++w2) mx1 = fmaxf(mx1, redf[32 + w2]);
+          constexpr int kG = (WT > 32) ? 19 : 20;
+          const int e = misc[S_EQ] + 23;
+          if ((double)W * (double)mx1 <= ldexp(1.0, kG + e)) {
+            misc[S_FAST] = 2;
+            redf[1] = ldexpf(1.5f, kG + e);
+          }
+        }
+        __syncthreads();
+        if (misc[S_FAST] == 2) {
+          fpath = 2;
+          split = true;
+          cmag = redf[1];
+          qexp = ldexp(1.0, misc[S_EQ]);
+          qinv = ldexp(1.0, -misc[S_EQ]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        const int m = tid + k * T;
+        const bool ok = m < M;
+        const int par = (sprev >> k) & 1;
+        const YT min1 = r_min1[k], min2 = r_min2[k];
+        const int ac = r_ac[k];
+        if (ok) {
+          const double sg = par ? 1.0 : -1.0;
+          const double d1 = (double)min1, d2 = (double)min2;
+          if (kGuard && split) {
+            const float s1v = par ? (float)min1 : -(float)min1;
+            sFA[m] = s1v;
+            sFA[m + N] = s1v;
+            sFB[m + 1] = s1v;
+            sFB[m + N + 1] = s1v;
+            sA2[m] = (uint16_t)ac;
+            if (P.wmode == FWBF_WEIGHTS_IMWBF) { // column ac reads min2: + sgn*(min2-min1)
+              const long long D = (long long)__dmul_rn(__dsub_rn(d2, d1), qinv); // exact integer
+              corr_add(sCorr, ac, par ? D : -D, 1);
+              // limb change when s_m goes 0 -> 1 (negated for 1 -> 0)
+              int2 dl;
+              dl.x = (int)(D & 0xffffffll) - (int)((-D) & 0xffffffll);
+              dl.y = (int)(D >> 24) - (int)((-D) >> 24);
+              reinterpret_cast<int2 *>(sM2)[m] = dl;
+            }
+          } else if (kGuard && fastp) {
+            chk1[m] = sg * d1;
+            chk1[m + N] = sg * d1;
+            chk2[m] = sg * d2;
+            chk2[m + N] = sg * d2;
+            if (P.wmode == FWBF_WEIGHTS_IMWBF) {
+              // column ac reads min2 at its local check index j (m = ac - c_j)
+              int d = ac - m;
+              if (d < 0) d += N;
+              const int j = P.offpos[d];
+              atomicOr(&amask[ac * aw + (j >> 5)], 1u << (j & 31));
+            }
+          } else if (CIRC) {
+            // ordered path: doubled records as above; the argmin bit sits at the
+            // check's position in column ac's ascending check list
+            chk1[m] = sg * d1;
+            chk1[m + N] = sg * d1;
+            chk2[m] = sg * d2;
+            chk2[m + N] = sg * d2;
+            if (P.wmode == FWBF_WEIGHTS_IMWBF) {
+              int d = ac - m;
+              if (d < 0) d += N;
+              int i = (int)P.jii[P.offpos[d]] - (int)P.i0tab[ac];
+              if (i < 0) i += W;
+              atomicOr(&amask[ac * aw + (i >> 5)], 1u << (i & 31));
+            }
+          } else {
+            chk1[m] = sg * d1;
+            chk2[m] = sg * d2;
+            amin[m] = (P.wmode == FWBF_WEIGHTS_IMWBF) ? ac : -1;
+          }
+        }
+      }
+    } else {
     for (int k = 0; k < nKm; ++k) {
       const int m = tid + k * T;
       const bool ok = m < M;
@@ -436,6 +600,7 @@ decode_kernel(const __grid_constant__ KParams P) {
           amin[m] = (P.wmode == FWBF_WEIGHTS_IMWBF) ? ac : -1;
         }
       }
+    }
     }
     __syncthreads();
     FWBF_PH(2)
