@@ -669,8 +669,10 @@ static int decode_awgn_t(fwbf_code *c, const fwbf_params *p, uint64_t seed, int6
   for (long long s = 0; s < count; s += chunk) {
     const long long nb = std::min(chunk, count - s);
     YT *yb = o.y_out ? (YT *)o.y_out + s * ld : scratch;
-    const int grid = (int)std::min<long long>(nb, (long long)c->sm_count * 8);
-    nk<<<grid, 128, smem, stream>>>((unsigned long long)seed, first + s, nb, sigma, o.codeword_bits, yb, ld, n, pm);
+    static const int gmul = getenv("FWBF_NOISE_GRID") ? atoi(getenv("FWBF_NOISE_GRID")) : 32;
+    static const int nthr = getenv("FWBF_NOISE_T") ? atoi(getenv("FWBF_NOISE_T")) : 128;
+    const int grid = (int)std::min<long long>(nb, (long long)c->sm_count * gmul);
+    nk<<<grid, nthr, smem, stream>>>((unsigned long long)seed, first + s, nb, sigma, o.codeword_bits, yb, ld, n, pm);
     CUDA_TRY(cudaGetLastError());
     fwbf_outputs oc = o;
     if (o.z_bits) oc.z_bits = o.z_bits + s * o.z_ld;

@@ -11,7 +11,7 @@
 namespace fwbf {
 
 template <typename YT>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
 noise_kernel(unsigned long long seed, long long first, long long count, double sigma,
              const uint32_t *codeword, YT *y, long long ld, int n, int pm) {
   extern __shared__ __align__(16) unsigned long long scratch[];
