@@ -316,10 +316,16 @@ def main():
         bytes_frame = 4 * n + 4 * zw + 8
         launch_ms = ms_step  # one decode launch per step on this stream
         achieved = B * bytes_frame / (launch_ms / 1e3) / 1e9
-        traffic = None
+        # ncu DRAM bytes of one decode launch (profiles/roofline_traffic.json,
+        # captured on a smaller launch of the same workload) scaled per frame
+        # to this run's launch of B frames, like `achieved`
+        traffic, traffic_src = None, None
         try:
-            tr = json.load(open(os.path.join(REPO, "profiles", "roofline_traffic.json")))
-            traffic = tr.get(a.code, {}).get("dram_bytes_per_launch")
+            tr = json.load(open(os.path.join(REPO, "profiles", "roofline_traffic.json"))).get(a.code, {})
+            if tr.get("dram_bytes_per_frame"):
+                traffic = tr["dram_bytes_per_frame"] * B
+                traffic_src = (f"{tr.get('source')}: {tr['dram_bytes_per_frame']:.0f} B/frame measured on a "
+                               f"{tr.get('frames_per_launch')}-frame launch, x {B} frames")
         except OSError:
             pass
         edges = h.n_edges
@@ -339,7 +345,7 @@ def main():
                                   ordered_path_frames=int(cnt[nat.CNT_ORDERED_FRAMES]),
                                   frames_per_s=world * B / (ms_step / 1e3)),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
                          "bytes_per_frame": bytes_frame,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                          "binding": {
