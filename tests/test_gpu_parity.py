@@ -193,3 +193,29 @@ def test_empty_batch(cuda_device):
     h = build_code("eg4")
     res = decode_batch(h, np.zeros((0, 255), np.float32), DecoderConfig(block_len_p=8), "fwbf")
     assert res.iterations.numel() == 0
+
+
+def test_code_too_large_for_shared_memory_fails_cleanly(cuda_device):
+    """Frame state lives in shared memory; a code beyond that fails with a
+    clear error at decode time (no launch, no CPU fallback)."""
+    from paper_1206_3362_b200.codes import ParityCheckMatrix
+    n = 60000
+    rows = [[(3 * r + k) % n for k in (0, 1, 2, 3, 4, 5)] for r in range(n // 2)]
+    h = ParityCheckMatrix([sorted(set(r)) for r in rows], n)
+    y = np.ones((2, n), np.float32)
+    with pytest.raises((nat.FwbfError, ValueError), match="shared memory|fit"):
+        decode_batch(h, y, DecoderConfig(block_len_p=24, k_max=3), "fwbf")
+
+
+def test_single_frame_extremes(cuda_device):
+    """One frame each: all +1 (converged at k = 0), all -1, all exact zeros and
+    alternating signs, on the split, guarded and ordered paths; vs the oracle."""
+    h = build_code("eg5")
+    n = h.n_cols
+    ys = np.stack([np.ones(n), -np.ones(n), np.zeros(n), np.where(np.arange(n) % 2, 1.0, -1.0),
+                   np.full(n, 1e-30), np.linspace(-3, 3, n)]).astype(np.float32)
+    cfg = DecoderConfig(block_len_p=31, k_max=30)
+    exp = _oracle_batch(h, ys, "fwbf", cfg)
+    for ordered in (0, 1, 2):
+        res = decode_batch(h, ys, cfg, "fwbf", flip_log=True, force_ordered=ordered)
+        assert_batch_equal(res, *exp, f"extremes/{ordered}")
