@@ -743,8 +743,10 @@ extern "C" int fwbf_decode_host_f32(fwbf_code *c, const fwbf_params *p, const fl
   if (!c->pipe_counters) CUDA_TRY(cudaMalloc((void **)&c->pipe_counters, FWBF_NCOUNTERS * sizeof(int64_t)));
   CUDA_TRY(cudaMemsetAsync(c->pipe_counters, 0, FWBF_NCOUNTERS * sizeof(long long), c->pipe_s[0]));
   CUDA_TRY(cudaStreamSynchronize(c->pipe_s[0]));
-  const long long nchunks = (batch + chunk - 1) / chunk;
-  for (long long ci = 0; ci < nchunks; ++ci) {
+  // chunk sizes ramp up geometrically (chunk/16, chunk/8, ... chunk) so the
+  // first decode starts after a short copy instead of a full chunk's
+  long long f0 = 0, cur = std::max<long long>(std::min<long long>(chunk, 4096), chunk / 16);
+  for (long long ci = 0; f0 < batch; ++ci) {
     const int s = (int)(ci & 1);
     cudaStream_t st = c->pipe_s[s];
     char *base = (char *)c->pipe_buf[s];
@@ -752,8 +754,7 @@ extern "C" int fwbf_decode_host_f32(fwbf_code *c, const fwbf_params *p, const fl
     uint32_t *dz = (uint32_t *)(base + yb);
     int32_t *dit = (int32_t *)(base + yb + zb);
     uint8_t *dfl = (uint8_t *)(base + yb + zb + ib);
-    const long long f0 = ci * chunk;
-    const long long nb = std::min<long long>(chunk, batch - f0);
+    const long long nb = std::min<long long>(cur, batch - f0);
     CUDA_TRY(cudaMemcpyAsync(dy, y_host + f0 * ld, (size_t)nb * ld * sizeof(float), cudaMemcpyHostToDevice, st));
     fwbf_outputs o{};
     o.z_bits = z_host ? dz : nullptr;
@@ -773,9 +774,8 @@ extern "C" int fwbf_decode_host_f32(fwbf_code *c, const fwbf_params *p, const fl
     }
     if (it_host) CUDA_TRY(cudaMemcpyAsync(it_host + f0, dit, (size_t)nb * 4, cudaMemcpyDeviceToHost, st));
     if (fl_host) CUDA_TRY(cudaMemcpyAsync(fl_host + f0, dfl, (size_t)nb, cudaMemcpyDeviceToHost, st));
-    if (ci == 0 && nchunks > 1) {
-      // stream 1 must not start decoding before the counters are cleared (done above, synced)
-    }
+    f0 += nb;
+    cur = std::min<long long>(chunk, 2 * cur);
   }
   CUDA_TRY(cudaStreamSynchronize(c->pipe_s[0]));
   CUDA_TRY(cudaStreamSynchronize(c->pipe_s[1]));
