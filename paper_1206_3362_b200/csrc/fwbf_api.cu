@@ -21,7 +21,8 @@
 #include "fwbf_internal.h"
 
 namespace fwbf {
-template <typename YT, bool CIRC, int KC, int TB, int WT> __global__ void decode_kernel(const __grid_constant__ KParams P);
+template <typename YT, bool CIRC, int KC, int TB, int WT, bool INC = false>
+__global__ void decode_kernel(const __grid_constant__ KParams P);
 template <typename YT>
 __global__ void noise_kernel(unsigned long long seed, long long first, long long count, double sigma,
                              const uint32_t *codeword, YT *y, long long ld, int n, int pm);
@@ -452,6 +453,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   const void *kern = nullptr;
   int T = 0;
   int kc = 1;
+  int kwt = 0; // compile-time circulant weight of the chosen kernel (0: runtime)
   if (circ) {
     if (sizeof(YT) == 4) {
       struct Shape { int kc, tb, wt; const void *fn; };
@@ -468,16 +470,26 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
       for (int i = 0; i < ntab && want_kc; ++i)
         if (tab[i].kc == want_kc && tab[i].tb == want_tb && tab[i].kc * tab[i].tb >= c->n &&
             (tab[i].wt == 0 || (tab[i].wt == c->w && !generic_only))) {
-          kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc;
+          kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc; kwt = tab[i].wt;
           if (tab[i].wt) break;
         }
       // prefer the smallest shape covering n with the weight compiled in
       for (int i = 0; i < ntab && !kern && !generic_only; ++i)
         if (tab[i].wt == c->w && tab[i].kc * tab[i].tb >= c->n && tab[i].kc * tab[i].tb < 4 * c->n + 256) {
-          kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc;
+          kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc; kwt = tab[i].wt;
         }
       for (int i = 0; i < ntab && !kern; ++i)
-        if (tab[i].wt == 0 && tab[i].kc * tab[i].tb >= c->n) { kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc; break; }
+        if (tab[i].wt == 0 && tab[i].kc * tab[i].tb >= c->n) { kern = tab[i].fn; T = tab[i].tb; kc = tab[i].kc; kwt = tab[i].wt; break; }
+      // IMWBF: the same shape with the incremental integer metric
+      if (kwt && p->algorithm == FWBF_ALG_IMWBF && !metric_out && !getenv("FWBF_NO_INC")) {
+        static const Shape inc[] = {
+#define FWBF_SHAPE_INC(YT_, C_, KC_, TB_, WT_) {KC_, TB_, WT_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, WT_, true>},
+            FWBF_INC_CONFIGS(FWBF_SHAPE_INC)
+#undef FWBF_SHAPE_INC
+        };
+        for (const Shape &sh : inc)
+          if (sh.kc == kc && sh.tb == T && sh.wt == kwt) kern = sh.fn;
+      }
     } else {
       struct Shape { int kc, tb, wt; const void *fn; };
       static const Shape shapes[] = {

@@ -146,7 +146,7 @@ __device__ __forceinline__ YT load_y(const KParams &P, long long f, int n) {
 //   CIRC : circulant H (index arithmetic) vs explicit CSR/CSC tables
 //   KC   : columns per thread on the guarded path (register accumulators)
 // ---------------------------------------------------------------------------
-template <typename YT, bool CIRC, int KC, int TB, int WT>
+template <typename YT, bool CIRC, int KC, int TB, int WT, bool INC>
 __global__ void __launch_bounds__(TB ? TB : 1024, TB == 256 ? FWBF_MINB_256 : 1024 / (TB ? TB : 1024))
 decode_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -627,6 +627,109 @@ decode_kernel(const __grid_constant__ KParams P) {
     int conv = 0, stalled = 0;
     long long logpos = 0;
     long long flips_total = 0;
+    if (INC && split && P.alg == FWBF_ALG_IMWBF) {
+      // IMWBF flips one bit per iteration (decoders.py:170-171), so after one
+      // full split-fp32 pass the metric is kept incrementally: the exact column
+      // sums live as int64 limb pairs in sCorr (units of q), and the W checks
+      // the flip toggles add (s ? +2 : -2) w / q to their W columns -- W^2
+      // integer updates per iteration instead of N*W edge visits.  Integer
+      // arithmetic is exact, so every metric equals the full recomputation.
+      {
+        constexpr int NP = SplitPairs<KC>::value;
+        unsigned long long hi[NP], lo[NP];
+#pragma unroll
+        for (int qp = 0; qp < NP; ++qp) { hi[qp] = 0ull; lo[qp] = 0ull; }
+        const unsigned long long cc = f2pack(cmag, cmag);
+        const uint32_t baseT = (uint32_t)__cvta_generic_to_shared(smem_raw) + 8u * (uint32_t)tid;
+#pragma unroll
+        for (int j = 0; j < (WT > 0 ? WT : 1); ++j)
+          GatherP2<0, NP, TB>::run(hi, lo, baseT + (uint32_t)P.uoff[j], cc);
+#pragma unroll
+        for (int qp = 0; qp < NP; ++qp) {
+          const float2 h = f2unpack(hi[qp]);
+          const float2 l = f2unpack(lo[qp]);
+          const int n = 2 * tid + 2 * T * qp;
+          if (n < N) {
+            int4 *cp = reinterpret_cast<int4 *>(sCorr + 2 * n);
+            const int4 cv = *cp;
+            const long long I0 = (long long)__dmul_rn(__dadd_rn((double)h.x, (double)l.x), qinv) +
+                                 (((long long)cv.y << 24) + cv.x);
+            const long long I1 = (long long)__dmul_rn(__dadd_rn((double)h.y, (double)l.y), qinv) +
+                                 (((long long)cv.w << 24) + cv.z);
+            *cp = make_int4((int)(I0 & 0xffffff), (int)(I0 >> 24), (int)(I1 & 0xffffff), (int)(I1 >> 24));
+          }
+        }
+      }
+      __syncthreads();
+      for (;;) {
+        if (misc[S_SWT] == 0) { conv = 1; break; }
+        if (k >= P.kmax) break;
+        // metric from the limb sums (renormalised) and the global argmax
+        double v = -dinf();
+        int i = 0x7fffffff;
+        for (int n = tid; n < N; n += T) {
+          int2 *cp = reinterpret_cast<int2 *>(sCorr) + n;
+          const int2 cv = *cp;
+          const long long S = ((long long)cv.y << 24) + cv.x;
+          *cp = make_int2((int)(S & 0xffffff), (int)(S >> 24));
+          const double aa = P.has_ay ? sAY[n]
+                                     : __dmul_rn(P.alpha, P.alias_y ? fabs((double)load_y<YT>(P, f, n))
+                                                                    : fabs((double)ybuf[n]));
+          const double e = __dsub_rn(__dmul_rn((double)S, qexp), aa);
+          if (e > v) { v = e; i = n; }
+        }
+        warp_amax(v, i);
+        if (lane == 0) { red_v[warp] = v; red_i[warp] = i; }
+        __syncthreads();
+        if (warp == 0) {
+          v = lane < nwarps ? red_v[lane] : -dinf();
+          i = lane < nwarps ? red_i[lane] : 0x7fffffff;
+          warp_amax(v, i);
+          const int c = i; // flipped unconditionally: IMWBF never stalls
+          if (lane == 0) {
+            zbits[c >> 5] ^= 1u << (c & 31);
+            flips[0] = c;
+            if (P.fliplog) {
+              P.fliplog[f * P.fliplog_stride + logpos] = c;
+              P.fliplog_counts[f * P.kmax + k] = 1;
+            }
+          }
+          int dsw = 0; // syndrome weight change
+          for (int j = lane; j < W; j += 32) {
+            int m = c - offs_s[j];
+            if (m < 0) m += N;
+            const uint32_t old = atomicXor(&sbits[m >> 5], 1u << (m & 31));
+            dsw += ((old >> (m & 31)) & 1u) ? -1 : 1;
+          }
+#pragma unroll
+          for (int off = 16; off; off >>= 1) dsw += __shfl_xor_sync(FULL_MASK, dsw, off);
+          if (lane == 0) misc[S_SWT] += dsw;
+        }
+        __syncthreads();
+        {
+          const int c = flips[0];
+          for (int qq = tid; qq < W * W; qq += T) {
+            const int j = qq / W, jj = qq - j * W;
+            int m = c - offs_s[j];
+            if (m < 0) m += N;
+            int n = m + offs_s[jj];
+            if (n >= N) n -= N;
+            long long A = (long long)__dmul_rn(__dmul_rn((double)fabsf(sFA[m]), 2.0), qinv);
+            if (P.wmode == FWBF_WEIGHTS_IMWBF && n == (int)sA2[m]) {
+              const int2 dl = reinterpret_cast<const int2 *>(sM2)[m];
+              A += ((long long)dl.y << 24) + dl.x; // = 2 (min2 - min1) / q
+            }
+            if (!((sbits[m >> 5] >> (m & 31)) & 1u)) A = -A;
+            atomicAdd(&sCorr[2 * n], (int)(A & 0xffffff));
+            atomicAdd(&sCorr[2 * n + 1], (int)(A >> 24));
+          }
+        }
+        __syncthreads();
+        logpos += 1;
+        flips_total += 1;
+        k += 1;
+      }
+    } else
     for (;;) {
       const int swt = misc[S_SWT];
       if (swt == 0 && !P.metric_out) { conv = 1; break; }
@@ -1206,9 +1309,12 @@ decode_kernel(const __grid_constant__ KParams P) {
 
 // explicit instantiations used by the launcher
 #define FWBF_INST(YT, C, KC, TB, WT) \
-  template __global__ void decode_kernel<YT, C, KC, TB, WT>(const __grid_constant__ KParams);
+  template __global__ void decode_kernel<YT, C, KC, TB, WT, false>(const __grid_constant__ KParams);
+#define FWBF_INST_INC(YT, C, KC, TB, WT) \
+  template __global__ void decode_kernel<YT, C, KC, TB, WT, true>(const __grid_constant__ KParams);
 FWBF_FAST_CONFIGS(FWBF_INST)
 FWBF_F64_CONFIGS(FWBF_INST)
+FWBF_INC_CONFIGS(FWBF_INST_INC)
 FWBF_INST(double, true, 1, 0, 0)
 FWBF_INST(float, false, 1, 0, 0)
 FWBF_INST(double, false, 1, 0, 0)

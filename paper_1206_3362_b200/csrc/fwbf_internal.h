@@ -19,6 +19,12 @@ constexpr int kMaxQcBlocks = 256;  // quasi-cyclic shift table entries in the pa
   X(float, true, 8, 512, 0)     \
   X(float, true, 8, 1024, 0)
 
+// IMWBF (one flip per iteration) with the incremental integer metric
+#define FWBF_INC_CONFIGS(X)     \
+  X(float, true, 2, 128, 16)    \
+  X(float, true, 4, 256, 32)    \
+  X(float, true, 4, 1024, 64)
+
 // float64 input (ordered path only) with the circulant weight compiled in
 #define FWBF_F64_CONFIGS(X)     \
   X(double, true, 2, 128, 16)   \

@@ -88,3 +88,28 @@ def test_fused_pass_matches_unfused(cuda_device, monkeypatch, code, p, stall, dt
     assert np.array_equal(a.iterations.cpu().numpy(), b.iterations.cpu().numpy())
     assert np.array_equal(a.flags.cpu().numpy(), b.flags.cpu().numpy())
     assert a.flip_logs() == b.flip_logs()
+
+
+@pytest.mark.parametrize("code,weight_mode,alpha,ebn0", [
+    ("eg4", "imwbf", 0.2, 3.0), ("eg5", "imwbf", 0.2, 4.0), ("eg5", "mwbf", 0.0, 4.0),
+    ("eg6", "imwbf", 0.3, 4.0)])
+def test_imwbf_incremental_matches_full_recompute(cuda_device, monkeypatch, code, weight_mode, alpha, ebn0):
+    """IMWBF on the split path keeps the metric incrementally (integer limb
+    updates per toggled check); it must give the flip sequence of the full
+    per-iteration recomputation, frame by frame, and the oracle's."""
+    h = build_code(code)
+    sigma = O.ebn0_to_sigma(ebn0, code_rate(code))
+    rng = np.random.default_rng(11)
+    frames = 512 if h.n_cols < 4000 else 128
+    y = (1.0 + sigma * rng.standard_normal((frames, h.n_cols))).astype(np.float32)
+    cfg = DecoderConfig(alpha=alpha, k_max=60, weight_mode=weight_mode)
+    a = decode_batch(h, y, cfg, "imwbf", flip_log=True)
+    monkeypatch.setenv("FWBF_NO_INC", "1")
+    b = decode_batch(h, y, cfg, "imwbf", flip_log=True)
+    assert np.array_equal(a.iterations.cpu().numpy(), b.iterations.cpu().numpy())
+    assert np.array_equal(a.z(), b.z())
+    assert a.flip_logs() == b.flip_logs()
+    z, its, fl, ft = COracle(h).decode_batch(y[:64], algorithm="imwbf", alpha=alpha, k_max=60,
+                                             weight_mode=weight_mode)
+    assert np.array_equal(a.iterations.cpu().numpy()[:64], its)
+    assert np.array_equal(a.z()[:64], z)
