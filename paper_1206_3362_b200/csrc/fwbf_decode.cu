@@ -295,10 +295,10 @@ decode_kernel(const __grid_constant__ KParams P) {
           // W G/2 of rounding) stay below 2^24 G.  Both exact in fp32.
           // C = 1.5 * 2^23 * G keeps t = v + C in [2^23 G, 2^24 G].
           constexpr int kG = (WT > 32) ? 19 : 20;
-          if (fast && WT > 0 && WT <= 64 && (KC % 2) == 0 && e >= -100 && !P.no_split &&
+          if (fast && WT > 0 && WT <= 64 && (KC % 2) == 0 && e >= -100 && e <= 100 && !P.no_split &&
               (double)W * (double)mx <= ldexp(1.0, kG + e)) {
             fast = 2;
-            cmag = ldexpf(1.5f, kG + e);
+            cmag = ldexpf(1.5f, kG + e); // C = 1.5 * 2^23 G, finite for e <= 100
           }
           misc[S_EQ] = e - 23; // quantum q = 2^(e-23)
         }
@@ -403,7 +403,7 @@ decode_kernel(const __grid_constant__ KParams P) {
         r_ac[k] = ac;
         if (ok) wmax = fmaxf(wmax, (float)min1);
       }
-      if (fpath == 1 && !P.no_split && misc[S_EQ] >= -123) { // uniform: fp64-guarded, not yet split
+      if (fpath == 1 && !P.no_split && misc[S_EQ] >= -123 && misc[S_EQ] <= 77) { // uniform: fp64-guarded, not yet split
         for (int off = 16; off; off >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(FULL_MASK, wmax, off));
         if (lane == 0) redf[32 + warp] = wmax; // init1's slots, already consumed
         __syncthreads();
