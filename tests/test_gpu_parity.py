@@ -214,7 +214,9 @@ def test_single_frame_extremes(cuda_device):
     n = h.n_cols
     ys = np.stack([np.ones(n), -np.ones(n), np.zeros(n), np.where(np.arange(n) % 2, 1.0, -1.0),
                    np.full(n, 1e-30), np.linspace(-3, 3, n), np.linspace(-3e35, 2e35, n),
-                   np.where(np.arange(n) % 3, 1e34, -2e33)]).astype(np.float32)
+                   np.where(np.arange(n) % 3, 1e34, -2e33), np.full(n, -1e-40),
+                   np.where(np.arange(n) % 5, 3e-41, -1e30), np.where(np.arange(n) % 2, 1.0, -0.0)
+                   ]).astype(np.float32)
     cfg = DecoderConfig(block_len_p=31, k_max=30)
     exp = _oracle_batch(h, ys, "fwbf", cfg)
     for ordered in (0, 1, 2):
