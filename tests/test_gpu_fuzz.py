@@ -11,7 +11,9 @@ pytestmark = pytest.mark.gpu
 
 
 def random_code(rng):
-    kind = rng.integers(0, 4)
+    kind = rng.integers(0, 5)
+    if kind == 4:  # the compile-time-weight kernels of the configs
+        return eg_ldpc(int(rng.choice([4, 5])))
     if kind == 0:
         return eg_ldpc(int(rng.integers(2, 5)))
     if kind == 1:
@@ -38,14 +40,18 @@ def random_code(rng):
 def random_y(rng, n, frames):
     sigma = float(rng.uniform(0.3, 0.9))
     y = 1.0 + sigma * rng.standard_normal((frames, n))
-    mode = rng.integers(0, 3)
+    mode = rng.integers(0, 5)
     if mode == 1:
         y = np.round(y * 4) / 4  # ties and exact zeros
+    elif mode == 3:  # per-frame power-of-two scale, far from 1 (guard and split boundaries)
+        y = y * (2.0 ** rng.integers(-90, 91, size=(frames, 1)))
+    elif mode == 4:  # heavy tails: a wide spread of exponents inside one frame
+        y = y / np.maximum(rng.random((frames, n)), 1e-6) ** 2
     y = y.astype(np.float32 if rng.integers(0, 2) else np.float64)
     return y
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(120))
 def test_random_parity(cuda_device, seed):
     rng = np.random.default_rng(1000 + seed)
     h = random_code(rng)
