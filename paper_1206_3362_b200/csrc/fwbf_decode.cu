@@ -661,6 +661,10 @@ decode_kernel(const __grid_constant__ KParams P) {
         }
       }
       __syncthreads();
+      // per check: 2 min1 / q as an int64 in the (now free) shifted copy sFB
+      long long *sA1 = reinterpret_cast<long long *>(smem_raw + ((P.off_fb + 7) & ~7));
+      for (int m = tid; m < M; m += T) sA1[m] = (long long)__dmul_rn(__dmul_rn((double)fabsf(sFA[m]), 2.0), qinv);
+      __syncthreads();
       for (;;) {
         if (misc[S_SWT] == 0) { conv = 1; break; }
         if (k >= P.kmax) break;
@@ -714,7 +718,7 @@ decode_kernel(const __grid_constant__ KParams P) {
             if (m < 0) m += N;
             int n = m + offs_s[jj];
             if (n >= N) n -= N;
-            long long A = (long long)__dmul_rn(__dmul_rn((double)fabsf(sFA[m]), 2.0), qinv);
+            long long A = sA1[m];
             if (P.wmode == FWBF_WEIGHTS_IMWBF && n == (int)sA2[m]) {
               const int2 dl = reinterpret_cast<const int2 *>(sM2)[m];
               A += ((long long)dl.y << 24) + dl.x; // = 2 (min2 - min1) / q
