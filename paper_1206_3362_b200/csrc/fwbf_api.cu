@@ -539,11 +539,16 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     const int pp = P.p;
     P.sel_spread = 0;
     if (pp > 1 && (pp & (pp - 1)) == 0) {
+      // power-of-two p: up to 32 threads per block, but all blocks in one round
+      // when the CTA has room (C, p = 64: 16 threads x 64 blocks)
       tpb = std::min(pp, 32);
+      while (tpb > 1 && (long long)P.nblocks * tpb > T) tpb >>= 1;
+      if (tpb < 4) tpb = std::min(pp, 4);
     } else if (pp > 1 && !(pp & 1)) {
       // p = 2^k * odd: groups of 2^k (<= 16) threads on consecutive blocks start
       // at distinct multiples of 2^k modulo 16 banks-of-doubles: conflict free
       tpb = std::min(16, pp & -pp);
+      while (tpb > 1 && (long long)P.nblocks * tpb > T) tpb >>= 1; // one round when possible
     } else if (pp & 1) {
       // largest power of two <= min(16, p) with all blocks in one round and
       // the half-warps of the CTA divisible into groups of tpb
