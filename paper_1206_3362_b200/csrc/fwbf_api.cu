@@ -26,6 +26,9 @@ __global__ void decode_kernel(const __grid_constant__ KParams P);
 template <typename YT>
 __global__ void noise_kernel(unsigned long long seed, long long first, long long count, double sigma,
                              const uint32_t *codeword, YT *y, long long ld, int n, int pm);
+template <typename YT>
+__global__ void noise_kernel_warp(unsigned long long seed, long long first, long long count, double sigma,
+                                  const uint32_t *codeword, YT *y, long long ld, int n);
 }
 
 using fwbf::KParams;
@@ -686,10 +689,16 @@ static int decode_awgn_t(fwbf_code *c, const fwbf_params *p, uint64_t seed, int6
   for (long long s = 0; s < count; s += chunk) {
     const long long nb = std::min(chunk, count - s);
     YT *yb = o.y_out ? (YT *)o.y_out + s * ld : scratch;
-    static const int gmul = getenv("FWBF_NOISE_GRID") ? atoi(getenv("FWBF_NOISE_GRID")) : 32;
-    static const int nthr = getenv("FWBF_NOISE_T") ? atoi(getenv("FWBF_NOISE_T")) : 128;
-    const int grid = (int)std::min<long long>(nb, (long long)c->sm_count * gmul);
-    nk<<<grid, nthr, smem, stream>>>((unsigned long long)seed, first + s, nb, sigma, o.codeword_bits, yb, ld, n, pm);
+    static const bool cta_gen = getenv("FWBF_NOISE_CTA") != nullptr; // the CTA-per-frame generator
+    if (cta_gen) {
+      const int grid = (int)std::min<long long>(nb, (long long)c->sm_count * 32);
+      nk<<<grid, 128, smem, stream>>>((unsigned long long)seed, first + s, nb, sigma, o.codeword_bits, yb, ld, n,
+                                      pm);
+    } else { // one frame per warp, 4 per CTA
+      const int grid = (int)std::min<long long>((nb + 3) / 4, (long long)c->sm_count * 16);
+      fwbf::noise_kernel_warp<YT><<<grid, 128, 0, stream>>>((unsigned long long)seed, first + s, nb, sigma,
+                                                            o.codeword_bits, yb, ld, n);
+    }
     CUDA_TRY(cudaGetLastError());
     fwbf_outputs oc = o;
     if (o.z_bits) oc.z_bits = o.z_bits + s * o.z_ld;

@@ -44,10 +44,11 @@ __device__ __forceinline__ U4 philox4x64_10(unsigned long long c0, unsigned long
 
 struct NoiseStream {
   unsigned long long key0, frame;
-  const unsigned long long *raw; // shared scratch, raw[p] for p < pm
+  const unsigned long long *raw; // shared scratch: raw[p - p0] for p0 <= p < p0 + pm
   int pm;
+  long long p0 = 0;
   __device__ unsigned long long at(long long p) const {
-    if (p < pm) return raw[p];
+    if (p >= p0 && p < p0 + pm) return raw[p - p0];
     const unsigned long long b = (unsigned long long)(p >> 2) + 1ull;
     const U4 o = philox4x64_10(b, 0ull, frame, 0ull, key0, 0ull);
     return o.v[p & 3];
@@ -156,6 +157,74 @@ __device__ void gen_frame(YT *ybuf, int N, unsigned long long seed, unsigned lon
     }
   }
   __syncthreads();
+}
+
+// Warp-level generator: one warp produces one frame with a rolling window of
+// 128 draws in shared memory (each lane computes one Philox block = 4 draws
+// per refill), so every warp of the CTA walks its own frame -- no CTA
+// barriers and 4x the concurrent walkers of gen_frame at the same occupancy.
+template <typename YT>
+__device__ void gen_frame_warp(YT *ybuf, int N, unsigned long long seed, unsigned long long frame,
+                               double sigma, const uint32_t *codeword, unsigned long long *win) {
+  const int lane = threadIdx.x & 31;
+  constexpr int WIN = 128;
+  if (sigma == 0.0) { // awgn_apply returns s unchanged and draws nothing (channel.py:34-35)
+    for (int n = lane; n < N; n += 32) {
+      const int c = codeword ? (int)((__ldg(codeword + (n >> 5)) >> (n & 31)) & 1u) : 0;
+      ybuf[n] = (YT)(c ? -1.0 : 1.0);
+    }
+    return;
+  }
+  NoiseStream s{seed, frame, win, WIN};
+  s.p0 = -WIN; // empty window
+  long long p = 0;
+  int k = 0;
+  while (k < N) {
+    if (p + 32 > s.p0 + WIN) { // refill: the window starts at p's Philox block
+      __syncwarp();
+      s.p0 = p & ~3ll;
+      const U4 o = philox4x64_10((unsigned long long)(s.p0 >> 2) + 1ull + lane, 0ull, frame, 0ull, seed, 0ull);
+      win[4 * lane + 0] = o.v[0];
+      win[4 * lane + 1] = o.v[1];
+      win[4 * lane + 2] = o.v[2];
+      win[4 * lane + 3] = o.v[3];
+      __syncwarp();
+    }
+    unsigned long long r = s.at(p + lane);
+    const int idx = (int)(r & 0xffull);
+    r >>= 8;
+    const bool neg = r & 1ull;
+    const unsigned long long rabs = (r >> 1) & 0x000fffffffffffffull;
+    double x = __dmul_rn((double)rabs, __ldg(&d_zig_w[idx]));
+    if (neg) x = -x;
+    const bool fast = rabs < __ldg(&d_zig_k[idx]);
+    const uint32_t slow = __ballot_sync(0xffffffffu, !fast);
+    const int sl = slow ? __ffs(slow) - 1 : 32;
+    const int nv = min(sl, N - k);
+    if (lane < nv) {
+      const int n = k + lane;
+      const int c = codeword ? (int)((__ldg(codeword + (n >> 5)) >> (n & 31)) & 1u) : 0;
+      ybuf[n] = (YT)__dadd_rn(c ? -1.0 : 1.0, __dmul_rn(sigma, x));
+    }
+    if (sl < 32 && k + sl < N) {
+      long long pos = p + sl + 1;
+      double v = 0.0;
+      if (lane == sl) v = zig_slow(s, pos, idx, rabs, x);
+      v = __shfl_sync(0xffffffffu, v, sl);
+      pos = __shfl_sync(0xffffffffu, pos, sl);
+      if (lane == 0) {
+        const int n = k + sl;
+        const int c = codeword ? (int)((__ldg(codeword + (n >> 5)) >> (n & 31)) & 1u) : 0;
+        ybuf[n] = (YT)__dadd_rn(c ? -1.0 : 1.0, __dmul_rn(sigma, v));
+      }
+      k += sl + 1;
+      p = pos;
+    } else {
+      k += nv;
+      p += nv;
+    }
+  }
+  __syncwarp();
 }
 
 } // namespace fwbf
