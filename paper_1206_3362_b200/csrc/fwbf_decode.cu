@@ -1194,7 +1194,38 @@ decode_kernel(const __grid_constant__ KParams P) {
       // their previous syndrome bits in `sprev`, so only toggled checks are
       // rewritten (negated; both copies on the guarded path).  With T a
       // multiple of 32, check tid + kk*T is bit `lane` of one warp-uniform word.
-      if (TB > 0) {
+      if (TB > 0 && kGuard && split) {
+        // split path: per-thread bases once, then [base + kk*TB] addressing
+        float *pFA = sFA + tid, *pFA2 = sFA + N + tid, *pFB = sFB + 1 + tid, *pFB2 = sFB + N + 1 + tid;
+        const int2 *pM2 = reinterpret_cast<const int2 *>(sM2) + tid;
+        const uint16_t *pA2 = sA2 + tid;
+        const bool imw = P.wmode == FWBF_WEIGHTS_IMWBF;
+        int pc = 0;
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+          if (kk * TB + warp * 32 < M) { // warp-uniform: this warp's word exists
+            const uint32_t word = sbits[(kk * TB + warp * 32) >> 5];
+            const bool s = (word >> lane) & 1u;
+            const bool tog = (tid + kk * TB < M) && (s != (bool)((sprev >> kk) & 1u));
+            if (tog) {
+              const float v1 = -pFA[kk * TB];
+              pFA[kk * TB] = v1;
+              pFA2[kk * TB] = v1;
+              pFB[kk * TB] = v1;
+              pFB2[kk * TB] = v1;
+              if (imw) { // correction sign flips with s_m
+                const int2 dl = pM2[kk * TB];
+                int *cp = sCorr + 2 * (int)pA2[kk * TB];
+                atomicAdd(cp, s ? dl.x : -dl.x);
+                atomicAdd(cp + 1, s ? dl.y : -dl.y);
+              }
+            }
+            sprev ^= (tog ? 1u : 0u) << kk;
+            pc += __popc(word);
+          }
+        }
+        if (lane == 0 && pc) atomicAdd(&misc[S_SWT], pc);
+      } else if (TB > 0) {
         int pc = 0;
 #pragma unroll
         for (int kk = 0; kk < KC; ++kk) {
