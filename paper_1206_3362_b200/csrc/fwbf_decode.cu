@@ -1009,6 +1009,7 @@ decode_kernel(const __grid_constant__ KParams P) {
             if (v > 0.0) {
               if (sub == 0) atomicXor(&zbits[i >> 5], 1u << (i & 31));
               if (CIRC) {
+#pragma unroll 4
                 for (int j = sub; j < W; j += TPB) {
                   int m = i - offs_s[j];
                   if (m < 0) m += N;
