@@ -125,6 +125,50 @@ template <int QP, int NP, int TB> struct GatherP2<QP, NP, TB, false> {
                                              unsigned long long) {}
 };
 
+// Split-path refresh of check m = tid + KK*TB (compile-time KK): shared
+// addresses come in pinned registers (base + KK*TB*size as immediates), so
+// the four sign-negating stores and the correction-limb atomics need no
+// per-check address arithmetic.
+struct RefreshAddr {
+  uint32_t fa, fa2, fb, fb2, m2, a2, corr;
+};
+template <int KK, int KC, int TB, bool GO = (KK < KC)> struct RefreshKK {
+  static __device__ __forceinline__ void run(const RefreshAddr &A, const uint32_t *sbits, uint32_t &sprev,
+                                             int &pc, int tid, int warp, int lane, int M, bool imw) {
+    if (KK * TB + warp * 32 < M) { // warp-uniform: this warp's word exists
+      const uint32_t word = sbits[(KK * TB + warp * 32) >> 5];
+      const bool s = (word >> lane) & 1u;
+      const bool tog = (tid + KK * TB < M) && (s != (bool)((sprev >> KK) & 1u));
+      if (tog) {
+        float v;
+        asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(A.fa), "n"(4 * KK * TB));
+        v = -v;
+        asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(A.fa), "n"(4 * KK * TB), "f"(v));
+        asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(A.fa2), "n"(4 * KK * TB), "f"(v));
+        asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(A.fb), "n"(4 * KK * TB), "f"(v));
+        asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(A.fb2), "n"(4 * KK * TB), "f"(v));
+        if (imw) { // correction sign flips with s_m
+          int dx, dy;
+          unsigned short a2;
+          asm volatile("ld.shared.v2.s32 {%0, %1}, [%2+%3];" : "=r"(dx), "=r"(dy) : "r"(A.m2), "n"(8 * KK * TB));
+          asm volatile("ld.shared.u16 %0, [%1+%2];" : "=h"(a2) : "r"(A.a2), "n"(2 * KK * TB));
+          const uint32_t cp = A.corr + 8u * (uint32_t)a2;
+          if (!s) { dx = -dx; dy = -dy; }
+          asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(cp), "r"(dx));
+          asm volatile("red.shared.add.s32 [%0+4], %1;" ::"r"(cp), "r"(dy));
+        }
+      }
+      sprev ^= (tog ? 1u : 0u) << KK;
+      pc += __popc(word);
+    }
+    RefreshKK<KK + 1, KC, TB>::run(A, sbits, sprev, pc, tid, warp, lane, M, imw);
+  }
+};
+template <int KK, int KC, int TB> struct RefreshKK<KK, KC, TB, false> {
+  static __device__ __forceinline__ void run(const RefreshAddr &, const uint32_t *, uint32_t &, int &, int, int,
+                                             int, int, bool) {}
+};
+
 // Exact argmin corrections as two int32 limbs: D = lo + hi * 2^24 with
 // lo in [0, 2^24) (D an integer multiple of the frame quantum q).
 __device__ __forceinline__ void corr_add(int *corr, int col, long long D, int sign) {
@@ -1196,35 +1240,21 @@ decode_kernel(const __grid_constant__ KParams P) {
       // rewritten (negated; both copies on the guarded path).  With T a
       // multiple of 32, check tid + kk*T is bit `lane` of one warp-uniform word.
       if (TB > 0 && kGuard && split) {
-        // split path: per-thread bases once, then [base + kk*TB] addressing
-        float *pFA = sFA + tid, *pFA2 = sFA + N + tid, *pFB = sFB + 1 + tid, *pFB2 = sFB + N + 1 + tid;
-        const int2 *pM2 = reinterpret_cast<const int2 *>(sM2) + tid;
-        const uint16_t *pA2 = sA2 + tid;
-        const bool imw = P.wmode == FWBF_WEIGHTS_IMWBF;
+        // split path: per-thread shared addresses once, [base + kk*TB] in PTX
+        RefreshAddr A;
+        const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
+        const uint32_t fa = s0 + (uint32_t)P.off_fa + 4u * (uint32_t)tid;
+        const uint32_t fb = s0 + (uint32_t)P.off_fb + 4u * (uint32_t)(tid + 1);
+        asm("mov.b32 %0, %1;" : "=r"(A.fa) : "r"(fa));
+        asm("mov.b32 %0, %1;" : "=r"(A.fa2) : "r"(fa + 4u * (uint32_t)N));
+        asm("mov.b32 %0, %1;" : "=r"(A.fb) : "r"(fb));
+        asm("mov.b32 %0, %1;" : "=r"(A.fb2) : "r"(fb + 4u * (uint32_t)N));
+        asm("mov.b32 %0, %1;" : "=r"(A.m2) : "r"(s0 + (uint32_t)P.off_m2s + 8u * (uint32_t)tid));
+        asm("mov.b32 %0, %1;" : "=r"(A.a2) : "r"(s0 + (uint32_t)P.off_a2m + 2u * (uint32_t)tid));
+        asm("mov.b32 %0, %1;" : "=r"(A.corr) : "r"(s0 + (uint32_t)P.off_corr));
         int pc = 0;
-#pragma unroll
-        for (int kk = 0; kk < KC; ++kk) {
-          if (kk * TB + warp * 32 < M) { // warp-uniform: this warp's word exists
-            const uint32_t word = sbits[(kk * TB + warp * 32) >> 5];
-            const bool s = (word >> lane) & 1u;
-            const bool tog = (tid + kk * TB < M) && (s != (bool)((sprev >> kk) & 1u));
-            if (tog) {
-              const float v1 = -pFA[kk * TB];
-              pFA[kk * TB] = v1;
-              pFA2[kk * TB] = v1;
-              pFB[kk * TB] = v1;
-              pFB2[kk * TB] = v1;
-              if (imw) { // correction sign flips with s_m
-                const int2 dl = pM2[kk * TB];
-                int *cp = sCorr + 2 * (int)pA2[kk * TB];
-                atomicAdd(cp, s ? dl.x : -dl.x);
-                atomicAdd(cp + 1, s ? dl.y : -dl.y);
-              }
-            }
-            sprev ^= (tog ? 1u : 0u) << kk;
-            pc += __popc(word);
-          }
-        }
+        RefreshKK<0, (TB > 0 ? KC : 1), (TB > 0 ? TB : 1)>::run(A, sbits, sprev, pc, tid, warp, lane, M,
+                                                              P.wmode == FWBF_WEIGHTS_IMWBF);
         if (lane == 0 && pc) atomicAdd(&misc[S_SWT], pc);
       } else if (TB > 0) {
         int pc = 0;
