@@ -152,7 +152,9 @@ def device_code(h, device: int = 0) -> DeviceCode:
         try:
             weakref.finalize(h, _CODES.pop, key, None)
         except TypeError:
-            pass
+            # not weak-referenceable: hold h so its id cannot be reused by
+            # another matrix while the cached handle exists
+            dc._owner = h
     return dc
 
 
