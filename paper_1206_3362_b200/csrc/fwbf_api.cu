@@ -78,6 +78,7 @@ struct fwbf_code {
   int64_t *pipe_counters = nullptr;
   void *noise_buf = nullptr;
   size_t noise_bytes = 0;
+  cudaEvent_t noise_evt = nullptr; // last use of noise_buf (device-side ordering across streams)
 };
 
 static constexpr int kWorkRing = 1024;
@@ -252,6 +253,7 @@ extern "C" int fwbf_code_destroy(fwbf_code *c) {
   }
   cudaFree(c->pipe_counters);
   cudaFree(c->noise_buf);
+  if (c->noise_evt) cudaEventDestroy(c->noise_evt);
   delete c;
   return FWBF_OK;
 }
@@ -667,8 +669,14 @@ static int decode_awgn_t(fwbf_code *c, const fwbf_params *p, uint64_t seed, int6
   chunk = std::max<long long>(bf, chunk / bf * bf);
   CUDA_TRY(cudaSetDevice(c->device));
   YT *scratch = nullptr;
+  // The library scratch for y is shared by every call on this handle: calls
+  // are serialised on the host (lock held while enqueueing) and on the device
+  // (each call's stream waits for the previous call's last use of it).
+  std::unique_lock<std::mutex> lock(c->pipe_mu, std::defer_lock);
   if (!o.y_out) {
-    std::lock_guard<std::mutex> lock(c->pipe_mu);
+    lock.lock();
+    if (!c->noise_evt) CUDA_TRY(cudaEventCreateWithFlags(&c->noise_evt, cudaEventDisableTiming));
+    else CUDA_TRY(cudaStreamWaitEvent(stream, c->noise_evt, 0));
     const size_t need = (size_t)chunk * ld * sizeof(YT);
     if (need > c->noise_bytes) {
       if (c->noise_buf) cudaFree(c->noise_buf);
@@ -715,6 +723,7 @@ static int decode_awgn_t(fwbf_code *c, const fwbf_params *p, uint64_t seed, int6
     rc = launch_decode<YT>(c, p, yb, nb, ld, &oc, stream);
     if (rc) return rc;
   }
+  if (!o.y_out) CUDA_TRY(cudaEventRecord(c->noise_evt, stream));
   return FWBF_OK;
 }
 

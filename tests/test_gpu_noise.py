@@ -109,3 +109,24 @@ def test_sigma_zero_noiseless(cuda_device):
     res = decode_awgn(h, DecoderConfig(block_len_p=16), "fwbf", 1, 0, 256, 0.0, return_y=True)
     assert np.all(res.y.cpu().numpy() == 1.0)
     assert np.all(res.iterations.cpu().numpy() == 0)
+
+
+def test_decode_awgn_concurrent_streams_share_scratch(cuda_device):
+    """Two decode_awgn calls on different streams share the handle's y scratch;
+    the library orders them on the device, so both results equal serial runs."""
+    import torch
+    from paper_1206_3362_b200 import DecoderConfig, eg_ldpc
+    from paper_1206_3362_b200.decoders import decode_awgn
+    h = eg_ldpc(5)
+    cfg = DecoderConfig(block_len_p=31, k_max=50)
+    ref_a = decode_awgn(h, cfg, "fwbf", 7, 0, 20000, 0.52)
+    ref_b = decode_awgn(h, cfg, "fwbf", 9, 0, 20000, 0.55)
+    torch.cuda.synchronize()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(sa):
+        ra = decode_awgn(h, cfg, "fwbf", 7, 0, 20000, 0.52)
+    with torch.cuda.stream(sb):
+        rb = decode_awgn(h, cfg, "fwbf", 9, 0, 20000, 0.55)
+    torch.cuda.synchronize()
+    assert torch.equal(ra.iterations, ref_a.iterations) and torch.equal(ra.z_bits, ref_a.z_bits)
+    assert torch.equal(rb.iterations, ref_b.iterations) and torch.equal(rb.z_bits, ref_b.z_bits)
