@@ -287,7 +287,7 @@ decode_kernel(const __grid_constant__ KParams P) {
       const int n = tid + k * T;
       const bool ok = n < N;
       YT v = ok ? load_y<YT>(P, f, n) : YT(0);
-      if (ok) ybuf[n] = v;
+      if (ok) ybuf[n] = v + YT(0); // -0.0 -> +0.0: the sign bit of ybuf is the hard decision (y < 0)
       const uint32_t b = __ballot_sync(FULL_MASK, ok && (v < YT(0)));
       if (lane == 0 && (k * T + warp * 32) < N) zbits[(k * T + warp * 32) >> 5] = b;
       if (ok) {
@@ -391,16 +391,18 @@ decode_kernel(const __grid_constant__ KParams P) {
             // so strict < keeps the lowest column on ties; min2 = second smallest
             // of the multiset (min(min2, max(min1, a)))
             const int *orr = offs_s + 192 + __ldg(P.jwtab + m);
+            uint32_t sgn = 0; // parity = XOR of the sign bits (ybuf holds no -0.0, no NaN here)
             for (int t = 0; t < W; ++t) {
               const int c = m + orr[t];
               const YT yv = ybuf[c];
-              par ^= (yv < YT(0));
+              sgn ^= __float_as_uint((float)yv);
               const YT a = fabs(yv);
               const bool lt = a < min1;
               min2 = fminf(min2, fmaxf(min1, a));
               min1 = fminf(min1, a);
               ac = lt ? c : ac;
             }
+            par = (int)(sgn >> 31);
           } else if (CIRC) {
             for (int j = 0; j < W; ++j) {
               int c = m + P.off[j];
