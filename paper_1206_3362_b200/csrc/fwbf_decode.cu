@@ -1041,11 +1041,12 @@ decode_kernel(const __grid_constant__ KParams P) {
               if (e > v) { v = e; i = base + o; }
             }
           }
-          for (int off = TPB >> 1; off; off >>= 1) {
-            const double v2 = __shfl_xor_sync(FULL_MASK, v, off);
-            const int i2 = __shfl_xor_sync(FULL_MASK, i, off);
-            amax_combine(v, i, v2, i2);
-          }
+          if (__any_sync(FULL_MASK, ok)) // warps without a block skip the butterfly
+            for (int off = TPB >> 1; off; off >>= 1) {
+              const double v2 = __shfl_xor_sync(FULL_MASK, v, off);
+              const int i2 = __shfl_xor_sync(FULL_MASK, i, off);
+              amax_combine(v, i, v2, i2);
+            }
           {
             const uint32_t pm = __ballot_sync(FULL_MASK, ok && sub == 0 && v > 0.0);
             if (lane == 0 && pm) atomicAdd(&misc[S_F], __popc(pm)); // one count per warp
@@ -1057,8 +1058,8 @@ decode_kernel(const __grid_constant__ KParams P) {
               if (CIRC) {
 #pragma unroll 4
                 for (int j = sub; j < W; j += TPB) {
-                  int m = i - offs_s[j];
-                  if (m < 0) m += N;
+                  const int d = i - offs_s[j]; // (i - c_j) mod N as an unsigned min
+                  const int m = (int)min((unsigned)d, (unsigned)(d + N));
                   atomicXor(&sbits[m >> 5], 1u << (m & 31));
                 }
               } else if (P.qc_z) {
