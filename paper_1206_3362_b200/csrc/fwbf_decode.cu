@@ -943,10 +943,36 @@ decode_kernel(const __grid_constant__ KParams P) {
             double v = -dinf();
             int i = 0x7fffffff;
             const int base = b * p, lim = min(p, N - base);
-            for (int o = lane; o < lim; o += 32) {
-              const int n = base + o;
-              const double e = __dsub_rn(col_sum(n), __dmul_rn(P.alpha, fabs((double)ybuf[n])));
-              if (e > v) { v = e; i = n; }
+            const int Zq = P.qc_z;
+            if (Zq && P.qc_jb <= 4 && (base >> qlz) == ((base + lim - 1) >> qlz)) {
+              // QC block inside one block column: its (<= 4) shifts once per block
+              const int cb = base >> qlz, jb = P.qc_jb;
+              int shv[4], rowb[4];
+#pragma unroll
+              for (int r = 0; r < 4; ++r) {
+                shv[r] = (r < jb) ? P.qc_shift[r * P.qc_kb + cb] : -1;
+                rowb[r] = r << qlz;
+              }
+              for (int o = lane; o < lim; o += 32) {
+                const int n = base + o, oz = n & (Zq - 1);
+                double acc = 0.0;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                  if (r < jb) {
+                    const int m = rowb[r] + ((oz - shv[r]) & (Zq - 1));
+                    const double w = ((amin[m] == n) ? chk2 : chk1)[m];
+                    acc = __dadd_rn(acc, shv[r] >= 0 ? w : 0.0); // absent block adds +0.0 (see col_sum)
+                  }
+                }
+                const double e = __dsub_rn(acc, __dmul_rn(P.alpha, fabs((double)ybuf[n])));
+                if (e > v) { v = e; i = n; }
+              }
+            } else {
+              for (int o = lane; o < lim; o += 32) {
+                const int n = base + o;
+                const double e = __dsub_rn(col_sum(n), __dmul_rn(P.alpha, fabs((double)ybuf[n])));
+                if (e > v) { v = e; i = n; }
+              }
             }
             warp_amax(v, i);
             if (lane == 0) { blk_v[b] = v; blk_i[b] = i; }
