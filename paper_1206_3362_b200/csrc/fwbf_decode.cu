@@ -1001,6 +1001,31 @@ decode_kernel(const __grid_constant__ KParams P) {
         } else {
         // y of the next column is fetched one column ahead (from global memory
         // when the metric buffer overlays y) so its latency hides behind a gather
+        if (!CIRC && !P.qc_z && !P.alias_y) {
+          // explicit CSC: two columns per step, their edge chains interleaved
+          // (each column's own sum stays in ascending check order)
+          for (int kk = 0; kk < nKy; kk += 2) {
+            const int n0 = tid + kk * T, n1 = n0 + T;
+            if (n0 >= N) break;
+            const bool two = n1 < N;
+            const int a0 = __ldg(P.col_ptr + n0), d0 = __ldg(P.col_ptr + n0 + 1) - a0;
+            const int a1 = two ? __ldg(P.col_ptr + n1) : 0, d1 = two ? __ldg(P.col_ptr + n1 + 1) - a1 : 0;
+            double acc0 = 0.0, acc1 = 0.0;
+            const int dm = d0 > d1 ? d0 : d1;
+            for (int t = 0; t < dm; ++t) {
+              if (t < d0) {
+                const int m = __ldg(P.col_idx + a0 + t);
+                acc0 = __dadd_rn(acc0, ((amin[m] == n0) ? chk2 : chk1)[m]);
+              }
+              if (t < d1) {
+                const int m = __ldg(P.col_idx + a1 + t);
+                acc1 = __dadd_rn(acc1, ((amin[m] == n1) ? chk2 : chk1)[m]);
+              }
+            }
+            Ebuf[n0] = __dsub_rn(acc0, __dmul_rn(P.alpha, fabs((double)ybuf[n0])));
+            if (two) Ebuf[n1] = __dsub_rn(acc1, __dmul_rn(P.alpha, fabs((double)ybuf[n1])));
+          }
+        } else {
         YT ynext = (tid < N) ? (P.alias_y ? load_y<YT>(P, f, tid) : ybuf[tid]) : YT(0);
         for (int kk = 0; kk < nKy; ++kk) {
           const int n = tid + kk * T;
@@ -1032,6 +1057,7 @@ decode_kernel(const __grid_constant__ KParams P) {
           }
           Ebuf[n] = __dsub_rn(acc, __dmul_rn(P.alpha, fabs((double)ycur)));
         }
+        } // explicit two-column branch
         }
       }
       __syncthreads();
