@@ -953,19 +953,29 @@ decode_kernel(const __grid_constant__ KParams P) {
                 shv[r] = (r < jb) ? P.qc_shift[r * P.qc_kb + cb] : -1;
                 rowb[r] = r << qlz;
               }
-              for (int o = lane; o < lim; o += 32) {
-                const int n = base + o, oz = n & (Zq - 1);
-                double acc = 0.0;
+              // two columns (o, o + 32) per step: independent fp64 chains
+              for (int o = lane; o < lim; o += 64) {
+                const int n0 = base + o, n1 = n0 + 32;
+                const bool two = o + 32 < lim;
+                const int oz0 = n0 & (Zq - 1), oz1 = (two ? n1 : n0) & (Zq - 1);
+                double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
                   if (r < jb) {
-                    const int m = rowb[r] + ((oz - shv[r]) & (Zq - 1));
-                    const double w = ((amin[m] == n) ? chk2 : chk1)[m];
-                    acc = __dadd_rn(acc, shv[r] >= 0 ? w : 0.0); // absent block adds +0.0 (see col_sum)
+                    const int m0 = rowb[r] + ((oz0 - shv[r]) & (Zq - 1));
+                    const int m1 = rowb[r] + ((oz1 - shv[r]) & (Zq - 1));
+                    const double w0 = ((amin[m0] == n0) ? chk2 : chk1)[m0];
+                    const double w1 = ((amin[m1] == n1) ? chk2 : chk1)[m1];
+                    acc0 = __dadd_rn(acc0, shv[r] >= 0 ? w0 : 0.0); // absent block adds +0.0 (see col_sum)
+                    acc1 = __dadd_rn(acc1, shv[r] >= 0 ? w1 : 0.0);
                   }
                 }
-                const double e = __dsub_rn(acc, __dmul_rn(P.alpha, fabs((double)ybuf[n])));
-                if (e > v) { v = e; i = n; }
+                const double e0 = __dsub_rn(acc0, __dmul_rn(P.alpha, fabs((double)ybuf[n0])));
+                if (e0 > v) { v = e0; i = n0; }
+                if (two) {
+                  const double e1 = __dsub_rn(acc1, __dmul_rn(P.alpha, fabs((double)ybuf[n1])));
+                  if (e1 > v) { v = e1; i = n1; }
+                }
               }
             } else {
               for (int o = lane; o < lim; o += 32) {
