@@ -113,3 +113,18 @@ def test_imwbf_incremental_matches_full_recompute(cuda_device, monkeypatch, code
                                              weight_mode=weight_mode)
     assert np.array_equal(a.iterations.cpu().numpy()[:64], its)
     assert np.array_equal(a.z()[:64], z)
+
+
+def test_deterministic_across_runs(cuda_device):
+    """Frames are claimed from an atomic queue in a different order every run;
+    the per-frame results and the counters must not depend on it."""
+    import torch
+    h = build_code("eg5")
+    sigma = O.ebn0_to_sigma(3.5, code_rate("eg5"))
+    g = torch.Generator(device="cuda").manual_seed(123)
+    y = (1.0 + sigma * torch.randn((1 << 17, h.n_cols), generator=g, device="cuda")).float()
+    cfg = DecoderConfig(block_len_p=31, k_max=100)
+    a = decode_batch(h, y, cfg, "fwbf")
+    b = decode_batch(h, y, cfg, "fwbf")
+    for name in ("z_bits", "iterations", "flags", "flips_total", "counters"):
+        assert torch.equal(getattr(a, name), getattr(b, name)), name
