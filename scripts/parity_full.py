@@ -1,0 +1,58 @@
+"""Full-size parity of the headline workload: the bench's 2^20 frames (same
+seeded generator as bench.py) decoded on the GPU and by the C oracle
+(oracle/wbf_oracle.c, pinned to the reference's fixtures) on all host cores;
+hard decisions, iterations, flags and flip counts compared frame by frame.
+Verification script (test infrastructure), not part of the product path.
+
+    python scripts/parity_full.py [--frames 1048576] [--ebn0 4.0] > parity.json
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from oracle.c_oracle import COracle
+from paper_1206_3362_b200 import DecoderConfig, decode_batch
+from tests.golden.codebook import build_code, code_rate
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--frames", type=int, default=1 << 20)
+ap.add_argument("--ebn0", type=float, default=4.0)
+ap.add_argument("--p", type=int, default=31)
+ap.add_argument("--seed", type=int, default=1)
+a = ap.parse_args()
+
+h = build_code("eg5")
+n = h.n_cols
+sigma = float(math.sqrt(1.0 / (2.0 * code_rate("eg5") * 10.0 ** (a.ebn0 / 10.0))))
+dev = torch.device("cuda", 0)
+g = torch.Generator(device=dev).manual_seed(a.seed * 1000003)   # bench.py, rank 0
+ld = (n + 3) // 4 * 4
+y = torch.empty((a.frames, ld), dtype=torch.float32, device=dev)
+for s in range(0, a.frames, 1 << 16):
+    y[s:min(a.frames, s + (1 << 16))].normal_(generator=g).mul_(sigma).add_(1.0)
+y = y[:, :n].contiguous()
+cfg = DecoderConfig(alpha=0.2, k_max=100, block_len_p=a.p)
+t0 = time.time()
+res = decode_batch(h, y, cfg, "fwbf")
+torch.cuda.synchronize()
+tg = time.time() - t0
+gz, git = res.z(), res.iterations.cpu().numpy()
+gfl, gft = res.flags.cpu().numpy() & 3, res.flips_total.cpu().numpy()
+yh = y.cpu().numpy()
+del y
+t0 = time.time()
+z, its, fl, ft = COracle(h).decode_batch(yh, threads=os.cpu_count(), algorithm="fwbf", alpha=0.2,
+                                         k_max=100, p=a.p)
+tc = time.time() - t0
+bad = np.nonzero((git != its) | (gfl != fl) | (gft != ft) | np.any(gz != z, axis=1))[0]
+print(json.dumps({"frames": a.frames, "ebn0_db": a.ebn0, "p": a.p, "mismatched_frames": int(bad.size),
+                  "first_mismatches": bad[:10].tolist(), "mean_iters": float(git.mean()),
+                  "fer": float(np.mean(np.any(gz != 0, axis=1))), "gpu_s": tg, "c_oracle_s": tc,
+                  "c_oracle_threads": os.cpu_count()}))
