@@ -26,11 +26,13 @@ ap.add_argument("--frames", type=int, default=1 << 20)
 ap.add_argument("--ebn0", type=float, default=4.0)
 ap.add_argument("--p", type=int, default=31)
 ap.add_argument("--seed", type=int, default=1)
+ap.add_argument("--code", default="eg5")
+ap.add_argument("--kmax", type=int, default=100)
 a = ap.parse_args()
 
-h = build_code("eg5")
+h = build_code(a.code)
 n = h.n_cols
-sigma = float(math.sqrt(1.0 / (2.0 * code_rate("eg5") * 10.0 ** (a.ebn0 / 10.0))))
+sigma = float(math.sqrt(1.0 / (2.0 * code_rate(a.code) * 10.0 ** (a.ebn0 / 10.0))))
 dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(a.seed * 1000003)   # bench.py, rank 0
 ld = (n + 3) // 4 * 4
@@ -38,7 +40,7 @@ y = torch.empty((a.frames, ld), dtype=torch.float32, device=dev)
 for s in range(0, a.frames, 1 << 16):
     y[s:min(a.frames, s + (1 << 16))].normal_(generator=g).mul_(sigma).add_(1.0)
 y = y[:, :n].contiguous()
-cfg = DecoderConfig(alpha=0.2, k_max=100, block_len_p=a.p)
+cfg = DecoderConfig(alpha=0.2, k_max=a.kmax, block_len_p=a.p)
 t0 = time.time()
 res = decode_batch(h, y, cfg, "fwbf")
 torch.cuda.synchronize()
@@ -49,10 +51,10 @@ yh = y.cpu().numpy()
 del y
 t0 = time.time()
 z, its, fl, ft = COracle(h).decode_batch(yh, threads=os.cpu_count(), algorithm="fwbf", alpha=0.2,
-                                         k_max=100, p=a.p)
+                                         k_max=a.kmax, p=a.p)
 tc = time.time() - t0
 bad = np.nonzero((git != its) | (gfl != fl) | (gft != ft) | np.any(gz != z, axis=1))[0]
-print(json.dumps({"frames": a.frames, "ebn0_db": a.ebn0, "p": a.p, "mismatched_frames": int(bad.size),
+print(json.dumps({"code": a.code, "k_max": a.kmax, "frames": a.frames, "ebn0_db": a.ebn0, "p": a.p, "mismatched_frames": int(bad.size),
                   "first_mismatches": bad[:10].tolist(), "mean_iters": float(git.mean()),
                   "fer": float(np.mean(np.any(gz != 0, axis=1))), "gpu_s": tg, "c_oracle_s": tc,
                   "c_oracle_threads": os.cpu_count()}))
