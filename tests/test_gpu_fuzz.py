@@ -1,6 +1,8 @@
 """Randomised parity: random small codes (regular, irregular, circulant), random
 decoder knobs, random inputs (including ties and zeros) -- CUDA vs oracle, bit-exact."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -51,7 +53,7 @@ def random_y(rng, n, frames):
     return y
 
 
-@pytest.mark.parametrize("seed", range(120))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("FWBF_FUZZ_N", "120"))))
 def test_random_parity(cuda_device, seed):
     rng = np.random.default_rng(1000 + seed)
     h = random_code(rng)
