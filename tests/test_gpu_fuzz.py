@@ -17,8 +17,8 @@ def random_code(rng):
     if kind == 4:  # the compile-time-weight kernels of the configs
         return eg_ldpc(int(rng.choice([4, 5])))
     if kind == 5:  # random circulant with a compiled-in weight (16 or 32) and an arbitrary n
-        w = int(rng.choice([16, 32]))
-        n = int(rng.integers(w + 8, 256 if w == 16 else 1024))
+        w = int(rng.choice([16, 32, 64]))
+        n = int(rng.integers(w + 8, {16: 256, 32: 1024, 64: 4096}[w]))
         first = np.sort(rng.choice(n, size=w, replace=False))
         return ParityCheckMatrix([(first + i) % n for i in range(n)], n)
     if kind == 0:
