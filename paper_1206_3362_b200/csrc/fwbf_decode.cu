@@ -11,16 +11,20 @@
 //   metric      :148-153  E_n = fl(sum_{m in M(n), ascending} (2s_m-1) w_nm) - fl(alpha|y_n|)
 //   selection   :156-183  block argmax (+ threshold), global argmax, top-lambda
 //
-// Two metric paths, selected per frame:
-//   * ORDERED: the column sum in ascending check order with fp64 adds, exactly
+// Three metric paths, selected per frame:
+//   0 ORDERED: the column sum in ascending check order with fp64 adds, exactly
 //     the reference's np.bincount sequence.  Bit-exact for any input.
-//   * GUARDED (float32 y, circulant H): sum_j sgn*min1[n - c_j] over doubled
-//     shared arrays plus an argmin correction.  Order-free and bit-exact when
-//     every partial sum is representable: all weights are float32 values, i.e.
-//     multiples of q = 2^(e_min - 23); partial sums are bounded by 2*dv*max|y|;
-//     so if 2*dv*max|y| < 2^53 q every fp64 add is exact and the result equals
-//     the reference's sum regardless of order.  Frames failing the guard take
-//     the ordered path (flagged FWBF_FLAG_ORDERED).
+//   1 GUARDED fp64 (float32 y, circulant H): order-free sum over doubled
+//     shared arrays.  All weights are float32 values, i.e. multiples of
+//     q = 2^(e_min - 23); if 2*dv*max|y| < 2^53 q every fp64 add is exact, so
+//     the result equals the reference's sum regardless of order.
+//   2 SPLIT fp32 (compile-time weight): each weight v = h + l on the grid
+//     G = 2^g q, h and l summed exactly in packed fp32 (FADD2); argmin
+//     min2 - min1 corrections as exact int32 limb pairs.
+// Frames failing a guard fall to the next path (flags record which).
+// Other passes: the fused metric + block argmax for explicit/QC codes with
+// 32 | p (no metric buffer) and, in the INC kernels, IMWBF's incremental
+// integer metric.
 //
 // Ties: every argmax takes the lowest index (numpy argmax / stable argsort).
 
