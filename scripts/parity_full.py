@@ -28,6 +28,10 @@ ap.add_argument("--p", type=int, default=31)
 ap.add_argument("--seed", type=int, default=1)
 ap.add_argument("--code", default="eg5")
 ap.add_argument("--kmax", type=int, default=100)
+ap.add_argument("--alg", default="fwbf")
+ap.add_argument("--lam", type=int, default=1)
+ap.add_argument("--weight-mode", default="imwbf")
+ap.add_argument("--alpha", type=float, default=0.2)
 a = ap.parse_args()
 
 h = build_code(a.code)
@@ -40,9 +44,9 @@ y = torch.empty((a.frames, ld), dtype=torch.float32, device=dev)
 for s in range(0, a.frames, 1 << 16):
     y[s:min(a.frames, s + (1 << 16))].normal_(generator=g).mul_(sigma).add_(1.0)
 y = y[:, :n].contiguous()
-cfg = DecoderConfig(alpha=0.2, k_max=a.kmax, block_len_p=a.p)
+cfg = DecoderConfig(alpha=a.alpha, k_max=a.kmax, block_len_p=a.p, lam=a.lam, weight_mode=a.weight_mode)
 t0 = time.time()
-res = decode_batch(h, y, cfg, "fwbf")
+res = decode_batch(h, y, cfg, a.alg)
 torch.cuda.synchronize()
 tg = time.time() - t0
 gz, git = res.z(), res.iterations.cpu().numpy()
@@ -50,11 +54,11 @@ gfl, gft = res.flags.cpu().numpy() & 3, res.flips_total.cpu().numpy()
 yh = y.cpu().numpy()
 del y
 t0 = time.time()
-z, its, fl, ft = COracle(h).decode_batch(yh, threads=os.cpu_count(), algorithm="fwbf", alpha=0.2,
-                                         k_max=a.kmax, p=a.p)
+z, its, fl, ft = COracle(h).decode_batch(yh, threads=os.cpu_count(), algorithm=a.alg, alpha=a.alpha,
+                                         k_max=a.kmax, p=a.p, lam=a.lam, weight_mode=a.weight_mode)
 tc = time.time() - t0
 bad = np.nonzero((git != its) | (gfl != fl) | (gft != ft) | np.any(gz != z, axis=1))[0]
-print(json.dumps({"code": a.code, "k_max": a.kmax, "frames": a.frames, "ebn0_db": a.ebn0, "p": a.p, "mismatched_frames": int(bad.size),
+print(json.dumps({"code": a.code, "algorithm": a.alg, "lam": a.lam, "weight_mode": a.weight_mode, "alpha": a.alpha, "k_max": a.kmax, "frames": a.frames, "ebn0_db": a.ebn0, "p": a.p, "mismatched_frames": int(bad.size),
                   "first_mismatches": bad[:10].tolist(), "mean_iters": float(git.mean()),
                   "fer": float(np.mean(np.any(gz != 0, axis=1))), "gpu_s": tg, "c_oracle_s": tc,
                   "c_oracle_threads": os.cpu_count()}))
