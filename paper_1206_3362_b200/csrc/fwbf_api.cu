@@ -81,6 +81,9 @@ struct fwbf_code {
   cudaEvent_t noise_evt = nullptr; // last use of noise_buf (device-side ordering across streams)
 };
 
+// Each decode launch takes the next of kWorkRing frame-queue counters of its
+// code handle (reset on the launch's stream), so up to kWorkRing launches per
+// handle may be in flight concurrently on different streams.
 static constexpr int kWorkRing = 1024;
 
 extern "C" int fwbf_abi_version(void) { return FWBF_ABI_VERSION; }
