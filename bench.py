@@ -319,9 +319,10 @@ def main():
         # ncu DRAM bytes of one decode launch (profiles/roofline_traffic.json,
         # captured on a smaller launch of the same workload) scaled per frame
         # to this run's launch of B frames, like `achieved`
-        traffic, traffic_src = None, None
+        traffic, traffic_src, trf = None, None, {}
         try:
             tr = json.load(open(os.path.join(REPO, "profiles", "roofline_traffic.json"))).get(a.code, {})
+            trf = tr
             if tr.get("dram_bytes_per_frame"):
                 traffic = tr["dram_bytes_per_frame"] * B
                 traffic_src = (f"{tr.get('source')}: {tr['dram_bytes_per_frame']:.0f} B/frame measured on a "
@@ -359,6 +360,10 @@ def main():
                              "smem_bytes_per_s_at_4B_per_edge": 4 * ev_rate,
                              "smem_peak_GBps": smem_peak / 1e9,
                              "dadd_peak_per_s": dadd_peak,
+                             "frac_of_fp64_lane_peak": ev_rate / dadd_peak,
+                             "ncu_issue_active_pct": trf.get("ncu_issue_active_pct"),
+                             "ncu_smem_pipe_pct": trf.get("ncu_smem_pipe_pct"),
+                             "ncu_source": trf.get("ncu_source"),
                              "clock_mhz_for_peaks": max_mhz}},
             "e2e": e2e,
             "gpu_launches": a.steps * 1,

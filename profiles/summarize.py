@@ -61,6 +61,10 @@ with open(os.path.join(HERE, f"{tag}_ncu_summary.md"), "w") as f:
 tp = os.path.join(HERE, "roofline_traffic.json")
 d = json.load(open(tp)) if os.path.exists(tp) else {}
 d["eg5"] = {"dram_bytes_per_launch": traffic, "frames_per_launch": frames,
-            "dram_bytes_per_frame": traffic / frames, "source": f"profiles/{tag}_launches.csv"}
+            "dram_bytes_per_frame": traffic / frames, "source": f"profiles/{tag}_launches.csv",
+            "ncu_issue_active_pct": float(m.get("smsp__issue_active.avg.pct_of_peak_sustained_active", 0) or 0),
+            "ncu_smem_pipe_pct": float(m.get(
+                "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", 0) or 0),
+            "ncu_source": f"profiles/{tag}_ncu_summary.md"}
 json.dump(d, open(tp, "w"), indent=1)
 print(open(os.path.join(HERE, f"{tag}_ncu_summary.md")).read())
