@@ -96,7 +96,8 @@ typedef struct {
   int32_t block_len_p;   /* >= 1 (FWBF) */
   int32_t stall;         /* FWBF_STALL_* */
   int32_t mlp_threshold; /* 0/1 */
-  int32_t force_ordered; /* testing: 1 = ordered path only, 2 = no split-fp32 path */
+  int32_t force_ordered; /* testing, bit flags: 1 = ordered path only, 2 = no split-fp32 path,
+                            4 = no filtered metric (exact split gather every iteration) */
 } fwbf_params;
 
 /* Output buffers (device memory, caller-owned, all optional). */
@@ -149,6 +150,12 @@ int fwbf_metric_f32(fwbf_code *code, const fwbf_params *params, const float *y, 
                     int64_t ld, double *metric, int64_t metric_ld, uint8_t *flags, void *stream);
 int fwbf_metric_f64(fwbf_code *code, const fwbf_params *params, const double *y, int64_t batch,
                     int64_t ld, double *metric, int64_t metric_ld, uint8_t *flags, void *stream);
+
+/* Diagnostic: how many FWBF decisions of the filtered metric (approximate fp32
+ * gather on split-path frames) this code's launches had
+ * to resolve with exact column sums: out[0] block argmaxes, out[1] stall
+ * global argmaxes.  Synchronous; reset != 0 zeroes the counters. */
+int fwbf_filter_stats(fwbf_code *code, int64_t *out, int32_t reset);
 
 /* Noise modes for fwbf_decode_awgn. */
 #define FWBF_NOISE_NUMPY_F64 0 /* the reference stream: numpy Philox(key=seed,

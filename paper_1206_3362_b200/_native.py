@@ -27,7 +27,7 @@ NOISE_NUMPY_F64, NOISE_NUMPY_F32 = 0, 1
 EXPORTS = ("fwbf_abi_version", "fwbf_last_error", "fwbf_device_count", "fwbf_code_create",
            "fwbf_code_destroy", "fwbf_code_info", "fwbf_max_flips_per_iter", "fwbf_decode_f32",
            "fwbf_decode_f64", "fwbf_decode_awgn", "fwbf_decode_host_f32", "fwbf_metric_f32",
-           "fwbf_metric_f64")
+           "fwbf_metric_f64", "fwbf_filter_stats")
 
 
 class CodeDesc(C.Structure):
@@ -91,6 +91,7 @@ def lib() -> C.CDLL:
             L.fwbf_metric_f32.argtypes = [vp, C.POINTER(Params), vp, C.c_int64, C.c_int64, vp, C.c_int64,
                                           vp, vp]
             L.fwbf_metric_f64.argtypes = L.fwbf_metric_f32.argtypes
+            L.fwbf_filter_stats.argtypes = [vp, C.POINTER(C.c_int64), C.c_int32]
             for f in EXPORTS:
                 if f not in ("fwbf_abi_version", "fwbf_last_error", "fwbf_device_count",
                              "fwbf_max_flips_per_iter"):

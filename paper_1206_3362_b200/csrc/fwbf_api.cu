@@ -21,7 +21,7 @@
 #include "fwbf_internal.h"
 
 namespace fwbf {
-template <typename YT, bool CIRC, int KC, int TB, int WT, bool INC = false>
+template <typename YT, bool CIRC, int KC, int TB, int WT, int MODE = 0>
 __global__ void decode_kernel(const __grid_constant__ KParams P);
 template <typename YT>
 __global__ void noise_kernel(unsigned long long seed, long long first, long long count, double sigma,
@@ -65,6 +65,7 @@ struct fwbf_code {
   uint8_t *d_jwtab = nullptr;
   int16_t *d_offpos = nullptr;
   unsigned int *d_work = nullptr; // ring of per-launch work counters
+  unsigned long long *d_fstats = nullptr; // [2] filtered-metric decisions resolved exactly (diagnostic)
   std::atomic<unsigned> work_slot{0};
   int qc_z = 0, qc_jb = 0, qc_kb = 0;
   short qc_shift[fwbf::kMaxQcBlocks];
@@ -233,6 +234,9 @@ extern "C" int fwbf_code_create(const fwbf_code_desc *desc, int device, fwbf_cod
   }
   ce = cudaMalloc((void **)&c->d_work, kWorkRing * sizeof(unsigned));
   if (ce != cudaSuccess) { fwbf_code_destroy(c); return fail(FWBF_ECUDA, "cudaMalloc: %s", cudaGetErrorString(ce)); }
+  ce = cudaMalloc((void **)&c->d_fstats, 2 * sizeof(unsigned long long));
+  if (ce == cudaSuccess) ce = cudaMemset(c->d_fstats, 0, 2 * sizeof(unsigned long long));
+  if (ce != cudaSuccess) { fwbf_code_destroy(c); return fail(FWBF_ECUDA, "cudaMalloc: %s", cudaGetErrorString(ce)); }
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   cudaDeviceGetAttribute(&c->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   *out = c;
@@ -250,6 +254,7 @@ extern "C" int fwbf_code_destroy(fwbf_code *c) {
   cudaFree(c->d_jwtab);
   cudaFree(c->d_offpos);
   cudaFree(c->d_work);
+  cudaFree(c->d_fstats);
   for (int i = 0; i < 2; ++i) {
     if (c->pipe_s[i]) cudaStreamDestroy(c->pipe_s[i]);
     if (c->pipe_buf[i]) cudaFree(c->pipe_buf[i]);
@@ -435,6 +440,10 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   P.force_ordered = (p->force_ordered & 1) ? 1 : 0;
   P.no_split = (p->force_ordered & 2) || getenv("FWBF_NO_SPLIT") ? 1 : 0;
   P.alpha = p->alpha;
+  // FWBF: approximate fp32 gather on split-path frames, close decisions
+  // resolved exactly (kernel: GatherF2 / exact_split_metric); same results
+  P.filter = p->algorithm == FWBF_ALG_FWBF && !metric_out && !(p->force_ordered & 4) && !getenv("FWBF_NO_FILTER");
+  P.filter_stats = c->d_fstats;
   P.nblocks = p->algorithm == FWBF_ALG_FWBF ? (c->n + p->block_len_p - 1) / p->block_len_p : 1;
   P.y = y;
   P.ld = ld;
@@ -491,11 +500,21 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
       // IMWBF: the same shape with the incremental integer metric
       if (kwt && p->algorithm == FWBF_ALG_IMWBF && !metric_out && !getenv("FWBF_NO_INC")) {
         static const Shape inc[] = {
-#define FWBF_SHAPE_INC(YT_, C_, KC_, TB_, WT_) {KC_, TB_, WT_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, WT_, true>},
+#define FWBF_SHAPE_INC(YT_, C_, KC_, TB_, WT_) {KC_, TB_, WT_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, WT_, 1>},
             FWBF_INC_CONFIGS(FWBF_SHAPE_INC)
 #undef FWBF_SHAPE_INC
         };
         for (const Shape &sh : inc)
+          if (sh.kc == kc && sh.tb == T && sh.wt == kwt) kern = sh.fn;
+      }
+      // FWBF: the same shape with the filtered metric (P.filter)
+      if (kwt && P.filter) {
+        static const Shape filt[] = {
+#define FWBF_SHAPE_FILT(YT_, C_, KC_, TB_, WT_) {KC_, TB_, WT_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, WT_, 2>},
+            FWBF_INC_CONFIGS(FWBF_SHAPE_FILT)
+#undef FWBF_SHAPE_FILT
+        };
+        for (const Shape &sh : filt)
           if (sh.kc == kc && sh.tb == T && sh.wt == kwt) kern = sh.fn;
       }
     } else {
@@ -619,6 +638,17 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     for (int i = 0; i < 6; ++i) fprintf(stderr, " %s %.1f%%", names[i], tot ? 100.0 * h[i] / tot : 0.0);
     fprintf(stderr, "\n");
   }
+  return FWBF_OK;
+}
+
+extern "C" int fwbf_filter_stats(fwbf_code *c, int64_t *out, int32_t reset) {
+  if (!c || !out) return fail(FWBF_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  unsigned long long h[2];
+  CUDA_TRY(cudaMemcpy(h, c->d_fstats, sizeof h, cudaMemcpyDeviceToHost));
+  out[0] = (int64_t)h[0];
+  out[1] = (int64_t)h[1];
+  if (reset) CUDA_TRY(cudaMemset(c->d_fstats, 0, sizeof h));
   return FWBF_OK;
 }
 

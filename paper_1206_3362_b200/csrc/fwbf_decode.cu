@@ -129,6 +129,22 @@ template <int QP, int NP, int TB> struct GatherP2<QP, NP, TB, false> {
                                              unsigned long long) {}
 };
 
+// Filtered (approximate) gather step: the same 8-byte load, summed directly in
+// fp32x2 -- one FADD2 per column pair instead of five.  The result is within
+// a per-frame bound delta of the exact sum; selection resolves every decision
+// the bound leaves open with the exact column sum (exact_split_metric).
+template <int QP, int NP, int TB, bool GO = (QP < NP)> struct GatherF2 {
+  static __device__ __forceinline__ void run(unsigned long long (&s)[NP], uint32_t a) {
+    unsigned long long v;
+    asm volatile("ld.shared.b64 %0, [%1+%2];" : "=l"(v) : "r"(a), "n"(QP * TB * 8));
+    s[QP] = fadd2(s[QP], v);
+    GatherF2<QP + 1, NP, TB>::run(s, a);
+  }
+};
+template <int QP, int NP, int TB> struct GatherF2<QP, NP, TB, false> {
+  static __device__ __forceinline__ void run(unsigned long long (&)[NP], uint32_t) {}
+};
+
 // Split-path refresh of check m = tid + KK*TB (compile-time KK): shared
 // addresses come in pinned registers (base + KK*TB*size as immediates), so
 // the four sign-negating stores and the correction-limb atomics need no
@@ -188,16 +204,37 @@ __device__ __forceinline__ YT load_y(const KParams &P, long long f, int n) {
   return __ldg(y + f * P.ld + n);
 }
 
+// Exact Eq.(1) metric of one column on the split path (the filter's fallback).
+// Every signed min1 is a float32 multiple of q and the path guard keeps all
+// partial sums of W of them below 2^53 q, so this fp64 sum is exact in any
+// order; adding the exact argmin correction and subtracting fl(alpha|y_n|)
+// reproduces the exact pass (and the reference) bit for bit.
+template <typename YT>
+__device__ __forceinline__ double exact_split_metric(const KParams &P, const float *sFA, const int *sCorr,
+                                                  const double *sAY, const YT *ybuf, long long f, int n, int W,
+                                                  double qexp) {
+  const int N = P.n;
+  double acc = 0.0;
+  for (int j = 0; j < W; ++j) acc = __dadd_rn(acc, (double)sFA[n + N - P.off[j]]);
+  const int2 cv = reinterpret_cast<const int2 *>(sCorr)[n];
+  if (cv.x | cv.y) acc = __dadd_rn(acc, __dmul_rn((double)(((long long)cv.y << 24) + cv.x), qexp));
+  const double aa = P.has_ay ? sAY[n]
+                             : __dmul_rn(P.alpha, P.alias_y ? fabs((double)load_y<YT>(P, f, n)) : fabs((double)ybuf[n]));
+  return __dsub_rn(acc, aa);
+}
+
 // ---------------------------------------------------------------------------
 // The decode kernel.
 //   YT   : float (float32 channel output) or double
 //   CIRC : circulant H (index arithmetic) vs explicit CSR/CSC tables
 //   KC   : columns per thread on the guarded path (register accumulators)
 // ---------------------------------------------------------------------------
-template <typename YT, bool CIRC, int KC, int TB, int WT, bool INC>
+template <typename YT, bool CIRC, int KC, int TB, int WT, int MODE>
 __global__ void __launch_bounds__(TB ? TB : 1024, TB == 256 ? FWBF_MINB_256 : 1024 / (TB ? TB : 1024))
 decode_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr bool INC = MODE == 1;  // IMWBF incremental integer metric
+  constexpr bool FILT = MODE == 2; // FWBF filtered metric on split-path frames
   const int tid = threadIdx.x;
   const int T = TB ? TB : (int)blockDim.x;  // compile-time on the guarded path
   const int lane = tid & 31;
@@ -223,7 +260,7 @@ decode_kernel(const __grid_constant__ KParams P) {
   int *misc = reinterpret_cast<int *>(smem_raw + P.off_misc);
   float *redf = reinterpret_cast<float *>(smem_raw + P.off_misc + 16 * 4);
   // misc slots
-  enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR, S_EQ, S_FB };
+  enum { S_FRAME = 0, S_F, S_SWT, S_GBEST, S_FAST, S_NONFIN, S_BITERR, S_EQ, S_FB, S_VMAX, S_YMAX };
   // fused metric + block argmax (explicit/QC codes, FWBF, p % 32 == 0): no
   // metric buffer; the flip counter alternates between S_F and S_FB by
   // iteration parity because flips are counted during the metric pass
@@ -353,6 +390,8 @@ decode_kernel(const __grid_constant__ KParams P) {
       }
       redf[0] = cmag;
       misc[S_FAST] = fast;
+      misc[S_VMAX] = 0;                  // largest check minimum (filter bound), see init 2
+      misc[S_YMAX] = __float_as_int(mx); // max |y| (float bits; nonnegative, so int order = float order)
     }
     __syncthreads();
     int fpath = misc[S_FAST];
@@ -452,6 +491,10 @@ decode_kernel(const __grid_constant__ KParams P) {
         r_min2[k] = min2;
         r_ac[k] = ac;
         if (ok) wmax = fmaxf(wmax, (float)min1);
+      }
+      if (FILT && fpath != 0) { // CTA max of the check minima: the filter's error bound
+        for (int off = 16; off; off >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(FULL_MASK, wmax, off));
+        if (lane == 0) atomicMax(&misc[S_VMAX], __float_as_int(wmax));
       }
       if (fpath == 1 && !P.no_split && misc[S_EQ] >= -123 && misc[S_EQ] <= 77) { // uniform: fp64-guarded, not yet split
         for (int off = 16; off; off >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(FULL_MASK, wmax, off));
@@ -654,6 +697,26 @@ decode_kernel(const __grid_constant__ KParams P) {
     }
     __syncthreads();
     FWBF_PH(2)
+    // Filtered metric (FWBF on the split path): the gather sums the signed
+    // min1 values directly in fp32.  Each of a column's W sequential
+    // round-to-nearest adds errs by at most u = 2^-24 of its partial sum
+    // (<= k vmax after k terms), so |approx - exact| <= u vmax W(W+1)/2; the
+    // fp64 finalize and the float store of the filtered metric add
+    // at most 2^-23 (W + alpha) max|y| (|E_n| <= (W + alpha) max|y|).  fdelta
+    // bounds both, for every column of the frame.
+    bool filt = false;
+    double fdelta = 0.0;
+    float fdp = 0.f, fd2 = 0.f;
+    if (FILT && kTwoPhase && split) {
+      filt = true;
+      const double vmax = (double)__int_as_float(misc[S_VMAX]);
+      const double ymax = (double)__int_as_float(misc[S_YMAX]);
+      fdelta = ldexp(vmax * (0.5 * (double)W * (double)(W + 1)) * 1.001, -24) +
+               ldexp(((double)W + P.alpha + 1.0) * ymax, -22);
+      fdp = __double2float_ru(fdelta);
+      // band width 2 fdelta, plus the float rounding of (max - fd2)
+      fd2 = __double2float_ru(2.0 * fdelta + ldexp(((double)W + P.alpha + 1.0) * ymax, -22));
+    }
 
     // ---------------- guarded path: per-column argmin masks into registers -----
     // Bit j of am[q] says column tid + q*T is the argmin of its j-th check
@@ -812,10 +875,47 @@ decode_kernel(const __grid_constant__ KParams P) {
         const unsigned long long cc = f2pack(cmag, cmag);
         // per-thread part of the address, plus a warp-uniform part per j
         const uint32_t baseT = (uint32_t)__cvta_generic_to_shared(smem_raw) + 8u * (uint32_t)tid;
+        if (filt) { // approximate: plain fp32 sums (within fdelta), lo stays 0
+#pragma unroll
+          for (int j = 0; j < (WT > 0 ? WT : 1); ++j)
+            GatherF2<0, NP, TB>::run(hi, baseT + (uint32_t)P.uoff[j]);
+        } else {
 #pragma unroll
         for (int j = 0; j < (WT > 0 ? WT : 1); ++j) // P.uoff[j]: host-computed uniform part
           GatherP2<0, NP, TB>::run(hi, lo, baseT + (uint32_t)P.uoff[j], cc);
-        if (WT <= 32) {
+        }
+        if (filt) {
+          // filtered metric, stored as float (the selection's band test covers
+          // the float rounding: fdelta)
+          float *Efl = reinterpret_cast<float *>(Ebuf);
+#pragma unroll
+          for (int qp = 0; qp < NP; ++qp) {
+            const float2 h = f2unpack(hi[qp]);
+            const int n = 2 * tid + 2 * T * qp;
+            if (n < N) {
+              const int4 cv = (n + 1 < N) ? *reinterpret_cast<const int4 *>(sCorr + 2 * n)
+                                          : make_int4(sCorr[2 * n], sCorr[2 * n + 1], 0, 0);
+              double a0 = (double)h.x, a1 = (double)h.y;
+              if (cv.x | cv.y) a0 = __dadd_rn(a0, __dmul_rn((double)(((long long)cv.y << 24) + cv.x), qexp));
+              if (cv.z | cv.w) a1 = __dadd_rn(a1, __dmul_rn((double)(((long long)cv.w << 24) + cv.z), qexp));
+              double aa0, aa1 = 0.0;
+              if (P.has_ay) {
+                aa0 = sAY[n];
+                if (n + 1 < N) aa1 = sAY[n + 1];
+              } else {
+                aa0 = __dmul_rn(P.alpha, P.alias_y ? fabs((double)load_y<YT>(P, f, n)) : fabs((double)ybuf[n]));
+                if (n + 1 < N)
+                  aa1 = __dmul_rn(P.alpha, P.alias_y ? fabs((double)load_y<YT>(P, f, n + 1))
+                                                     : fabs((double)ybuf[n + 1]));
+              }
+              const float e0 = __double2float_rn(__dsub_rn(a0, aa0));
+              if (n + 1 < N)
+                *reinterpret_cast<float2 *>(Efl + n) = make_float2(e0, __double2float_rn(__dsub_rn(a1, aa1)));
+              else
+                Efl[n] = e0;
+            }
+          }
+        } else if (WT <= 32) {
 #pragma unroll
         for (int qp = 0; qp < NP; ++qp) {
           // columns (n, n+1), n even: 16-byte accesses to the per-column arrays
@@ -1093,26 +1193,78 @@ decode_kernel(const __grid_constant__ KParams P) {
         const int p = P.p;
         const int nb = P.nblocks;
         const int TPB = 1 << sel_lt;
-        const int sub = sel_sub, gpc = sel_gpc, slot = sel_slot, rounds = fused ? 0 : sel_rounds;
+        const int sub = sel_sub, gpc = sel_gpc, slot = sel_slot;
+        const int rounds = fused ? 0 : sel_rounds;
         for (int r = 0; r < rounds; ++r) {
           const int b = r * gpc + slot;
           const bool ok = b < nb;
+          const int base = b * p;
+          const int lim = ok ? min(p, N - base) : 0;
           double v = -dinf();
           int i = 0x7fffffff;
+          if (filt) {
+            // Filtered metric (float, within fdelta of the exact one): scan
+            // with the runner-up value, butterfly over (max, index, runner-up).
+            // The block's decision is settled when the runner-up is more than
+            // 2 fdelta below the maximum (then the maximum is the exact first
+            // maximum) and the maximum is farther than fdelta from 0 (then its
+            // sign is exact); otherwise the columns in the band are recomputed
+            // exactly.  fd2 / fdp are rounded outwards (see fdelta).
+            const float *Efl = reinterpret_cast<const float *>(Ebuf);
+            float fv = -INFINITY, fv2 = -INFINITY;
+            if (ok)
+              for (int o = sub; o < lim; o += TPB) {
+                const float e = Efl[base + o];
+                fv2 = fmaxf(fv2, fminf(fv, e));
+                if (e > fv) { fv = e; i = base + o; }
+              }
+            bool amb = false;
+            if (__any_sync(FULL_MASK, ok)) {
+              for (int off = TPB >> 1; off; off >>= 1) {
+                const float vo = __shfl_xor_sync(FULL_MASK, fv, off);
+                const int io = __shfl_xor_sync(FULL_MASK, i, off);
+                const float v2o = __shfl_xor_sync(FULL_MASK, fv2, off);
+                fv2 = fmaxf(fmaxf(fv2, v2o), fminf(fv, vo));
+                if (vo > fv || (vo == fv && io < i)) { fv = vo; i = io; }
+              }
+              amb = ok && (fv2 >= fv - fd2 || (fv > -fdp && fv <= fdp));
+            }
+            v = (double)fv;
+            if (__any_sync(FULL_MASK, amb)) {
+              double ve = -dinf();
+              int ie = 0x7fffffff;
+              if (amb)
+                for (int o = sub; o < lim; o += TPB) {
+                  const int n = base + o;
+                  if (Efl[n] >= fv - fd2)
+                    amax_combine(ve, ie, exact_split_metric<YT>(P, sFA, sCorr, sAY, ybuf, f, n, W, qexp), n);
+                }
+              for (int off = TPB >> 1; off; off >>= 1) {
+                const double v2 = __shfl_xor_sync(FULL_MASK, ve, off);
+                const int i2 = __shfl_xor_sync(FULL_MASK, ie, off);
+                amax_combine(ve, ie, v2, i2);
+              }
+              if (amb) {
+                v = ve;
+                i = ie;
+                if (sub == 0 && P.filter_stats) atomicAdd((unsigned long long *)P.filter_stats, 1ull);
+              }
+            }
+          } else {
           if (ok) {
-            const int base = b * p;
-            const int lim = min(p, N - base);
             for (int o = sub; o < lim; o += TPB) {
               const double e = Ebuf[base + o];
               if (e > v) { v = e; i = base + o; }
             }
           }
-          if (__any_sync(FULL_MASK, ok)) // warps without a block skip the butterfly
+          if (__any_sync(FULL_MASK, ok)) { // warps without a block skip the butterfly
             for (int off = TPB >> 1; off; off >>= 1) {
               const double v2 = __shfl_xor_sync(FULL_MASK, v, off);
               const int i2 = __shfl_xor_sync(FULL_MASK, i, off);
               amax_combine(v, i, v2, i2);
             }
+          }
+          }
           {
             const uint32_t pm = __ballot_sync(FULL_MASK, ok && sub == 0 && v > 0.0);
             if (lane == 0 && pm) atomicAdd(&misc[S_F], __popc(pm)); // one count per warp
@@ -1168,6 +1320,23 @@ decode_kernel(const __grid_constant__ KParams P) {
             int gi = 0x7fffffff;
             for (int bb = lane; bb < nb; bb += 32) amax_combine(gv, gi, blk_v[bb], blk_i[bb]);
             warp_amax(gv, gi);
+            if (filt) { // the block maxima are exact argmaxes, their values within fdelta
+              const double thr = gv - (double)fd2;
+              int cnt = 0;
+              for (int bb = lane; bb < nb; bb += 32) cnt += blk_v[bb] >= thr;
+              for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(FULL_MASK, cnt, off);
+              if (cnt > 1) {
+                double ve = -dinf();
+                int ie = 0x7fffffff;
+                for (int bb = lane; bb < nb; bb += 32)
+                  if (blk_v[bb] >= thr)
+                    amax_combine(ve, ie, exact_split_metric<YT>(P, sFA, sCorr, sAY, ybuf, f, blk_i[bb], W, qexp),
+                                 blk_i[bb]);
+                warp_amax(ve, ie);
+                gi = ie;
+                if (lane == 0 && P.filter_stats) atomicAdd((unsigned long long *)P.filter_stats + 1, 1ull);
+              }
+            }
             if (lane == 0) { misc[S_GBEST] = gi; flips[0] = gi; }
           }
         }
@@ -1444,12 +1613,15 @@ decode_kernel(const __grid_constant__ KParams P) {
 
 // explicit instantiations used by the launcher
 #define FWBF_INST(YT, C, KC, TB, WT) \
-  template __global__ void decode_kernel<YT, C, KC, TB, WT, false>(const __grid_constant__ KParams);
+  template __global__ void decode_kernel<YT, C, KC, TB, WT, 0>(const __grid_constant__ KParams);
 #define FWBF_INST_INC(YT, C, KC, TB, WT) \
-  template __global__ void decode_kernel<YT, C, KC, TB, WT, true>(const __grid_constant__ KParams);
+  template __global__ void decode_kernel<YT, C, KC, TB, WT, 1>(const __grid_constant__ KParams);
+#define FWBF_INST_FILT(YT, C, KC, TB, WT) \
+  template __global__ void decode_kernel<YT, C, KC, TB, WT, 2>(const __grid_constant__ KParams);
 FWBF_FAST_CONFIGS(FWBF_INST)
 FWBF_F64_CONFIGS(FWBF_INST)
 FWBF_INC_CONFIGS(FWBF_INST_INC)
+FWBF_INC_CONFIGS(FWBF_INST_FILT)
 FWBF_INST(double, true, 1, 0, 0)
 FWBF_INST(float, false, 1, 0, 0)
 FWBF_INST(double, false, 1, 0, 0)

@@ -19,7 +19,8 @@ constexpr int kMaxQcBlocks = 256;  // quasi-cyclic shift table entries in the pa
   X(float, true, 8, 512, 0)     \
   X(float, true, 8, 1024, 0)
 
-// IMWBF (one flip per iteration) with the incremental integer metric
+// compile-time-weight shapes that also exist as MODE 1 (IMWBF, one flip per
+// iteration, incremental integer metric) and MODE 2 (FWBF, filtered metric)
 #define FWBF_INC_CONFIGS(X)     \
   X(float, true, 2, 128, 16)    \
   X(float, true, 4, 256, 32)    \
@@ -87,6 +88,8 @@ struct KParams {
   long long metric_ld;
   int uoff[kMaxCircWeight]; // split-fp32 gather: byte offset of check (n - c_j) for even n, minus 4n
   int no_split; // disable the split-fp32 path (testing)
+  int filter;   // FWBF on the split path: approximate fp32 gather + exact resolution of close decisions
+  unsigned long long *filter_stats; // optional [2]: blocks resolved exactly, stall argmaxes resolved exactly
 };
 
 } // namespace fwbf

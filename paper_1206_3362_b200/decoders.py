@@ -136,6 +136,13 @@ class DeviceCode:
     def close(self):
         self._fin()
 
+    def filter_stats(self, reset: bool = False) -> Tuple[int, int]:
+        """(block argmaxes, stall argmaxes) the filtered FWBF metric resolved with
+        exact column sums in this code's launches so far (diagnostic)."""
+        out = (C.c_int64 * 2)()
+        nat.check(nat.lib().fwbf_filter_stats(self.handle, out, 1 if reset else 0), "filter_stats")
+        return int(out[0]), int(out[1])
+
 
 _CODES: Dict[Tuple[int, int], DeviceCode] = {}
 
@@ -170,7 +177,7 @@ def make_params(cfg: DecoderConfig, algorithm: str, force_ordered=False) -> nat.
     p.block_len_p = int(cfg.block_len_p) if cfg.block_len_p is not None else 0
     p.stall = nat.STALL[cfg.stall_policy]
     p.mlp_threshold = 1 if cfg.mlp_threshold else 0
-    p.force_ordered = int(force_ordered)  # True/1: ordered path; 2: no split-fp32 path
+    p.force_ordered = int(force_ordered)  # bit flags: 1 ordered path; 2 no split-fp32 path; 4 no filtered metric
     return p
 
 

@@ -36,7 +36,7 @@ def assert_batch_equal(res, z, iters, conv, stalled, flips_total, logs, tag):
             assert a == b, f"{tag}: flip log of frame {i} differs"
 
 
-@pytest.mark.parametrize("ordered", [0, 1, 2], ids=["default", "ordered", "fp64guard"])
+@pytest.mark.parametrize("ordered", [0, 1, 2, 4], ids=["default", "ordered", "fp64guard", "nofilter"])
 @pytest.mark.parametrize("name", case_names())
 def test_golden_fixture(cuda_device, name, ordered):
     c = load_case(name)
