@@ -245,6 +245,7 @@ def main():
     for _ in range(a.warmup):
         step()
     torch.cuda.synchronize()
+    dc.filter_stats(reset=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -258,6 +259,7 @@ def main():
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
+    fstats = dc.filter_stats(reset=True)   # exact resolutions of the filtered metric, timed steps
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -334,7 +336,11 @@ def main():
         ev_rate = edge_visits / (launch_ms / 1e3)
         dadd_peak = sms * 64 * max_mhz * 1e6
         smem_peak = sms * 128 * max_mhz * 1e6
-        gather_bound = sms * 25.6 * max_mhz * 1e6
+        # filtered gather (FWBF on split-path frames): one 8-byte LDS brings the
+        # float32 signed weights of two columns, one FADD2 adds them -- 4 B of
+        # shared memory per edge visit, so 128 B/clk/SM caps it at 32 visits/clk/SM
+        gather_bound = sms * 32.0 * max_mhz * 1e6
+        block_decisions = B * a.steps * ((n + a.p - 1) // a.p) * mean_iters
         line = {
             "metric": "FWBF decoded info Gbit/s", "value": value, "unit": "Gbit/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
@@ -350,9 +356,12 @@ def main():
                          "bytes_per_frame": bytes_frame,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                          "binding": {
-                             "resource": "SM FP32 pipe + shared memory: split-fp32 metric gather "
-                                         "(4 B and 5 fp32 adds per edge visit; 25.6 edge visits/clk/SM "
-                                         "at 128 fp32 lanes/clk)",
+                             "resource": "shared memory: filtered metric gather (one 8-byte LDS + one "
+                                         "FADD2 per two edge visits; 4 B/edge at 128 B/clk/SM = 32 edge "
+                                         "visits/clk/SM)",
+                             "filter_exact_block_decisions": fstats[0],
+                             "filter_exact_fraction": fstats[0] / max(1.0, block_decisions),
+                             "filter_exact_stall_argmaxes": fstats[1],
                              "edge_visits_per_frame": edges * (1.0 + mean_iters),
                              "edge_visits_per_s": ev_rate,
                              "gather_bound_per_s": gather_bound,
