@@ -152,7 +152,9 @@ template <int QP, int NP, int TB> struct GatherF2<QP, NP, TB, false> {
 struct RefreshAddr {
   uint32_t fa, fa2, fb, fb2, m2, a2, corr;
 };
-template <int KK, int KC, int TB, bool GO = (KK < KC)> struct RefreshKK {
+// CC (MODE 2): the argmin column's correction is one int32 on the coarse grid
+// (m2 addresses the per-check Dc, corr the per-column Cc): one atomic.
+template <int KK, int KC, int TB, bool CC = false, bool GO = (KK < KC)> struct RefreshKK {
   static __device__ __forceinline__ void run(const RefreshAddr &A, const uint32_t *sbits, uint32_t &sprev,
                                              int &pc, int tid, int warp, int lane, int M, bool imw) {
     if (KK * TB + warp * 32 < M) { // warp-uniform: this warp's word exists
@@ -167,7 +169,13 @@ template <int KK, int KC, int TB, bool GO = (KK < KC)> struct RefreshKK {
         asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(A.fa2), "n"(4 * KK * TB), "f"(v));
         asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(A.fb), "n"(4 * KK * TB), "f"(v));
         asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(A.fb2), "n"(4 * KK * TB), "f"(v));
-        if (imw) { // correction sign flips with s_m
+        if (CC && imw) { // correction sign flips with s_m: +-2 Dc
+          int dc;
+          unsigned short a2;
+          asm volatile("ld.shared.s32 %0, [%1+%2];" : "=r"(dc) : "r"(A.m2), "n"(4 * KK * TB));
+          asm volatile("ld.shared.u16 %0, [%1+%2];" : "=h"(a2) : "r"(A.a2), "n"(2 * KK * TB));
+          asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(A.corr + 4u * (uint32_t)a2), "r"(s ? 2 * dc : -2 * dc));
+        } else if (imw) { // correction sign flips with s_m
           int dx, dy;
           unsigned short a2;
           asm volatile("ld.shared.v2.s32 {%0, %1}, [%2+%3];" : "=r"(dx), "=r"(dy) : "r"(A.m2), "n"(8 * KK * TB));
@@ -181,10 +189,10 @@ template <int KK, int KC, int TB, bool GO = (KK < KC)> struct RefreshKK {
       sprev ^= (tog ? 1u : 0u) << KK;
       pc += __popc(word);
     }
-    RefreshKK<KK + 1, KC, TB>::run(A, sbits, sprev, pc, tid, warp, lane, M, imw);
+    RefreshKK<KK + 1, KC, TB, CC>::run(A, sbits, sprev, pc, tid, warp, lane, M, imw);
   }
 };
-template <int KK, int KC, int TB> struct RefreshKK<KK, KC, TB, false> {
+template <int KK, int KC, int TB, bool CC> struct RefreshKK<KK, KC, TB, CC, false> {
   static __device__ __forceinline__ void run(const RefreshAddr &, const uint32_t *, uint32_t &, int &, int, int,
                                              int, int, bool) {}
 };
@@ -204,20 +212,31 @@ __device__ __forceinline__ YT load_y(const KParams &P, long long f, int n) {
   return __ldg(y + f * P.ld + n);
 }
 
-// Exact Eq.(1) metric of one column on the split path (the filter's fallback).
-// Every signed min1 is a float32 multiple of q and the path guard keeps all
-// partial sums of W of them below 2^53 q, so this fp64 sum is exact in any
-// order; adding the exact argmin correction and subtracting fl(alpha|y_n|)
-// reproduces the exact pass (and the reference) bit for bit.
+// Exact Eq.(1) metric of one column on the split path (the filter's fallback,
+// MODE 2).  Every signed min1 is a float32 multiple of q and the path guard
+// keeps all partial sums of W of them below 2^53 q, so this fp64 sum is exact
+// in any order.  The argmin correction is rebuilt exactly from the column's
+// own checks: check m = (n - c_j) mod N contributes sgn_m D_m (D_m = (min2 -
+// min1) / q, an exact int64) when its argmin is n, sgn_m being the sign of its
+// min1 copy (the iteration-start syndrome; sbits may already hold this
+// iteration's flips).  Subtracting fl(alpha|y_n|) reproduces the exact pass
+// (and the reference) bit for bit.
 template <typename YT>
-__device__ __forceinline__ double exact_split_metric(const KParams &P, const float *sFA, const int *sCorr,
-                                                  const double *sAY, const YT *ybuf, long long f, int n, int W,
-                                                  double qexp) {
+__device__ __forceinline__ double exact_split_metric(const KParams &P, const float *sFA, const uint16_t *sA2,
+                                                  const long long *sD, const double *sAY, const YT *ybuf,
+                                                  long long f, int n, int W, double qexp) {
   const int N = P.n;
   double acc = 0.0;
-  for (int j = 0; j < W; ++j) acc = __dadd_rn(acc, (double)sFA[n + N - P.off[j]]);
-  const int2 cv = reinterpret_cast<const int2 *>(sCorr)[n];
-  if (cv.x | cv.y) acc = __dadd_rn(acc, __dmul_rn((double)(((long long)cv.y << 24) + cv.x), qexp));
+  long long corr = 0;
+  const bool imw = P.wmode == FWBF_WEIGHTS_IMWBF;
+  for (int j = 0; j < W; ++j) {
+    const int d = n + N - P.off[j]; // doubled copy: check (n - c_j) mod N
+    const float v = sFA[d];
+    acc = __dadd_rn(acc, (double)v);
+    const int m = d >= N ? d - N : d;
+    if (imw && sA2[m] == n) corr += signbit(v) ? -sD[m] : sD[m];
+  }
+  if (corr) acc = __dadd_rn(acc, __dmul_rn((double)corr, qexp));
   const double aa = P.has_ay ? sAY[n]
                              : __dmul_rn(P.alpha, P.alias_y ? fabs((double)load_y<YT>(P, f, n)) : fabs((double)ybuf[n]));
   return __dsub_rn(acc, aa);
@@ -416,6 +435,11 @@ decode_kernel(const __grid_constant__ KParams P) {
     // values the split sums actually see) instead of max|y| -- about ten times
     // looser -- before any path-specific state is written.
     constexpr bool kTwoPhase = kGuard && TB > 0 && WT > 0 && (KC % 2) == 0 && WT <= 64;
+    // MODE 2 argmin corrections on a coarse grid G = 2^gsh q: one int32 per
+    // column (Cc, in the first half of sCorr), per check the exact D (int64, in
+    // sM2) and its grid value Dc (int32, second half of sCorr)
+    int gsh = 0;
+    float Gf = 0.f;
     constexpr int KR = kTwoPhase ? KC : 1;
     YT r_min1[KR], r_min2[KR];
     int r_ac[KR];
@@ -519,6 +543,11 @@ decode_kernel(const __grid_constant__ KParams P) {
           qinv = ldexp(1.0, -misc[S_EQ]);
         }
       }
+      if (FILT && split) { // D < max|y| / q < 2^bits; Dc = D / 2^gsh rounded, |Dc| <= 2^24
+        const int bits = ilogbf(__int_as_float(misc[S_YMAX])) + 1 - misc[S_EQ];
+        gsh = bits > 24 ? bits - 24 : 0;
+        Gf = ldexpf(1.f, gsh + misc[S_EQ]);
+      }
 #pragma unroll
       for (int k = 0; k < KR; ++k) {
         const int m = tid + k * T;
@@ -536,7 +565,13 @@ decode_kernel(const __grid_constant__ KParams P) {
             sFB[m + 1] = s1v;
             sFB[m + N + 1] = s1v;
             sA2[m] = (uint16_t)ac;
-            if (P.wmode == FWBF_WEIGHTS_IMWBF) { // column ac reads min2: + sgn*(min2-min1)
+            if (FILT && P.wmode == FWBF_WEIGHTS_IMWBF) {
+              const long long D = (long long)__dmul_rn(__dsub_rn(d2, d1), qinv); // exact integer
+              const int Dc = (int)((D + (gsh ? (1ll << (gsh - 1)) : 0ll)) >> gsh);
+              reinterpret_cast<long long *>(sM2)[m] = D;
+              sCorr[N + m] = Dc;
+              atomicAdd(&sCorr[ac], par ? Dc : -Dc);
+            } else if (P.wmode == FWBF_WEIGHTS_IMWBF) { // column ac reads min2: + sgn*(min2-min1)
               const long long D = (long long)__dmul_rn(__dsub_rn(d2, d1), qinv); // exact integer
               corr_add(sCorr, ac, par ? D : -D, 1);
               // limb change when s_m goes 0 -> 1 (negated for 1 -> 0)
@@ -701,9 +736,10 @@ decode_kernel(const __grid_constant__ KParams P) {
     // min1 values directly in fp32.  Each of a column's W sequential
     // round-to-nearest adds errs by at most u = 2^-24 of its partial sum
     // (<= k vmax after k terms), so |approx - exact| <= u vmax W(W+1)/2; the
-    // fp64 finalize and the float store of the filtered metric add
-    // at most 2^-23 (W + alpha) max|y| (|E_n| <= (W + alpha) max|y|).  fdelta
-    // bounds both, for every column of the frame.
+    // float finalize (the int-to-float correction, one FMA, fl32(alpha|y|),
+    // one subtraction) adds at most 2^-22 (W + alpha + 1) max|y| (every
+    // operand is at most (W + alpha) max|y|), and the coarse correction grid
+    // W G / 2.  fdelta bounds all of it, for every column of the frame.
     bool filt = false;
     double fdelta = 0.0;
     float fdp = 0.f, fd2 = 0.f;
@@ -711,8 +747,10 @@ decode_kernel(const __grid_constant__ KParams P) {
       filt = true;
       const double vmax = (double)__int_as_float(misc[S_VMAX]);
       const double ymax = (double)__int_as_float(misc[S_YMAX]);
+      // + the coarse argmin corrections: at most W checks of a column, each
+      // rounded to the grid G by at most G/2
       fdelta = ldexp(vmax * (0.5 * (double)W * (double)(W + 1)) * 1.001, -24) +
-               ldexp(((double)W + P.alpha + 1.0) * ymax, -22);
+               ldexp(((double)W + P.alpha + 1.0) * ymax, -22) + 0.5 * (double)W * (double)Gf;
       fdp = __double2float_ru(fdelta);
       // band width 2 fdelta, plus the float rounding of (max - fd2)
       fd2 = __double2float_ru(2.0 * fdelta + ldexp(((double)W + P.alpha + 1.0) * ymax, -22));
@@ -733,7 +771,14 @@ decode_kernel(const __grid_constant__ KParams P) {
     if (kGuard && split && P.has_ay) { // fl(alpha |y_n|) once per frame (ybuf is still valid here)
       for (int n = tid; n < N; n += T) sAY[n] = __dmul_rn(P.alpha, fabs((double)ybuf[n]));
     }
-    if (P.alias_y) __syncthreads(); // amask / ybuf may overlay Ebuf (compact layout)
+    if (FILT && split) { // MODE 2: fl32(fl64(alpha |y_n|)) after the float metric (even offset)
+      float *aaf = reinterpret_cast<float *>(Ebuf) + ((N + 1) & ~1);
+      for (int n = tid; n < N; n += T)
+        aaf[n] = __double2float_rn(P.has_ay ? sAY[n]
+                                            : __dmul_rn(P.alpha, P.alias_y ? fabs((double)load_y<YT>(P, f, n))
+                                                                           : fabs((double)ybuf[n])));
+    }
+    if (P.alias_y || (FILT && split)) __syncthreads(); // amask / ybuf may overlay Ebuf (compact layout); MODE 2 tables
 
     // ---------------- iterations -----------------------------------------------
     int k = 0;
@@ -885,34 +930,22 @@ decode_kernel(const __grid_constant__ KParams P) {
           GatherP2<0, NP, TB>::run(hi, lo, baseT + (uint32_t)P.uoff[j], cc);
         }
         if (filt) {
-          // filtered metric, stored as float (the selection's band test covers
-          // the float rounding: fdelta)
+          // filtered metric in float: sum + Cc G (coarse argmin correction) -
+          // fl32(alpha |y|); the selection's band test covers every rounding
           float *Efl = reinterpret_cast<float *>(Ebuf);
+          const float *aaf = Efl + ((N + 1) & ~1);
 #pragma unroll
           for (int qp = 0; qp < NP; ++qp) {
             const float2 h = f2unpack(hi[qp]);
             const int n = 2 * tid + 2 * T * qp;
-            if (n < N) {
-              const int4 cv = (n + 1 < N) ? *reinterpret_cast<const int4 *>(sCorr + 2 * n)
-                                          : make_int4(sCorr[2 * n], sCorr[2 * n + 1], 0, 0);
-              double a0 = (double)h.x, a1 = (double)h.y;
-              if (cv.x | cv.y) a0 = __dadd_rn(a0, __dmul_rn((double)(((long long)cv.y << 24) + cv.x), qexp));
-              if (cv.z | cv.w) a1 = __dadd_rn(a1, __dmul_rn((double)(((long long)cv.w << 24) + cv.z), qexp));
-              double aa0, aa1 = 0.0;
-              if (P.has_ay) {
-                aa0 = sAY[n];
-                if (n + 1 < N) aa1 = sAY[n + 1];
-              } else {
-                aa0 = __dmul_rn(P.alpha, P.alias_y ? fabs((double)load_y<YT>(P, f, n)) : fabs((double)ybuf[n]));
-                if (n + 1 < N)
-                  aa1 = __dmul_rn(P.alpha, P.alias_y ? fabs((double)load_y<YT>(P, f, n + 1))
-                                                     : fabs((double)ybuf[n + 1]));
-              }
-              const float e0 = __double2float_rn(__dsub_rn(a0, aa0));
-              if (n + 1 < N)
-                *reinterpret_cast<float2 *>(Efl + n) = make_float2(e0, __double2float_rn(__dsub_rn(a1, aa1)));
-              else
-                Efl[n] = e0;
+            if (n + 1 < N) {
+              const int2 cc = *reinterpret_cast<const int2 *>(sCorr + n);
+              const float2 aa = *reinterpret_cast<const float2 *>(aaf + n);
+              *reinterpret_cast<float2 *>(Efl + n) =
+                  make_float2(__fsub_rn(__fmaf_rn((float)cc.x, Gf, h.x), aa.x),
+                              __fsub_rn(__fmaf_rn((float)cc.y, Gf, h.y), aa.y));
+            } else if (n < N) {
+              Efl[n] = __fsub_rn(__fmaf_rn((float)sCorr[n], Gf, h.x), aaf[n]);
             }
           }
         } else if (WT <= 32) {
@@ -1237,7 +1270,7 @@ decode_kernel(const __grid_constant__ KParams P) {
                 for (int o = sub; o < lim; o += TPB) {
                   const int n = base + o;
                   if (Efl[n] >= fv - fd2)
-                    amax_combine(ve, ie, exact_split_metric<YT>(P, sFA, sCorr, sAY, ybuf, f, n, W, qexp), n);
+                    amax_combine(ve, ie, exact_split_metric<YT>(P, sFA, sA2, reinterpret_cast<const long long *>(sM2), sAY, ybuf, f, n, W, qexp), n);
                 }
               for (int off = TPB >> 1; off; off >>= 1) {
                 const double v2 = __shfl_xor_sync(FULL_MASK, ve, off);
@@ -1330,7 +1363,7 @@ decode_kernel(const __grid_constant__ KParams P) {
                 int ie = 0x7fffffff;
                 for (int bb = lane; bb < nb; bb += 32)
                   if (blk_v[bb] >= thr)
-                    amax_combine(ve, ie, exact_split_metric<YT>(P, sFA, sCorr, sAY, ybuf, f, blk_i[bb], W, qexp),
+                    amax_combine(ve, ie, exact_split_metric<YT>(P, sFA, sA2, reinterpret_cast<const long long *>(sM2), sAY, ybuf, f, blk_i[bb], W, qexp),
                                  blk_i[bb]);
                 warp_amax(ve, ie);
                 gi = ie;
@@ -1487,11 +1520,14 @@ decode_kernel(const __grid_constant__ KParams P) {
         asm("mov.b32 %0, %1;" : "=r"(A.fa2) : "r"(fa + 4u * (uint32_t)N));
         asm("mov.b32 %0, %1;" : "=r"(A.fb) : "r"(fb));
         asm("mov.b32 %0, %1;" : "=r"(A.fb2) : "r"(fb + 4u * (uint32_t)N));
-        asm("mov.b32 %0, %1;" : "=r"(A.m2) : "r"(s0 + (uint32_t)P.off_m2s + 8u * (uint32_t)tid));
+        if (FILT) // per-check Dc in the second half of sCorr
+          asm("mov.b32 %0, %1;" : "=r"(A.m2) : "r"(s0 + (uint32_t)P.off_corr + 4u * (uint32_t)(N + tid)));
+        else
+          asm("mov.b32 %0, %1;" : "=r"(A.m2) : "r"(s0 + (uint32_t)P.off_m2s + 8u * (uint32_t)tid));
         asm("mov.b32 %0, %1;" : "=r"(A.a2) : "r"(s0 + (uint32_t)P.off_a2m + 2u * (uint32_t)tid));
         asm("mov.b32 %0, %1;" : "=r"(A.corr) : "r"(s0 + (uint32_t)P.off_corr));
         int pc = 0;
-        RefreshKK<0, (TB > 0 ? KC : 1), (TB > 0 ? TB : 1)>::run(A, sbits, sprev, pc, tid, warp, lane, M,
+        RefreshKK<0, (TB > 0 ? KC : 1), (TB > 0 ? TB : 1), FILT>::run(A, sbits, sprev, pc, tid, warp, lane, M,
                                                               P.wmode == FWBF_WEIGHTS_IMWBF);
         if (lane == 0 && pc) atomicAdd(&misc[S_SWT], pc);
       } else if (TB > 0) {
