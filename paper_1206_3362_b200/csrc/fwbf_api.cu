@@ -321,7 +321,7 @@ struct Plan {
 };
 
 static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool circ, int cover, KParams &P,
-                   bool compact = false, bool fused = false) {
+                   bool compact = false, bool fused = false, bool mode2 = false) {
   const int n = c->n, m = c->m;
   const int zw = (n + 31) / 32, sw = (m + 31) / 32;
   int nb = 1;
@@ -345,7 +345,27 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
   // check records: guarded path (circulant) = two doubled arrays sgn*min1,
   // sgn*min2 with a pad up to the threads' column cover; ordered path =
   // chk1[m], chk2[m], amin[m] inside the same region.
-  if (circ) {
+  if (circ && mode2) {
+    // MODE 2 (filtered FWBF): split frames keep the two doubled float32 copies,
+    // min2 per check (float), the argmin column and one coarse correction per
+    // column; |y| lives in the metric region. Other frames take the ordered
+    // path on single (wrapped) fp64 records with the argmin masks after them.
+    const int dblf = (2 * n + std::max(0, cover - n) + 2 + 31) / 32 * 32;
+    const int split_bytes = 2 * dblf * 4 + align16(m * 4) + align16(m * 2) + align16(n * 4);
+    const int fp64_bytes = 2 * align16(m * 8) + n * aw * 4;
+    const int r = take(std::max(fp64_bytes, split_bytes));
+    P.off_chk1 = r;
+    P.off_chk2 = r + align16(m * 8);
+    P.off_amask = P.off_chk2 + align16(m * 8);
+    P.off_fa = r;
+    P.off_fb = r + dblf * 4;
+    P.off_m2s = r + 2 * dblf * 4;
+    P.off_a2m = P.off_m2s + align16(m * 4);
+    P.off_corr = P.off_a2m + align16(m * 2);
+    P.off_ay = P.off_corr;
+    P.has_ay = 0;
+    P.off_amin = 0;
+  } else if (circ) {
     // both doubled arrays; chk2 - chk1 is a multiple of 128 B so a lane that
     // reads min2 instead of min1 hits the same banks (no extra wavefront)
     const int dbl = (2 * n + std::max(0, cover - n) + 31) / 32 * 32;
@@ -442,7 +462,8 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   P.alpha = p->alpha;
   // FWBF: approximate fp32 gather on split-path frames, close decisions
   // resolved exactly (kernel: GatherF2 / exact_split_metric); same results
-  P.filter = p->algorithm == FWBF_ALG_FWBF && !metric_out && !(p->force_ordered & 4) && !getenv("FWBF_NO_FILTER");
+  P.filter = p->algorithm == FWBF_ALG_FWBF && !metric_out && !(p->force_ordered & 4) && !getenv("FWBF_NO_FILTER") &&
+             !P.no_split; // the guarded fp64 path exists only in the exact kernels
   P.filter_stats = c->d_fstats;
   P.nblocks = p->algorithm == FWBF_ALG_FWBF ? (c->n + p->block_len_p - 1) / p->block_len_p : 1;
   P.y = y;
@@ -471,6 +492,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   int T = 0;
   int kc = 1;
   int kwt = 0; // compile-time circulant weight of the chosen kernel (0: runtime)
+  bool mode2 = false; // MODE 2 (filtered) kernel: its own shared-memory layout
   if (circ) {
     if (sizeof(YT) == 4) {
       struct Shape { int kc, tb, wt; const void *fn; };
@@ -509,13 +531,16 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
       }
       // FWBF: the same shape with the filtered metric (P.filter)
       if (kwt && P.filter) {
+        mode2 = true;
         static const Shape filt[] = {
 #define FWBF_SHAPE_FILT(YT_, C_, KC_, TB_, WT_) {KC_, TB_, WT_, (const void *)fwbf::decode_kernel<YT_, C_, KC_, TB_, WT_, 2>},
             FWBF_INC_CONFIGS(FWBF_SHAPE_FILT)
 #undef FWBF_SHAPE_FILT
         };
+        bool found = false;
         for (const Shape &sh : filt)
-          if (sh.kc == kc && sh.tb == T && sh.wt == kwt) kern = sh.fn;
+          if (sh.kc == kc && sh.tb == T && sh.wt == kwt) { kern = sh.fn; found = true; }
+        mode2 = found;
       }
     } else {
       struct Shape { int kc, tb, wt; const void *fn; };
@@ -553,10 +578,10 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   if (!circ)
     if (const char *e = getenv("FWBF_EXPLICIT_T")) T = atoi(e); // tuning: threads per CTA (multiple of 32)
   const bool compact = circ && sizeof(YT) == 4 && c->w <= 32 && !getenv("FWBF_NO_COMPACT");
-  layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, P.fused);
+  layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, P.fused, mode2);
   if (P.fused && P.smem_bytes > c->smem_optin) { // y must stay resident for the fused pass
     P.fused = 0;
-    layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, false);
+    layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, false, mode2);
   }
   {
     // FWBF block-argmax groups: odd p -> one thread per block (stride-p reads
@@ -607,6 +632,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
       P.uoff[j] = ((d & 1) ? P.off_fb + 4 : P.off_fa) + 4 * d;
     }
   }
+  if (const char *e = getenv("FWBF_SMEM_PAD")) P.smem_bytes += atoi(e); // tuning: occupancy sensitivity
   if (P.smem_bytes > c->smem_optin)
     return fail(FWBF_EUNSUPPORTED, "frame state needs %d B of shared memory (device max %d)",
                 P.smem_bytes, c->smem_optin);

@@ -38,6 +38,9 @@
 #ifndef FWBF_MINB_256
 #define FWBF_MINB_256 4
 #endif
+#ifndef FWBF_MINB_256_FILT
+#define FWBF_MINB_256_FILT 5
+#endif
 
 namespace fwbf {
 
@@ -145,12 +148,19 @@ template <int QP, int NP, int TB> struct GatherF2<QP, NP, TB, false> {
   static __device__ __forceinline__ void run(unsigned long long (&)[NP], uint32_t) {}
 };
 
+// MODE 2 coarse argmin correction of a check, in units of the frame's grid G:
+// a deterministic function of the check's float32 minima (init and every
+// refresh compute the same value), within G/2 + 2^-23 max|y| of min2 - min1.
+__device__ __forceinline__ int coarse_dc(float min2, float min1abs, float invG) {
+  return __float2int_rn(__fmul_rn(__fsub_rn(min2, min1abs), invG));
+}
+
 // Split-path refresh of check m = tid + KK*TB (compile-time KK): shared
 // addresses come in pinned registers (base + KK*TB*size as immediates), so
 // the four sign-negating stores and the correction-limb atomics need no
 // per-check address arithmetic.
 struct RefreshAddr {
-  uint32_t fa, fa2, fb, fb2, m2, a2, corr;
+  uint32_t fa, fa2, fb, fb2, m2, a2, corr, invg;
 };
 // CC (MODE 2): the argmin column's correction is one int32 on the coarse grid
 // (m2 addresses the per-check Dc, corr the per-column Cc): one atomic.
@@ -169,11 +179,12 @@ template <int KK, int KC, int TB, bool CC = false, bool GO = (KK < KC)> struct R
         asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(A.fa2), "n"(4 * KK * TB), "f"(v));
         asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(A.fb), "n"(4 * KK * TB), "f"(v));
         asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(A.fb2), "n"(4 * KK * TB), "f"(v));
-        if (CC && imw) { // correction sign flips with s_m: +-2 Dc
-          int dc;
+        if (CC && imw) { // correction sign flips with s_m: +-2 Dc (Dc from the float minima)
+          float mn2;
           unsigned short a2;
-          asm volatile("ld.shared.s32 %0, [%1+%2];" : "=r"(dc) : "r"(A.m2), "n"(4 * KK * TB));
+          asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(mn2) : "r"(A.m2), "n"(4 * KK * TB));
           asm volatile("ld.shared.u16 %0, [%1+%2];" : "=h"(a2) : "r"(A.a2), "n"(2 * KK * TB));
+          const int dc = coarse_dc(mn2, fabsf(v), __uint_as_float(A.invg));
           asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(A.corr + 4u * (uint32_t)a2), "r"(s ? 2 * dc : -2 * dc));
         } else if (imw) { // correction sign flips with s_m
           int dx, dy;
@@ -217,14 +228,14 @@ __device__ __forceinline__ YT load_y(const KParams &P, long long f, int n) {
 // keeps all partial sums of W of them below 2^53 q, so this fp64 sum is exact
 // in any order.  The argmin correction is rebuilt exactly from the column's
 // own checks: check m = (n - c_j) mod N contributes sgn_m D_m (D_m = (min2 -
-// min1) / q, an exact int64) when its argmin is n, sgn_m being the sign of its
+// min1) / q from the stored float32 minima, an exact int64) when its argmin is
+// n, sgn_m being the sign of its
 // min1 copy (the iteration-start syndrome; sbits may already hold this
 // iteration's flips).  Subtracting fl(alpha|y_n|) reproduces the exact pass
 // (and the reference) bit for bit.
-template <typename YT>
 __device__ __forceinline__ double exact_split_metric(const KParams &P, const float *sFA, const uint16_t *sA2,
-                                                  const long long *sD, const double *sAY, const YT *ybuf,
-                                                  long long f, int n, int W, double qexp) {
+                                                  const float *sMin2, const float *yabs, int n, int W,
+                                                  double qexp, double qinv) {
   const int N = P.n;
   double acc = 0.0;
   long long corr = 0;
@@ -234,12 +245,13 @@ __device__ __forceinline__ double exact_split_metric(const KParams &P, const flo
     const float v = sFA[d];
     acc = __dadd_rn(acc, (double)v);
     const int m = d >= N ? d - N : d;
-    if (imw && sA2[m] == n) corr += signbit(v) ? -sD[m] : sD[m];
+    if (imw && sA2[m] == n) {
+      const long long D = (long long)__dmul_rn(__dsub_rn((double)sMin2[m], (double)fabsf(v)), qinv); // exact
+      corr += signbit(v) ? -D : D;
+    }
   }
   if (corr) acc = __dadd_rn(acc, __dmul_rn((double)corr, qexp));
-  const double aa = P.has_ay ? sAY[n]
-                             : __dmul_rn(P.alpha, P.alias_y ? fabs((double)load_y<YT>(P, f, n)) : fabs((double)ybuf[n]));
-  return __dsub_rn(acc, aa);
+  return __dsub_rn(acc, __dmul_rn(P.alpha, (double)yabs[n]));
 }
 
 // ---------------------------------------------------------------------------
@@ -249,7 +261,7 @@ __device__ __forceinline__ double exact_split_metric(const KParams &P, const flo
 //   KC   : columns per thread on the guarded path (register accumulators)
 // ---------------------------------------------------------------------------
 template <typename YT, bool CIRC, int KC, int TB, int WT, int MODE>
-__global__ void __launch_bounds__(TB ? TB : 1024, TB == 256 ? FWBF_MINB_256 : 1024 / (TB ? TB : 1024))
+__global__ void __launch_bounds__(TB ? TB : 1024, TB == 256 ? (MODE == 2 ? FWBF_MINB_256_FILT : FWBF_MINB_256) : 1024 / (TB ? TB : 1024))
 decode_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr bool INC = MODE == 1;  // IMWBF incremental integer metric
@@ -359,8 +371,12 @@ decode_kernel(const __grid_constant__ KParams P) {
           for (int q = 0; q < aw; ++q) amask[n * aw + q] = 0u;
           if (WT > 0 && sizeof(YT) == 4) {
             int *cz = reinterpret_cast<int *>(smem_raw + P.off_corr);
-            cz[2 * n] = 0;
-            cz[2 * n + 1] = 0;
+            if (FILT) {
+              cz[n] = 0; // MODE 2: one coarse correction per column
+            } else {
+              cz[2 * n] = 0;
+              cz[2 * n + 1] = 0;
+            }
           }
         }
       }
@@ -439,7 +455,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     // column (Cc, in the first half of sCorr), per check the exact D (int64, in
     // sM2) and its grid value Dc (int32, second half of sCorr)
     int gsh = 0;
-    float Gf = 0.f;
+    float Gf = 0.f, invGf = 0.f;
     constexpr int KR = kTwoPhase ? KC : 1;
     YT r_min1[KR], r_min2[KR];
     int r_ac[KR];
@@ -543,10 +559,27 @@ decode_kernel(const __grid_constant__ KParams P) {
           qinv = ldexp(1.0, -misc[S_EQ]);
         }
       }
+      if (FILT && fpath == 1) {
+        // MODE 2 has no guarded-fp64 arrays.  Its filtered gather is approximate
+        // anyway and its exact fallback only needs the fp64 guard (every sum of
+        // W minima and the correction exact), so fp64-guarded frames run the
+        // filtered path too (the quantum bounds keep G and 1/G finite floats);
+        // the rest take the ordered path.
+        if (misc[S_EQ] >= -123 && misc[S_EQ] <= 77) {
+          fpath = 2;
+          split = true;
+          qexp = ldexp(1.0, misc[S_EQ]);
+          qinv = ldexp(1.0, -misc[S_EQ]);
+        } else {
+          fpath = 0;
+          fastp = false;
+        }
+      }
       if (FILT && split) { // D < max|y| / q < 2^bits; Dc = D / 2^gsh rounded, |Dc| <= 2^24
         const int bits = ilogbf(__int_as_float(misc[S_YMAX])) + 1 - misc[S_EQ];
         gsh = bits > 24 ? bits - 24 : 0;
         Gf = ldexpf(1.f, gsh + misc[S_EQ]);
+        invGf = ldexpf(1.f, -(gsh + misc[S_EQ]));
       }
 #pragma unroll
       for (int k = 0; k < KR; ++k) {
@@ -566,10 +599,8 @@ decode_kernel(const __grid_constant__ KParams P) {
             sFB[m + N + 1] = s1v;
             sA2[m] = (uint16_t)ac;
             if (FILT && P.wmode == FWBF_WEIGHTS_IMWBF) {
-              const long long D = (long long)__dmul_rn(__dsub_rn(d2, d1), qinv); // exact integer
-              const int Dc = (int)((D + (gsh ? (1ll << (gsh - 1)) : 0ll)) >> gsh);
-              reinterpret_cast<long long *>(sM2)[m] = D;
-              sCorr[N + m] = Dc;
+              reinterpret_cast<float *>(sM2)[m] = (float)min2; // MODE 2: min2 per check
+              const int Dc = coarse_dc((float)min2, (float)min1, invGf);
               atomicAdd(&sCorr[ac], par ? Dc : -Dc);
             } else if (P.wmode == FWBF_WEIGHTS_IMWBF) { // column ac reads min2: + sgn*(min2-min1)
               const long long D = (long long)__dmul_rn(__dsub_rn(d2, d1), qinv); // exact integer
@@ -593,12 +624,15 @@ decode_kernel(const __grid_constant__ KParams P) {
               atomicOr(&amask[ac * aw + (j >> 5)], 1u << (j & 31));
             }
           } else if (CIRC) {
-            // ordered path: doubled records as above; the argmin bit sits at the
-            // check's position in column ac's ascending check list
+            // ordered path: doubled records as above (MODE 2: single, wrapped
+            // on read); the argmin bit sits at the check's position in column
+            // ac's ascending check list
             chk1[m] = sg * d1;
-            chk1[m + N] = sg * d1;
             chk2[m] = sg * d2;
-            chk2[m + N] = sg * d2;
+            if (!FILT) {
+              chk1[m + N] = sg * d1;
+              chk2[m + N] = sg * d2;
+            }
             if (P.wmode == FWBF_WEIGHTS_IMWBF) {
               int d = ac - m;
               if (d < 0) d += N;
@@ -750,7 +784,8 @@ decode_kernel(const __grid_constant__ KParams P) {
       // + the coarse argmin corrections: at most W checks of a column, each
       // rounded to the grid G by at most G/2
       fdelta = ldexp(vmax * (0.5 * (double)W * (double)(W + 1)) * 1.001, -24) +
-               ldexp(((double)W + P.alpha + 1.0) * ymax, -22) + 0.5 * (double)W * (double)Gf;
+               ldexp(((double)W + P.alpha + 1.0) * ymax, -22) + 0.5 * (double)W * (double)Gf +
+               ldexp((double)W * ymax, -23);
       fdp = __double2float_ru(fdelta);
       // band width 2 fdelta, plus the float rounding of (max - fd2)
       fd2 = __double2float_ru(2.0 * fdelta + ldexp(((double)W + P.alpha + 1.0) * ymax, -22));
@@ -768,15 +803,15 @@ decode_kernel(const __grid_constant__ KParams P) {
         am[q][1] = (n < N && aw > 1) ? amask[n * aw + 1] : 0u;
       }
     }
-    if (kGuard && split && P.has_ay) { // fl(alpha |y_n|) once per frame (ybuf is still valid here)
+    if (!FILT && kGuard && split && P.has_ay) { // fl(alpha |y_n|) once per frame (ybuf is still valid here)
       for (int n = tid; n < N; n += T) sAY[n] = __dmul_rn(P.alpha, fabs((double)ybuf[n]));
     }
-    if (FILT && split) { // MODE 2: fl32(fl64(alpha |y_n|)) after the float metric (even offset)
-      float *aaf = reinterpret_cast<float *>(Ebuf) + ((N + 1) & ~1);
+    // MODE 2: |y_n| (float, exact) after the float metric (even offset)
+    const float *yabsT = reinterpret_cast<const float *>(Ebuf) + ((N + 1) & ~1);
+    if (FILT && split) {
+      float *ya = reinterpret_cast<float *>(Ebuf) + ((N + 1) & ~1);
       for (int n = tid; n < N; n += T)
-        aaf[n] = __double2float_rn(P.has_ay ? sAY[n]
-                                            : __dmul_rn(P.alpha, P.alias_y ? fabs((double)load_y<YT>(P, f, n))
-                                                                           : fabs((double)ybuf[n])));
+        ya[n] = fabsf((float)(P.alias_y ? load_y<YT>(P, f, n) : ybuf[n]));
     }
     if (P.alias_y || (FILT && split)) __syncthreads(); // amask / ybuf may overlay Ebuf (compact layout); MODE 2 tables
 
@@ -933,19 +968,19 @@ decode_kernel(const __grid_constant__ KParams P) {
           // filtered metric in float: sum + Cc G (coarse argmin correction) -
           // fl32(alpha |y|); the selection's band test covers every rounding
           float *Efl = reinterpret_cast<float *>(Ebuf);
-          const float *aaf = Efl + ((N + 1) & ~1);
+          const float alf = (float)P.alpha;
 #pragma unroll
           for (int qp = 0; qp < NP; ++qp) {
             const float2 h = f2unpack(hi[qp]);
             const int n = 2 * tid + 2 * T * qp;
             if (n + 1 < N) {
               const int2 cc = *reinterpret_cast<const int2 *>(sCorr + n);
-              const float2 aa = *reinterpret_cast<const float2 *>(aaf + n);
+              const float2 ya = *reinterpret_cast<const float2 *>(yabsT + n);
               *reinterpret_cast<float2 *>(Efl + n) =
-                  make_float2(__fsub_rn(__fmaf_rn((float)cc.x, Gf, h.x), aa.x),
-                              __fsub_rn(__fmaf_rn((float)cc.y, Gf, h.y), aa.y));
+                  make_float2(__fsub_rn(__fmaf_rn((float)cc.x, Gf, h.x), __fmul_rn(alf, ya.x)),
+                              __fsub_rn(__fmaf_rn((float)cc.y, Gf, h.y), __fmul_rn(alf, ya.y)));
             } else if (n < N) {
-              Efl[n] = __fsub_rn(__fmaf_rn((float)sCorr[n], Gf, h.x), aaf[n]);
+              Efl[n] = __fsub_rn(__fmaf_rn((float)sCorr[n], Gf, h.x), __fmul_rn(alf, yabsT[n]));
             }
           }
         } else if (WT <= 32) {
@@ -1188,14 +1223,16 @@ decode_kernel(const __grid_constant__ KParams P) {
             const double *c1 = chk1 + n, *c2 = chk2 + n;
             const uint32_t mk = amask[n * aw];
             const int w0 = W < 32 ? W : 32;
+            // MODE 2 keeps single records: wrap the check index instead
+            const int wrapN = FILT ? N : 0x7fffffff;
             for (int i = 0; i < w0; ++i) {
-              const int d = dn[i];
+              const int d = (n + dn[i] >= wrapN) ? dn[i] - N : dn[i];
               acc = __dadd_rn(acc, (((mk >> i) & 1u) ? c2 : c1)[d]);
             }
             if (W > 32) {
               const uint32_t mkh = amask[n * aw + 1];
               for (int i = 32; i < W; ++i) {
-                const int d = dn[i];
+                const int d = (n + dn[i] >= wrapN) ? dn[i] - N : dn[i];
                 acc = __dadd_rn(acc, (((mkh >> (i - 32)) & 1u) ? c2 : c1)[d]);
               }
             }
@@ -1270,7 +1307,7 @@ decode_kernel(const __grid_constant__ KParams P) {
                 for (int o = sub; o < lim; o += TPB) {
                   const int n = base + o;
                   if (Efl[n] >= fv - fd2)
-                    amax_combine(ve, ie, exact_split_metric<YT>(P, sFA, sA2, reinterpret_cast<const long long *>(sM2), sAY, ybuf, f, n, W, qexp), n);
+                    amax_combine(ve, ie, exact_split_metric(P, sFA, sA2, reinterpret_cast<const float *>(sM2), yabsT, n, W, qexp, qinv), n);
                 }
               for (int off = TPB >> 1; off; off >>= 1) {
                 const double v2 = __shfl_xor_sync(FULL_MASK, ve, off);
@@ -1363,7 +1400,7 @@ decode_kernel(const __grid_constant__ KParams P) {
                 int ie = 0x7fffffff;
                 for (int bb = lane; bb < nb; bb += 32)
                   if (blk_v[bb] >= thr)
-                    amax_combine(ve, ie, exact_split_metric<YT>(P, sFA, sA2, reinterpret_cast<const long long *>(sM2), sAY, ybuf, f, blk_i[bb], W, qexp),
+                    amax_combine(ve, ie, exact_split_metric(P, sFA, sA2, reinterpret_cast<const float *>(sM2), yabsT, blk_i[bb], W, qexp, qinv),
                                  blk_i[bb]);
                 warp_amax(ve, ie);
                 gi = ie;
@@ -1520,8 +1557,9 @@ decode_kernel(const __grid_constant__ KParams P) {
         asm("mov.b32 %0, %1;" : "=r"(A.fa2) : "r"(fa + 4u * (uint32_t)N));
         asm("mov.b32 %0, %1;" : "=r"(A.fb) : "r"(fb));
         asm("mov.b32 %0, %1;" : "=r"(A.fb2) : "r"(fb + 4u * (uint32_t)N));
-        if (FILT) // per-check Dc in the second half of sCorr
-          asm("mov.b32 %0, %1;" : "=r"(A.m2) : "r"(s0 + (uint32_t)P.off_corr + 4u * (uint32_t)(N + tid)));
+        A.invg = __float_as_uint(invGf);
+        if (FILT) // per-check min2 (float)
+          asm("mov.b32 %0, %1;" : "=r"(A.m2) : "r"(s0 + (uint32_t)P.off_m2s + 4u * (uint32_t)tid));
         else
           asm("mov.b32 %0, %1;" : "=r"(A.m2) : "r"(s0 + (uint32_t)P.off_m2s + 8u * (uint32_t)tid));
         asm("mov.b32 %0, %1;" : "=r"(A.a2) : "r"(s0 + (uint32_t)P.off_a2m + 2u * (uint32_t)tid));
@@ -1558,7 +1596,7 @@ decode_kernel(const __grid_constant__ KParams P) {
                 const double v2 = -chk2[m];
                 chk1[m] = v1;
                 chk2[m] = v2;
-                if (CIRC) { chk1[m + N] = v1; chk2[m + N] = v2; }
+                if (CIRC && !FILT) { chk1[m + N] = v1; chk2[m + N] = v2; }
               }
             }
             sprev ^= (tog ? 1u : 0u) << kk;
@@ -1578,7 +1616,7 @@ decode_kernel(const __grid_constant__ KParams P) {
             const double v2 = -chk2[m];
             chk1[m] = v1;
             chk2[m] = v2;
-            if (CIRC) { chk1[m + N] = v1; chk2[m + N] = v2; }
+            if (CIRC && !FILT) { chk1[m + N] = v1; chk2[m + N] = v2; }
             sprev ^= 1u << kk;
           }
           const uint32_t b = __ballot_sync(FULL_MASK, s);

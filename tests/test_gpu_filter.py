@@ -12,6 +12,7 @@ import pytest
 from oracle import wbf_oracle as O
 from oracle.c_oracle import COracle
 from paper_1206_3362_b200 import DecoderConfig, decode_batch
+from paper_1206_3362_b200 import _native as nat
 from paper_1206_3362_b200.decoders import device_code
 from tests.golden.codebook import build_code, code_rate
 
@@ -35,7 +36,11 @@ def _same(a, b, tag):
         u, v = getattr(a, name).cpu().numpy(), getattr(b, name).cpu().numpy()
         assert np.array_equal(u, v), f"{tag}: {name} differs at {np.nonzero(u != v)[0][:8]}"
     assert np.array_equal(a.z_bits.cpu().numpy(), b.z_bits.cpu().numpy()), f"{tag}: z differs"
-    assert np.array_equal(a.flags.cpu().numpy(), b.flags.cpu().numpy()), f"{tag}: flags differ"
+    # converged / stalled / non-finite must agree; the metric path bits may
+    # not (the filtered kernels run frames that fail the split-fp32 guard on
+    # the ordered path instead of the guarded fp64 one)
+    fa, fb = a.flags.cpu().numpy(), b.flags.cpu().numpy()
+    assert np.array_equal(fa & 11, fb & 11), f"{tag}: flags differ"
 
 
 def _oracle(h, y, cfg):
@@ -120,4 +125,6 @@ def test_filter_equals_exact_full_size(cuda_device, ebn0, p):
     a = decode_batch(h, y, cfg, "fwbf")
     b = decode_batch(h, y, cfg, "fwbf", force_ordered=NOFILTER)
     _same(a, b, f"full/{ebn0}/{p}")
-    assert np.array_equal(a.counters.cpu().numpy(), b.counters.cpu().numpy())
+    ca, cb = a.counters.cpu().numpy(), b.counters.cpu().numpy()
+    keep = [i for i in range(len(ca)) if i != nat.CNT_ORDERED_FRAMES]
+    assert np.array_equal(ca[keep], cb[keep])
