@@ -929,7 +929,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     } else
     for (;;) {
       const int swt = misc[S_SWT];
-      if (swt == 0 && !P.metric_out) { conv = 1; break; }
+      if (swt == 0 && (FILT || !P.metric_out)) { conv = 1; break; } // MODE 2 never has a stage view
       if (k >= P.kmax) break;
 
       // ---- Eq.(1) metric for every bit -> Ebuf ----
@@ -1246,7 +1246,7 @@ decode_kernel(const __grid_constant__ KParams P) {
       }
       __syncthreads();
       FWBF_PH(3)
-      if (P.metric_out) { // stage view (fwbf_metric_*): Eq.(1) on the initial state, then stop
+      if (!FILT && P.metric_out) { // stage view (fwbf_metric_*): Eq.(1) on the initial state, then stop
         for (int n = tid; n < N; n += T) P.metric_out[f * P.metric_ld + n] = Ebuf[n];
         break;
       }
@@ -1255,7 +1255,7 @@ decode_kernel(const __grid_constant__ KParams P) {
       if (tid == 0) misc[S_SWT] = 0; // every thread read it at the loop top (before the E barrier)
       int F = 0;
       bool applied = false;
-      if (P.alg == FWBF_ALG_FWBF) {
+      if (FILT || P.alg == FWBF_ALG_FWBF) { // MODE 2 is FWBF only
         // Groups of TPB = 2^log2_tpb threads own one p-block each: strided scan
         // (ascending per thread, strict >), butterfly argmax in the group, then
         // the group applies its flip when the block maximum is > 0
