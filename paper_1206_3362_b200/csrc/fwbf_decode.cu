@@ -1126,6 +1126,26 @@ decode_kernel(const __grid_constant__ KParams P) {
                 rowb[r] = r << qlz;
               }
               // two columns (o, o + 32) per step: independent fp64 chains
+              const bool full4 = jb == 4 && shv[0] >= 0 && shv[1] >= 0 && shv[2] >= 0 && shv[3] >= 0 &&
+                                 (lim & 63) == 0; // block-uniform
+              if (full4) { // every row block present, whole column pairs: no absent-block selects
+                for (int o = lane; o < lim; o += 64) {
+                  const int n0 = base + o, n1 = n0 + 32;
+                  const int oz0 = n0 & (Zq - 1), oz1 = n1 & (Zq - 1);
+                  double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+                  for (int r = 0; r < 4; ++r) {
+                    const int m0 = rowb[r] + ((oz0 - shv[r]) & (Zq - 1));
+                    const int m1 = rowb[r] + ((oz1 - shv[r]) & (Zq - 1));
+                    acc0 = __dadd_rn(acc0, ((amin[m0] == n0) ? chk2 : chk1)[m0]);
+                    acc1 = __dadd_rn(acc1, ((amin[m1] == n1) ? chk2 : chk1)[m1]);
+                  }
+                  const double e0 = __dsub_rn(acc0, __dmul_rn(P.alpha, fabs((double)ybuf[n0])));
+                  if (e0 > v) { v = e0; i = n0; }
+                  const double e1 = __dsub_rn(acc1, __dmul_rn(P.alpha, fabs((double)ybuf[n1])));
+                  if (e1 > v) { v = e1; i = n1; }
+                }
+              } else
               for (int o = lane; o < lim; o += 64) {
                 const int n0 = base + o, n1 = n0 + 32;
                 const bool two = o + 32 < lim;
