@@ -26,6 +26,14 @@
 // 32 | p (no metric buffer) and, in the INC kernels, IMWBF's incremental
 // integer metric.
 //
+// Kernel MODEs (template): 0 exact (the paths above, any algorithm); 1 IMWBF
+// incremental metric; 2 FWBF filtered metric -- frames passing the fp64 guard
+// sum the float32 minima directly (one FADD2 per column pair per check),
+// store the metric as float, and the selection re-decides every block whose
+// decision is within the frame's error bound of changing with exact column
+// sums.  MODE 2 also has its own, smaller shared-memory
+// layout (5 CTAs/SM on EG(1023)) with coarse integer argmin corrections.
+//
 // Ties: every argmax takes the lowest index (numpy argmax / stable argsort).
 
 #include <cuda_runtime.h>
