@@ -128,3 +128,21 @@ def test_filter_equals_exact_full_size(cuda_device, ebn0, p):
     ca, cb = a.counters.cpu().numpy(), b.counters.cpu().numpy()
     keep = [i for i in range(len(ca)) if i != nat.CNT_ORDERED_FRAMES]
     assert np.array_equal(ca[keep], cb[keep])
+
+
+@pytest.mark.parametrize("tiny", [3e-7, 1e-12, 1e-30])
+def test_fp64_guarded_frames_take_the_filtered_path(cuda_device, tiny):
+    # One tiny |y| per frame makes the quantum q tiny: the split-fp32 guard
+    # fails but the fp64 guard holds, so the MODE 2 kernel filters these frames
+    # too (its exact fallback only needs the fp64 guard); 1e-30 also leaves the
+    # quantum range of the coarse corrections, which sends frames to the
+    # ordered path.  Results must equal the oracle either way.
+    h, y = _frames("eg5", 3.5, 64, seed=21)
+    y[:, 100] = tiny
+    y[1::2, 600] = -tiny
+    cfg = DecoderConfig(block_len_p=31, k_max=60)
+    a = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+    b = decode_batch(h, y, cfg, "fwbf", flip_log=True, force_ordered=NOFILTER)
+    _same(a, b, f"tiny {tiny}")
+    assert a.flip_logs() == b.flip_logs()
+    _vs_oracle(a, h, y, cfg, f"tiny {tiny}")
