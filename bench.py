@@ -47,8 +47,11 @@ def parse():
     ap.add_argument("--kmax", type=int, default=100)
     ap.add_argument("--alpha", type=float, default=0.2)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--cpu-frames", type=int, default=2048,
-                    help="bounded CPU sample (frames) for cpu_baseline / --impl reference")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0,
+                    help="bounded CPU sample (seconds of work) for the cpu_baseline leg")
+    ap.add_argument("--ref-seconds", type=float, default=60.0,
+                    help="--impl reference: total timed CPU work over the K steps")
+    ap.add_argument("--ref-1worker-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunk", type=int, default=1 << 17)
@@ -111,65 +114,150 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------- CPU reference arm
+#
+# The reference decoder is pure Python + numpy (fwbf 0.1.0).  It is installed
+# unmodified into baseline/_ref (pip --target) and run
+# through its own public Monte Carlo entry point, harness.run_point
+# (/root/reference/pkg/src/fwbf/harness.py:118-173), on the bench workload:
+# same code, decoder, p, alpha, K_max and Eb/N0, the reference's own channel
+# (float64 y), `workers` = all host cores, target_word_errors huge so the run
+# is a fixed number of frames.  The code is built once, outside the timed
+# region; the rate is passed so run_point skips its GF(2) rank.  If
+# baseline/_ref is missing, the oracle port (oracle/wbf_oracle.py) stands in
+# and `kind` says "port".
 
-def _cpu_worker(args):
+def _host_cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def _ref_fwbf():
+    """The installed reference package (baseline/_ref), or None."""
+    path = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "fwbf")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import fwbf  # noqa: F401
+    except Exception:
+        return None
+    if not os.path.abspath(fwbf.__file__).startswith(path):
+        return None
+    return fwbf
+
+
+class CpuArm:
+    """The reference's own run_point (or the oracle port) on this host's cores."""
+
+    def __init__(self, a, workers: int):
+        self.a, self.workers = a, workers
+        self.k = K_INFO[a.code]
+        self.fw = _ref_fwbf()
+        from tests.golden.codebook import build_code
+        if self.fw is not None:
+            self.kind = "reference"
+            if a.code == "eg5":
+                self.h = self.fw.eg_ldpc_construct(5)          # the reference's own constructor
+            else:
+                hh = build_code(a.code)
+                self.h = self.fw.ParityCheckMatrix(hh.row_adj, hh.n_cols)
+        else:
+            self.kind = "port"
+            self.h = build_code(a.code)
+
+    def run(self, frames: int):
+        """Decode `frames` frames; returns (frames, seconds, mean iterations)."""
+        a = self.a
+        if self.fw is not None:
+            fw = self.fw
+            cfg = fw.DecoderConfig(alpha=a.alpha, k_max=a.kmax, block_len_p=a.p)
+            ec = fw.ExperimentConfig(h=self.h, decoder="fwbf", decoder_cfg=cfg, ebn0_db=(a.ebn0,),
+                                     rate=self.k / self.h.n_cols, target_word_errors=1 << 62,
+                                     max_frames=frames, master_seed=a.seed, workers=self.workers)
+            t0 = time.perf_counter()
+            st = fw.run_point(ec, a.ebn0)
+            return st.frames, time.perf_counter() - t0, st.mean_iters
+        return port_decode_rate(a, frames, self.workers)
+
+    def calibrated_frames(self, seconds: float) -> int:
+        """Frames for about `seconds` of work (whole 128-frame batches per worker)."""
+        unit = 128 * self.workers
+        n, dt, _ = self.run(unit)
+        fps = n / max(dt, 1e-6)
+        return max(unit, int(fps * seconds / unit + 0.5) * unit)
+
+    def sample_text(self, frames: int) -> str:
+        a = self.a
+        if self.kind == "reference":
+            return (f"{frames} frames per run of the bench workload through the installed reference's own "
+                    f"fwbf.harness.run_point (baseline/_ref, unmodified; reference channel, float64 y), "
+                    f"workers={self.workers}")
+        return (f"{frames} seeded frames of the bench workload through oracle/wbf_oracle.py (numpy "
+                f"restatement of the reference decode loop), {self.workers}-process pool")
+
+
+def _port_worker(args):
     code, ebn0, p, kmax, alpha, seed, start, count = args
     import numpy as np
     from oracle import wbf_oracle as O
     from tests.golden.codebook import build_code, code_rate
     g = O.Graph.of(build_code(code))
     sigma = O.ebn0_to_sigma(ebn0, code_rate(code))
-    rng = np.random.default_rng([seed, start])
-    y = (1.0 + sigma * rng.standard_normal((count, g.n))).astype(np.float32)
     its = 0
-    for i in range(count):
-        its += O.decode(g, y[i], "fwbf", alpha=alpha, k_max=kmax, p=p).iterations
+    for i in range(start, start + count):
+        y = O.channel_frame(np.zeros(g.n, np.uint8), sigma, seed, i)
+        its += O.decode(g, y, "fwbf", alpha=alpha, k_max=kmax, p=p).iterations
     return count, its
 
 
-def cpu_decode_rate(a, frames: int, cores: int):
-    """Oracle port (the reference's numpy decode loop) over `frames` seeded frames."""
+def port_decode_rate(a, frames: int, cores: int):
+    """Fallback when baseline/_ref is absent: the oracle port over `frames` frames."""
     from multiprocessing import get_context
-    chunk = max(1, frames // (cores * 4))
-    jobs = [(a.code, a.ebn0, a.p, a.kmax, a.alpha, a.seed + 7, s, min(chunk, frames - s))
+    chunk = 128
+    jobs = [(a.code, a.ebn0, a.p, a.kmax, a.alpha, a.seed, s, min(chunk, frames - s))
             for s in range(0, frames, chunk)]
     t0 = time.perf_counter()
     if cores == 1:
-        res = [_cpu_worker(j) for j in jobs]
+        res = [_port_worker(j) for j in jobs]
     else:
         with get_context("fork").Pool(cores) as pool:
-            res = pool.map(_cpu_worker, jobs)
+            res = pool.map(_port_worker, jobs)
     dt = time.perf_counter() - t0
     n = sum(r[0] for r in res)
-    its = sum(r[1] for r in res)
-    return n, dt, its / max(1, n)
+    return n, dt, sum(r[1] for r in res) / max(1, n)
 
 
 def run_reference(a, rank: int):
+    """--impl reference: rank 0 times the reference CPU decoder; other ranks exit."""
     if rank != 0:
         return
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    k = K_INFO[a.code]
-    frames = a.cpu_frames
-    for _ in range(a.warmup and 1):
-        cpu_decode_rate(a, max(cores, 64), cores)
-    times, its = [], []
+    cores = _host_cores()
+    arm = CpuArm(a, cores)
+    # per-step sample: the whole timed run takes about ref_seconds (>= 30 s of
+    # work), split over the K steps in whole batches per worker
+    step_s = max(2.0, a.ref_seconds / max(1, a.steps))
+    frames = arm.calibrated_frames(step_s)   # also the warm-up (pool start, imports)
+    times, its, nfr = [], [], 0
     for _ in range(a.steps):
-        n, dt, mi = cpu_decode_rate(a, frames, cores)
+        n, dt, mi = arm.run(frames)
         times.append(dt)
         its.append(mi)
+        nfr += n
     t = sum(times)
-    value = frames * a.steps * k / t / 1e9
+    value = nfr * arm.k / t / 1e9
+    one = CpuArm(a, 1)
+    f1 = one.calibrated_frames(a.ref_1worker_seconds)
+    n1, dt1, _ = one.run(f1)
     line = {
         "impl": "reference", "metric": "FWBF decoded info Gbit/s", "value": value, "unit": "Gbit/s",
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": 1e3 * t / a.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference channel, seeded)",
         "config": config_dict(a, mean_iters=statistics.mean(its)),
-        "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": cores, "kind": "port",
-                         "sample": f"{frames} seeded frames per step of the bench workload, "
-                                   f"oracle/wbf_oracle.py (numpy restatement of the reference "
-                                   f"decode loop) on a {cores}-process pool"},
+        "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": cores, "kind": arm.kind,
+                         "sample": arm.sample_text(frames) + f"; {a.steps} runs, {t:.1f} s timed in total"},
+        "cpu_1worker": {"value": n1 * arm.k / dt1 / 1e9, "unit": "Gbit/s", "cores": 1, "frames": n1,
+                        "seconds": dt1},
         "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -233,14 +321,17 @@ def main():
                       flips_total=torch.zeros(B, dtype=torch.int32, device=dev),
                       bit_errors=torch.zeros(B, dtype=torch.int32, device=dev),
                       counters=torch.zeros(nat.NCOUNTERS, dtype=torch.int64, device=dev))
+    res.iter_hist = torch.zeros(a.kmax + 1, dtype=torch.int64, device=dev)
     out = _outputs(res)
     stream = torch.cuda.current_stream(dev)
 
     def step():
         res.counters.zero_()
+        res.iter_hist.zero_()
         nat.check(L.fwbf_decode_f32(dc.handle, C.byref(prm), C.c_void_p(y.data_ptr()), B, ld,
                                     C.byref(out), C.c_void_p(stream.cuda_stream)), "decode")
         reduce_counters(res.counters)
+        reduce_counters(res.iter_hist)
 
     for _ in range(a.warmup):
         step()
@@ -350,41 +441,47 @@ def main():
                                   fer=float(cnt[nat.CNT_WORD_ERRORS] / frames_all),
                                   ber=float(cnt[nat.CNT_BIT_ERRORS] / (frames_all * n)),
                                   ordered_path_frames=int(cnt[nat.CNT_ORDERED_FRAMES]),
+                                  iter_hist=[int(v) for v in res.iter_hist.cpu().tolist()],
                                   frames_per_s=world * B / (ms_step / 1e3)),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "bytes_per_frame": bytes_frame,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
-                         "binding": {
-                             "resource": "shared memory: filtered metric gather (one 8-byte LDS + one "
-                                         "FADD2 per two edge visits; 4 B/edge at 128 B/clk/SM = 32 edge "
-                                         "visits/clk/SM)",
-                             "filter_exact_block_decisions": fstats[0],
-                             "filter_exact_fraction": fstats[0] / max(1.0, block_decisions),
-                             "filter_exact_stall_argmaxes": fstats[1],
-                             "edge_visits_per_frame": edges * (1.0 + mean_iters),
-                             "edge_visits_per_s": ev_rate,
-                             "gather_bound_per_s": gather_bound,
-                             "frac": ev_rate / gather_bound,
+            # The binding roofline: the path is issue-bound, not
+            # HBM-bound.  achieved = edge visits E (1 + I) per frame x frames/s
+            # over the decode launches (CUDA events on the launch stream);
+            # peak = one fp64 add per lane per clock = SMs x 64 x clock.  The
+            # ncu issue-slot and shared-pipe utilisations of the same kernel
+            # (profiles/roofline_traffic.json) ride along; HBM is a sub-record.
+            "roofline": {"bound": "issue", "resource": "fp64-lane edge visits (one add per lane per clock)",
+                         "achieved": ev_rate, "peak": dadd_peak, "unit": "edge-visits/s",
+                         "frac": ev_rate / dadd_peak,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "edge_visits_per_frame": edges * (1.0 + mean_iters),
+                         "ncu_issue_active_pct": trf.get("ncu_issue_active_pct"),
+                         "ncu_smem_pipe_pct": trf.get("ncu_smem_pipe_pct"),
+                         "ncu_source": trf.get("ncu_source"),
+                         "clock_mhz_for_peaks": max_mhz,
+                         "gather_bound": {
+                             "resource": "shared memory: filtered metric gather (one 8-byte LDS + one FADD2 "
+                                         "per two edge visits; 4 B/edge at 128 B/clk/SM = 32 edge visits/clk/SM)",
+                             "peak": gather_bound, "frac": ev_rate / gather_bound,
                              "smem_bytes_per_s_at_4B_per_edge": 4 * ev_rate,
-                             "smem_peak_GBps": smem_peak / 1e9,
-                             "dadd_peak_per_s": dadd_peak,
-                             "frac_of_fp64_lane_peak": ev_rate / dadd_peak,
-                             "ncu_issue_active_pct": trf.get("ncu_issue_active_pct"),
-                             "ncu_smem_pipe_pct": trf.get("ncu_smem_pipe_pct"),
-                             "ncu_source": trf.get("ncu_source"),
-                             "clock_mhz_for_peaks": max_mhz}},
+                             "smem_peak_GBps": smem_peak / 1e9},
+                         "filter": {"exact_block_decisions": fstats[0],
+                                    "exact_fraction": fstats[0] / max(1.0, block_decisions),
+                                    "exact_stall_argmaxes": fstats[1]},
+                         "hbm": {"achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                                 "frac": achieved / hbm_peak, "bytes_per_frame": bytes_frame,
+                                 "traffic": traffic,
+                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}},
             "e2e": e2e,
             "gpu_launches": a.steps * 1,
             "clocks": csum,
         }
         if not a.no_cpu_baseline and world == 1:
-            cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-            nf, dt, _ = cpu_decode_rate(a, a.cpu_frames, cores)
-            line["cpu_baseline"] = {
-                "value": nf * kinfo / dt / 1e9, "unit": "Gbit/s", "cores": cores, "kind": "port",
-                "sample": f"{nf} seeded frames of the same workload through oracle/wbf_oracle.py "
-                          f"(numpy restatement of the reference decode loop), {cores}-process pool"}
+            cores = _host_cores()
+            arm = CpuArm(a, cores)
+            nf0 = arm.calibrated_frames(a.cpu_seconds)
+            nf, dt, _ = arm.run(nf0)
+            line["cpu_baseline"] = {"value": nf * kinfo / dt / 1e9, "unit": "Gbit/s", "cores": cores,
+                                    "kind": arm.kind, "sample": arm.sample_text(nf) + f", {dt:.1f} s"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

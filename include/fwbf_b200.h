@@ -180,6 +180,51 @@ int fwbf_decode_host_f32(fwbf_code *code, const fwbf_params *params, const float
                          int32_t *iterations_host, uint8_t *flags_host,
                          int64_t *counters_host, int64_t chunk_frames);
 
+/* ---- Stage views (fwbf_stage.cu): the reference's stage functions one at a
+ * time, batched over B frames, float64 like the reference, device memory.
+ * The decode kernels fuse all of them; these serve the stage-level API and
+ * its parity tests. ---- */
+
+/* hard_decision (decoders.py:106-108): z[i] = y[i] < 0; dtype 4 = float32,
+ * 8 = float64; count elements. */
+int fwbf_stage_hard_decision(int32_t dtype, const void *y, int64_t count, uint8_t *z, void *stream);
+
+/* ParityCheckMatrix.syndrome (matrix.py:72-79): z [B][n] uint8 -> s [B][m]. */
+int fwbf_stage_syndrome(fwbf_code *code, const uint8_t *z, int64_t batch, uint8_t *syndrome, void *stream);
+
+/* compute_weights + WeightTable.edge_weights (decoders.py:80-103): per check
+ * min1, min2 (float64) and argmin_col (int64, first occurrence), [B][m];
+ * edge_w [B][n_edges] in row-major edge order (nullable).  Fails with
+ * FWBF_EINVAL when a check has fewer than 2 bits, like the reference. */
+int fwbf_stage_weights(fwbf_code *code, const double *y, int64_t batch, int64_t ld, double *min1,
+                       double *min2, int64_t *argmin_col, double *edge_w, void *stream);
+
+/* WeightTable.edge_weights (decoders.py:80-84) of a given table [B][m] ->
+ * edge_w [B][n_edges] in row-major edge order. */
+int fwbf_stage_edge_weights(fwbf_code *code, const double *min1, const double *min2,
+                            const int64_t *argmin_col, int64_t batch, double *edge_w, void *stream);
+
+/* all_metrics (decoders.py:148-153): syndrome [B][m] uint8, edge_w [B][n_edges],
+ * abs_y [B][n] -> out [B][n] = fl(sum in ascending check order) - fl(alpha|y|). */
+int fwbf_stage_all_metrics(fwbf_code *code, const uint8_t *syndrome, const double *edge_w,
+                           const double *abs_y, double alpha, int64_t batch, double *out, void *stream);
+
+/* block_argmax (decoders.py:156-167): values [B][ld], first maximum of each
+ * p-block (tail padded with -inf) -> out [B][ceil(n/p)] int64. */
+int fwbf_stage_block_argmax(const double *values, int64_t batch, int64_t n, int64_t ld, int32_t p,
+                            int64_t *out, void *stream);
+
+/* bit_metric (decoders.py:138-145) for columns cols[0..k) of one state. */
+int fwbf_stage_bit_metric(fwbf_code *code, const int32_t *cols, int32_t k, const uint8_t *syndrome,
+                          const double *min1, const double *min2, const int64_t *argmin_col,
+                          const double *y, double alpha, double *out, void *stream);
+
+/* The reference channel without a decode (frame_rng + transmit,
+ * channel.py:29-82): y[f][n] for frames first..first+count-1, noise_mode as
+ * for fwbf_decode_awgn (y is double* for NUMPY_F64, float* for NUMPY_F32). */
+int fwbf_channel_awgn(fwbf_code *code, uint64_t seed, int64_t first_frame, int64_t count, double sigma,
+                      const uint32_t *codeword_bits, int32_t noise_mode, void *y, int64_t ld, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,9 @@ NOISE_NUMPY_F64, NOISE_NUMPY_F32 = 0, 1
 EXPORTS = ("fwbf_abi_version", "fwbf_last_error", "fwbf_device_count", "fwbf_code_create",
            "fwbf_code_destroy", "fwbf_code_info", "fwbf_max_flips_per_iter", "fwbf_decode_f32",
            "fwbf_decode_f64", "fwbf_decode_awgn", "fwbf_decode_host_f32", "fwbf_metric_f32",
-           "fwbf_metric_f64", "fwbf_filter_stats")
+           "fwbf_metric_f64", "fwbf_filter_stats", "fwbf_stage_hard_decision", "fwbf_stage_syndrome",
+           "fwbf_stage_weights", "fwbf_stage_edge_weights", "fwbf_stage_all_metrics", "fwbf_stage_block_argmax",
+           "fwbf_stage_bit_metric", "fwbf_channel_awgn")
 
 
 class CodeDesc(C.Structure):
@@ -92,6 +94,15 @@ def lib() -> C.CDLL:
                                           vp, vp]
             L.fwbf_metric_f64.argtypes = L.fwbf_metric_f32.argtypes
             L.fwbf_filter_stats.argtypes = [vp, C.POINTER(C.c_int64), C.c_int32]
+            i64, i32, dbl = C.c_int64, C.c_int32, C.c_double
+            L.fwbf_stage_hard_decision.argtypes = [i32, vp, i64, vp, vp]
+            L.fwbf_stage_syndrome.argtypes = [vp, vp, i64, vp, vp]
+            L.fwbf_stage_weights.argtypes = [vp, vp, i64, i64, vp, vp, vp, vp, vp]
+            L.fwbf_stage_edge_weights.argtypes = [vp, vp, vp, vp, i64, vp, vp]
+            L.fwbf_stage_all_metrics.argtypes = [vp, vp, vp, vp, dbl, i64, vp, vp]
+            L.fwbf_stage_block_argmax.argtypes = [vp, i64, i64, i64, i32, vp, vp]
+            L.fwbf_stage_bit_metric.argtypes = [vp, vp, i32, vp, vp, vp, vp, vp, dbl, vp, vp]
+            L.fwbf_channel_awgn.argtypes = [vp, C.c_uint64, i64, i64, dbl, vp, i32, vp, i64, vp]
             for f in EXPORTS:
                 if f not in ("fwbf_abi_version", "fwbf_last_error", "fwbf_device_count",
                              "fwbf_max_flips_per_iter"):

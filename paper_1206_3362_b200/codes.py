@@ -26,7 +26,8 @@ import numpy as np
 __all__ = [
     "ParityCheckMatrix", "CodeStructure", "detect_structure", "eg_ldpc",
     "qc_ldpc", "gallager_rc", "gf2_rank", "validate_rc", "code_dimension",
-    "write_alist", "read_alist", "AlistError",
+    "write_alist", "read_alist", "AlistError", "AlistFormatError", "AlistRangeError",
+    "AlistMismatchError", "CodeSpec", "code_spec", "RcReport",
 ]
 
 
@@ -83,6 +84,17 @@ class ParityCheckMatrix:
     @property
     def n_edges(self) -> int:
         return int(self.edge_col.size)
+
+    @property
+    def row_pad(self) -> np.ndarray:
+        """[M, max row weight] column indices padded with the sentinel N (matrix.py:53-58)."""
+        pad = np.full((self.n_rows, self.max_row_weight), self.n_cols, dtype=np.int64)
+        for m, arr in enumerate(self.row_adj):
+            pad[m, :arr.size] = arr
+        return pad
+
+    def transpose(self) -> "ParityCheckMatrix":
+        return ParityCheckMatrix(self.col_adj, self.n_rows)
 
     def syndrome(self, z) -> np.ndarray:
         """z H^T over GF(2) (reference `matrix.py:72-79`)."""
@@ -359,22 +371,84 @@ def code_dimension(h: ParityCheckMatrix) -> int:
     return h.n_cols - gf2_rank(h)
 
 
-def validate_rc(h: ParityCheckMatrix) -> bool:
-    """True iff no two rows (equivalently no two columns) share two positions."""
-    seen = set()
-    for adj in h.row_adj:
-        a = adj.tolist()
-        for i in range(len(a)):
-            for j in range(i + 1, len(a)):
-                key = a[i] * h.n_cols + a[j]
-                if key in seen:
-                    return False
-                seen.add(key)
-    return True
+@dataclass(frozen=True)
+class CodeSpec:
+    """Block length, dimension, rate and (regular) weights of H (matrix.py:96-105)."""
+
+    n: int
+    k: int
+    rate: float
+    row_weight: Optional[int]  # None: irregular
+    col_weight: Optional[int]
+
+
+def code_spec(h: ParityCheckMatrix) -> CodeSpec:
+    """(n, k = n - rank_GF2(H), k/n, weights) -- matrix.py:127-134; a degenerate
+    code (k = 0 or k = n) raises ValueError."""
+    k = code_dimension(h)
+    if k <= 0 or k >= h.n_cols:
+        raise ValueError(f"degenerate code: n={h.n_cols}, k={k}")
+    rws, cws = np.unique(h.row_weights), np.unique(h.col_weights)
+    return CodeSpec(n=h.n_cols, k=k, rate=k / h.n_cols,
+                    row_weight=int(rws[0]) if rws.size == 1 else None,
+                    col_weight=int(cws[0]) if cws.size == 1 else None)
+
+
+@dataclass(frozen=True)
+class RcReport:
+    """Row-column constraint check (matrix.py:137-143): ``ok`` plus the
+    lexicographically smallest pair of rows and of columns that share two or
+    more positions.  Truthy iff ok."""
+
+    ok: bool
+    row_pair: Optional[tuple]
+    col_pair: Optional[tuple]
+
+    def __bool__(self) -> bool:
+        return bool(self.ok)
+
+
+def _smallest_shared_pair(lists: Sequence[np.ndarray], universe: int) -> Optional[tuple]:
+    """Smallest (a, b), a < b, of items co-occurring in two or more of `lists`
+    (each sorted): every list contributes its item pairs a * universe + b; a
+    duplicated key is a pair seen twice."""
+    keys = []
+    for lst in lists:
+        lst = np.asarray(lst, dtype=np.int64)
+        if lst.size > 1:
+            a, b = np.triu_indices(lst.size, 1)
+            keys.append(lst[a] * universe + lst[b])
+    if not keys:
+        return None
+    k = np.sort(np.concatenate(keys))
+    dup = k[1:][k[1:] == k[:-1]]
+    if dup.size == 0:
+        return None
+    first = int(dup[0])
+    return (first // universe, first % universe)
+
+
+def validate_rc(h: ParityCheckMatrix) -> RcReport:
+    """No two rows, and no two columns, share more than one position."""
+    rows = _smallest_shared_pair(h.col_adj, h.n_rows)   # rows co-occurring in two columns
+    cols = _smallest_shared_pair(h.row_adj, h.n_cols)   # columns co-occurring in two rows
+    return RcReport(ok=rows is None and cols is None, row_pair=rows, col_pair=cols)
 
 
 class AlistError(ValueError):
-    pass
+    """An alist file could not be parsed (alist.py:19-20)."""
+
+
+class AlistFormatError(AlistError):
+    """Bad tokens, line counts or weights (alist.py:23-24)."""
+
+
+class AlistRangeError(AlistError):
+    """An index outside [1, M] or [1, N] (alist.py:27-28)."""
+
+
+class AlistMismatchError(AlistError):
+    """Column-side and row-side lists disagree (alist.py:31-32)."""
 
 
 def write_alist(h: ParityCheckMatrix, path: str | os.PathLike) -> None:
@@ -389,35 +463,74 @@ def write_alist(h: ParityCheckMatrix, path: str | os.PathLike) -> None:
             f.write(" ".join(str(int(v) + 1) for v in adj) + "\n")
 
 
-def read_alist(path: str | os.PathLike) -> ParityCheckMatrix:
-    """Parse an alist file; zero padding is ignored, the two views must agree."""
-    with open(path, "r", encoding="ascii") as f:
-        lines = [ln.split() for ln in f.read().splitlines()]
-    while lines and not lines[-1]:
-        lines.pop()
+def _alist_ints(line: str, lineno: int) -> List[int]:
     try:
-        n, m = map(int, lines[0])
-        col_w = list(map(int, lines[2]))
-        row_w = list(map(int, lines[3]))
-        col_lists = [[int(t) for t in ln if int(t) != 0] for ln in lines[4:4 + n]]
-        row_lists = [[int(t) for t in ln if int(t) != 0] for ln in lines[4 + n:4 + n + m]]
-    except (ValueError, IndexError) as exc:
-        raise AlistError(f"malformed alist: {exc}") from None
-    if len(col_lists) != n or len(row_lists) != m or len(col_w) != n or len(row_w) != m:
-        raise AlistError("line counts disagree with the header")
-    rows = [[v - 1 for v in r] for r in row_lists]
-    for r, w in zip(rows, row_w):
-        if len(r) != w or any(not 0 <= v < n for v in r):
-            raise AlistError("row list disagrees with its weight or range")
-    from_cols = [set() for _ in range(m)]
-    for c, lst in enumerate(col_lists):
-        if len(lst) != col_w[c]:
-            raise AlistError("column list disagrees with its weight")
-        for v in lst:
-            if not 1 <= v <= m:
-                raise AlistError("row index out of range")
-            from_cols[v - 1].add(c)
+        return [int(t) for t in line.split()]
+    except ValueError:
+        bad = next(t for t in line.split() if not t.lstrip("+-").isdigit())
+        raise AlistFormatError(f"line {lineno}: non-integer token {bad!r}") from None
+
+
+def _alist_lists(lines: Sequence[str], lineno0: int, weights: Sequence[int], wmax: int, bound: int,
+                 what: str) -> List[List[int]]:
+    """One 1-based index list per line, zero padding dropped; checked against the
+    declared weights and range (alist.py:57-78)."""
+    out = []
+    for i, line in enumerate(lines):
+        ln = lineno0 + i
+        toks = _alist_ints(line, ln)
+        if len(toks) > wmax:
+            raise AlistFormatError(f"line {ln}: {what} {i} lists more than max weight {wmax} entries")
+        vals = [v for v in toks if v]
+        if len(vals) != weights[i]:
+            raise AlistFormatError(f"line {ln}: {what} {i} declares weight {weights[i]} "
+                                   f"but lists {len(vals)} indices")
+        for v in vals:
+            if v < 1 or v > bound:
+                raise AlistRangeError(f"line {ln}: index {v} out of range [1, {bound}]")
+        if len(set(vals)) != len(vals):
+            raise AlistFormatError(f"line {ln}: {what} {i} has duplicate indices")
+        out.append(sorted(v - 1 for v in vals))
+    return out
+
+
+def read_alist(path: str | os.PathLike) -> ParityCheckMatrix:
+    """Parse an alist file (alist.py:81-128): header, weights, then the column
+    and row lists; every failure is an AlistError subclass (a ValueError)."""
+    with open(path, "r", encoding="ascii") as f:
+        lines = f.read().split("\n")
+    while lines and not lines[-1].strip():
+        lines.pop()
+    if len(lines) < 4:
+        raise AlistFormatError("file has fewer than 4 header lines")
+    head = _alist_ints(lines[0], 1)
+    if len(head) != 2:
+        raise AlistFormatError("line 1: expected 'N M'")
+    n, m = head
+    if n < 1 or m < 1:
+        raise AlistFormatError(f"line 1: non-positive dimensions {n} x {m}")
+    mx = _alist_ints(lines[1], 2)
+    if len(mx) != 2:
+        raise AlistFormatError("line 2: expected 'max_col_weight max_row_weight'")
+    cw, rw = _alist_ints(lines[2], 3), _alist_ints(lines[3], 4)
+    if len(cw) != n:
+        raise AlistFormatError(f"line 3: expected {n} column weights, got {len(cw)}")
+    if len(rw) != m:
+        raise AlistFormatError(f"line 4: expected {m} row weights, got {len(rw)}")
+    if min(cw) < 0 or max(cw) > mx[0]:
+        raise AlistFormatError("line 3: a column weight exceeds the declared maximum")
+    if min(rw) < 0 or max(rw) > mx[1]:
+        raise AlistFormatError("line 4: a row weight exceeds the declared maximum")
+    if len(lines) != 4 + n + m:
+        raise AlistFormatError(f"expected {4 + n + m} lines, got {len(lines)}")
+    col_lists = _alist_lists(lines[4:4 + n], 5, cw, mx[0], m, "column")
+    row_lists = _alist_lists(lines[4 + n:], 5 + n, rw, mx[1], n, "row")
+    seen = [[] for _ in range(m)]
+    for col, rows in enumerate(col_lists):
+        for r in rows:
+            seen[r].append(col)
     for r in range(m):
-        if from_cols[r] != set(rows[r]):
-            raise AlistError(f"row {r}: column and row views disagree")
-    return ParityCheckMatrix(rows, n)
+        if seen[r] != row_lists[r]:  # both ascending
+            raise AlistMismatchError(f"row {r}: column-side adjacency {seen[r]} "
+                                     f"!= row-side adjacency {row_lists[r]}")
+    return ParityCheckMatrix(row_lists, n)

@@ -26,6 +26,17 @@ __global__ void decode_kernel(const __grid_constant__ KParams P);
 template <typename YT>
 __global__ void noise_kernel(unsigned long long seed, long long first, long long count, double sigma,
                              const uint32_t *codeword, YT *y, long long ld, int n, int pm);
+template <typename T> __global__ void stage_hard_decision(const T *, long long, uint8_t *);
+__global__ void stage_syndrome(const int *, const int *, int, int, const uint8_t *, long long, uint8_t *);
+__global__ void stage_weights(const int *, const int *, int, long long, const double *, long long, long long,
+                              double *, double *, long long *, double *);
+__global__ void stage_edge_weights(const int *, const int *, int, long long, const double *, const double *,
+                                   const long long *, long long, double *);
+__global__ void stage_all_metrics(const int *, const int *, const int *, int, int, long long, const uint8_t *,
+                                  const double *, const double *, double, long long, double *);
+__global__ void stage_block_argmax(const double *, long long, int, long long, int, int, long long *);
+__global__ void stage_bit_metric(const int *, const int *, const int *, int, const uint8_t *, const double *,
+                                 const double *, const long long *, const double *, double, double *);
 template <typename YT>
 __global__ void noise_kernel_warp(unsigned long long seed, long long first, long long count, double sigma,
                                   const uint32_t *codeword, YT *y, long long ld, int n);
@@ -51,6 +62,18 @@ static int fail(int code, const char *fmt, ...) {
     if (e_ != cudaSuccess) return fail(FWBF_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
   } while (0)
 
+// Every C entry point that selects its handle's device restores the caller's
+// current device on every exit path (the caller's CUDA context is not ours).
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&prev) != cudaSuccess) { cudaGetLastError(); prev = -1; }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 struct fwbf_code {
   int device = 0;
   int n = 0, m = 0;
@@ -61,6 +84,7 @@ struct fwbf_code {
   int dneg[fwbf::kMaxCircWeight] = {0};
   unsigned char jii[fwbf::kMaxCircWeight] = {0};
   int *d_row_ptr = nullptr, *d_row_idx = nullptr, *d_col_ptr = nullptr, *d_col_idx = nullptr;
+  int *d_col_eid = nullptr; // row-major edge index per CSC entry (stage kernels)
   uint8_t *d_i0tab = nullptr;
   uint8_t *d_jwtab = nullptr;
   int16_t *d_offpos = nullptr;
@@ -144,13 +168,18 @@ extern "C" int fwbf_code_create(const fwbf_code_desc *desc, int device, fwbf_cod
   }
   const long long E = row_ptr[m];
   // CSC with ascending checks per column (matrix.py:38-42 builds col_adj row by row).
-  std::vector<int> col_ptr(n + 1, 0), col_idx(E);
+  // col_eid: the row-major edge index of each CSC entry (the reference's edge
+  // order, matrix.py:49-52), for the stage kernels' edge-weight vectors.
+  std::vector<int> col_ptr(n + 1, 0), col_idx(E), col_eid(E);
   for (long long e = 0; e < E; ++e) col_ptr[row_idx[e] + 1]++;
   for (int i = 0; i < n; ++i) col_ptr[i + 1] += col_ptr[i];
   {
     std::vector<int> fill(col_ptr.begin(), col_ptr.end() - 1);
     for (int i = 0; i < m; ++i)
-      for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) col_idx[fill[row_idx[e]]++] = i;
+      for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+        col_eid[fill[row_idx[e]]] = e;
+        col_idx[fill[row_idx[e]]++] = i;
+      }
   }
   fwbf_code *c = new fwbf_code();
   c->device = device;
@@ -224,10 +253,12 @@ extern "C" int fwbf_code_create(const fwbf_code_desc *desc, int device, fwbf_cod
     }
   }
   int rc;
+  DeviceGuard dg;
   cudaError_t ce = cudaSetDevice(device);
   if (ce != cudaSuccess) { delete c; return fail(FWBF_ECUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(ce)); }
   if ((rc = upload(&c->d_row_ptr, row_ptr)) || (rc = upload(&c->d_row_idx, row_idx)) ||
       (rc = upload(&c->d_col_ptr, col_ptr)) || (rc = upload(&c->d_col_idx, col_idx)) ||
+      (rc = upload(&c->d_col_eid, col_eid)) ||
       (rc = upload(&c->d_i0tab, i0tab)) || (rc = upload(&c->d_jwtab, jwtab)) || (rc = upload(&c->d_offpos, offpos))) {
     fwbf_code_destroy(c);
     return rc;
@@ -245,11 +276,13 @@ extern "C" int fwbf_code_create(const fwbf_code_desc *desc, int device, fwbf_cod
 
 extern "C" int fwbf_code_destroy(fwbf_code *c) {
   if (!c) return FWBF_OK;
+  DeviceGuard dg;
   cudaSetDevice(c->device);
   cudaFree(c->d_row_ptr);
   cudaFree(c->d_row_idx);
   cudaFree(c->d_col_ptr);
   cudaFree(c->d_col_idx);
+  cudaFree(c->d_col_eid);
   cudaFree(c->d_i0tab);
   cudaFree(c->d_jwtab);
   cudaFree(c->d_offpos);
@@ -407,6 +440,41 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
   P.smem_bytes = o;
 }
 
+// Launch-plan cache: the dynamic shared-memory attribute and the occupancy of
+// a (device, kernel, threads, smem) shape are queried once, not per launch
+// (small batches would otherwise pay two driver calls per decode).
+struct PlanKey {
+  int device;
+  const void *kern;
+  int threads, smem;
+  bool operator==(const PlanKey &o) const {
+    return device == o.device && kern == o.kern && threads == o.threads && smem == o.smem;
+  }
+};
+
+static int plan_occupancy(int device, const void *kern, int threads, int smem, int *per_sm) {
+  static std::mutex mu;
+  static std::vector<std::pair<PlanKey, int>> plans;
+  static std::vector<std::pair<std::pair<int, const void *>, int>> attr; // (device, kern) -> smem attribute set
+  const PlanKey key{device, kern, threads, smem};
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto &pl : plans)
+    if (pl.first == key) { *per_sm = pl.second; return FWBF_OK; }
+  int *have = nullptr;
+  for (auto &a : attr)
+    if (a.first.first == device && a.first.second == kern) have = &a.second;
+  if (!have || *have < smem) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (have) *have = smem;
+    else attr.push_back({{device, kern}, smem});
+  }
+  int occ = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+  plans.push_back({key, occ});
+  *per_sm = occ;
+  return FWBF_OK;
+}
+
 template <typename YT>
 static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long long batch,
                          long long ld, const fwbf_outputs *out, cudaStream_t stream,
@@ -428,6 +496,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   if (o.z_bits && o.z_ld < (c->n + 31) / 32) return fail(FWBF_EINVAL, "z_ld too small");
   if (o.batch_word_err && o.batch_frames < 1) return fail(FWBF_EINVAL, "batch_frames must be >= 1");
 
+  DeviceGuard dg;
   CUDA_TRY(cudaSetDevice(c->device));
   KParams P;
   memset(&P, 0, sizeof P);
@@ -577,6 +646,13 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   if (!circ && !P.fused && c->n <= 2048) T = std::min(256, std::max(64, ((c->n + 7) / 8 + 31) / 32 * 32));
   if (!circ)
     if (const char *e = getenv("FWBF_EXPLICIT_T")) T = atoi(e); // tuning: threads per CTA (multiple of 32)
+  // Each thread keeps the previous syndrome bits of its checks tid + k*T in
+  // one 32-bit register (k < ceil(M/T)): redundant H with M > 32 T needs a
+  // wider CTA.
+  if (c->m > 32 * T) T = ((c->m + 31) / 32 + 31) / 32 * 32;
+  if (c->m > 32 * T || T > 1024)
+    return fail(FWBF_EUNSUPPORTED, "%d checks exceed the 32 x %d per-thread syndrome registers", c->m,
+                std::min(T, 1024));
   const bool compact = circ && sizeof(YT) == 4 && c->w <= 32 && !getenv("FWBF_NO_COMPACT");
   layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, P.fused, mode2);
   if (P.fused && P.smem_bytes > c->smem_optin) { // y must stay resident for the fused pass
@@ -636,9 +712,9 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   if (P.smem_bytes > c->smem_optin)
     return fail(FWBF_EUNSUPPORTED, "frame state needs %d B of shared memory (device max %d)",
                 P.smem_bytes, c->smem_optin);
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P.smem_bytes));
   int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, P.smem_bytes));
+  rc = plan_occupancy(c->device, kern, T, P.smem_bytes, &per_sm);
+  if (rc) return rc;
   if (per_sm < 1) return fail(FWBF_EUNSUPPORTED, "kernel does not fit on an SM");
   const long long grid = std::min<long long>(batch, (long long)per_sm * c->sm_count);
   CUDA_TRY(cudaMemsetAsync(P.work_counter, 0, sizeof(unsigned), stream));
@@ -669,6 +745,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
 
 extern "C" int fwbf_filter_stats(fwbf_code *c, int64_t *out, int32_t reset) {
   if (!c || !out) return fail(FWBF_EINVAL, "null argument");
+  DeviceGuard dg;
   CUDA_TRY(cudaSetDevice(c->device));
   unsigned long long h[2];
   CUDA_TRY(cudaMemcpy(h, c->d_fstats, sizeof h, cudaMemcpyDeviceToHost));
@@ -726,6 +803,7 @@ static int decode_awgn_t(fwbf_code *c, const fwbf_params *p, uint64_t seed, int6
   long long chunk = std::min<long long>(count, 1 << 18);
   const int bf = o.batch_word_err ? std::max(1, o.batch_frames) : 1;
   chunk = std::max<long long>(bf, chunk / bf * bf);
+  DeviceGuard dg;
   CUDA_TRY(cudaSetDevice(c->device));
   YT *scratch = nullptr;
   // The library scratch for y is shared by every call on this handle: calls
@@ -816,6 +894,7 @@ extern "C" int fwbf_decode_host_f32(fwbf_code *c, const fwbf_params *p, const fl
   if (chunk <= 0) chunk = 65536;
   chunk = std::min<int64_t>(chunk, batch);
   std::lock_guard<std::mutex> lock(c->pipe_mu);
+  DeviceGuard dg;
   CUDA_TRY(cudaSetDevice(c->device));
   // per-stream buffer: y chunk | z chunk | iterations | flags
   const size_t yb = (size_t)chunk * ld * sizeof(float);
@@ -878,5 +957,125 @@ extern "C" int fwbf_decode_host_f32(fwbf_code *c, const fwbf_params *p, const fl
     CUDA_TRY(cudaMemcpy(tmp, c->pipe_counters, sizeof tmp, cudaMemcpyDeviceToHost));
     for (int i = 0; i < FWBF_NCOUNTERS; ++i) cnt_host[i] += tmp[i];
   }
+  return FWBF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Stage views (fwbf_stage.cu): the reference's per-stage functions, batched.
+// ---------------------------------------------------------------------------
+static int stage_grid(long long items) {
+  const long long g = (items + 255) / 256;
+  return (int)std::max<long long>(1, std::min<long long>(g, 148LL * 64));
+}
+
+#define STAGE_LAUNCH(kern, items, stream, ...)                                       \
+  do {                                                                               \
+    if ((items) > 0) {                                                               \
+      fwbf::kern<<<stage_grid(items), 256, 0, (cudaStream_t)(stream)>>>(__VA_ARGS__); \
+      CUDA_TRY(cudaGetLastError());                                                  \
+    }                                                                                \
+  } while (0)
+
+extern "C" int fwbf_stage_hard_decision(int32_t dtype, const void *y, int64_t count, uint8_t *z, void *stream) {
+  if (count < 0) return fail(FWBF_EINVAL, "count must be nonnegative");
+  if (count && (!y || !z)) return fail(FWBF_EINVAL, "null buffer");
+  if (dtype == 4) STAGE_LAUNCH(stage_hard_decision<float>, count, stream, (const float *)y, count, z);
+  else if (dtype == 8) STAGE_LAUNCH(stage_hard_decision<double>, count, stream, (const double *)y, count, z);
+  else return fail(FWBF_EINVAL, "dtype must be 4 (float32) or 8 (float64)");
+  return FWBF_OK;
+}
+
+extern "C" int fwbf_stage_syndrome(fwbf_code *c, const uint8_t *z, int64_t batch, uint8_t *s, void *stream) {
+  if (!c) return fail(FWBF_EINVAL, "null code");
+  if (batch < 0) return fail(FWBF_EINVAL, "batch must be nonnegative");
+  DeviceGuard dg;
+  CUDA_TRY(cudaSetDevice(c->device));
+  STAGE_LAUNCH(stage_syndrome, batch * c->m, stream, c->d_row_ptr, c->d_row_idx, c->n, c->m, z, (long long)batch, s);
+  return FWBF_OK;
+}
+
+extern "C" int fwbf_stage_weights(fwbf_code *c, const double *y, int64_t batch, int64_t ld, double *min1,
+                                  double *min2, int64_t *argmin_col, double *edge_w, void *stream) {
+  if (!c) return fail(FWBF_EINVAL, "null code");
+  if (c->m && c->min_row_w < 2) return fail(FWBF_EINVAL, "every check must contain at least 2 bits");
+  if (batch < 0) return fail(FWBF_EINVAL, "batch must be nonnegative");
+  if (ld < c->n) return fail(FWBF_EINVAL, "expected a length-%d frame", c->n);
+  DeviceGuard dg;
+  CUDA_TRY(cudaSetDevice(c->device));
+  STAGE_LAUNCH(stage_weights, batch * c->m, stream, c->d_row_ptr, c->d_row_idx, c->m, c->n_edges, y,
+               (long long)batch, (long long)ld, min1, min2, (long long *)argmin_col, edge_w);
+  return FWBF_OK;
+}
+
+extern "C" int fwbf_stage_edge_weights(fwbf_code *c, const double *min1, const double *min2,
+                                       const int64_t *argmin_col, int64_t batch, double *edge_w, void *stream) {
+  if (!c) return fail(FWBF_EINVAL, "null code");
+  if (batch < 0) return fail(FWBF_EINVAL, "batch must be nonnegative");
+  DeviceGuard dg;
+  CUDA_TRY(cudaSetDevice(c->device));
+  STAGE_LAUNCH(stage_edge_weights, batch * c->m, stream, c->d_row_ptr, c->d_row_idx, c->m, c->n_edges, min1, min2,
+               (const long long *)argmin_col, (long long)batch, edge_w);
+  return FWBF_OK;
+}
+
+extern "C" int fwbf_stage_all_metrics(fwbf_code *c, const uint8_t *syndrome, const double *edge_w,
+                                      const double *abs_y, double alpha, int64_t batch, double *out,
+                                      void *stream) {
+  if (!c) return fail(FWBF_EINVAL, "null code");
+  if (batch < 0) return fail(FWBF_EINVAL, "batch must be nonnegative");
+  DeviceGuard dg;
+  CUDA_TRY(cudaSetDevice(c->device));
+  STAGE_LAUNCH(stage_all_metrics, batch * c->n, stream, c->d_col_ptr, c->d_col_idx, c->d_col_eid, c->n, c->m,
+               c->n_edges, syndrome, edge_w, abs_y, alpha, (long long)batch, out);
+  return FWBF_OK;
+}
+
+extern "C" int fwbf_stage_block_argmax(const double *values, int64_t batch, int64_t n, int64_t ld,
+                                       int32_t p, int64_t *out, void *stream) {
+  if (p < 1) return fail(FWBF_EINVAL, "block length p must be >= 1");
+  if (batch < 0 || n < 0 || ld < n) return fail(FWBF_EINVAL, "bad shape");
+  if (n > 0x7fffffffLL) return fail(FWBF_EUNSUPPORTED, "vector too long");
+  if (n == 0) return FWBF_OK;
+  const int nb = (int)((n + p - 1) / p);
+  STAGE_LAUNCH(stage_block_argmax, batch * nb, stream, values, (long long)batch, (int)n, (long long)ld, (int)p,
+               nb, (long long *)out);
+  return FWBF_OK;
+}
+
+extern "C" int fwbf_stage_bit_metric(fwbf_code *c, const int32_t *cols, int32_t k, const uint8_t *syndrome,
+                                     const double *min1, const double *min2, const int64_t *argmin_col,
+                                     const double *y, double alpha, double *out, void *stream) {
+  if (!c) return fail(FWBF_EINVAL, "null code");
+  if (k < 0) return fail(FWBF_EINVAL, "k must be nonnegative");
+  DeviceGuard dg;
+  CUDA_TRY(cudaSetDevice(c->device));
+  STAGE_LAUNCH(stage_bit_metric, (long long)k, stream, c->d_col_ptr, c->d_col_idx, cols, k, syndrome, min1, min2,
+               (const long long *)argmin_col, y, alpha, out);
+  return FWBF_OK;
+}
+
+// The reference channel alone (no decode): y[f][n] for frames
+// first..first+count, numpy's stream (fwbf_noise.cuh), float64 or float32.
+extern "C" int fwbf_channel_awgn(fwbf_code *c, uint64_t seed, int64_t first, int64_t count, double sigma,
+                                 const uint32_t *codeword_bits, int32_t noise_mode, void *y, int64_t ld,
+                                 void *stream) {
+  if (!c) return fail(FWBF_EINVAL, "null code");
+  if (first < 0 || count < 0) return fail(FWBF_EINVAL, "seed and frame index must be nonnegative");
+  if (!(sigma >= 0)) return fail(FWBF_EINVAL, "sigma must be nonnegative");
+  if (ld < c->n) return fail(FWBF_EINVAL, "ld too small");
+  if (count == 0) return FWBF_OK;
+  if (!y) return fail(FWBF_EINVAL, "y is null");
+  DeviceGuard dg;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int grid = (int)std::min<long long>((count + 3) / 4, (long long)c->sm_count * 16);
+  if (noise_mode == FWBF_NOISE_NUMPY_F64)
+    fwbf::noise_kernel_warp<double><<<grid, 128, 0, (cudaStream_t)stream>>>(
+        (unsigned long long)seed, first, count, sigma, codeword_bits, (double *)y, ld, c->n);
+  else if (noise_mode == FWBF_NOISE_NUMPY_F32)
+    fwbf::noise_kernel_warp<float><<<grid, 128, 0, (cudaStream_t)stream>>>(
+        (unsigned long long)seed, first, count, sigma, codeword_bits, (float *)y, ld, c->n);
+  else
+    return fail(FWBF_EINVAL, "unknown noise mode %d", noise_mode);
+  CUDA_TRY(cudaGetLastError());
   return FWBF_OK;
 }

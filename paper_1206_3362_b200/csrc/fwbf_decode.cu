@@ -357,7 +357,9 @@ decode_kernel(const __grid_constant__ KParams P) {
     if (tid == 0) misc[S_FRAME] = (int)atomicAdd(P.work_counter, 1u);
     __syncthreads();
     FWBF_PH(0)
-    const long long f = misc[S_FRAME];
+    // tickets are unsigned: batch <= 2^31 - 1 plus one extra ticket per CTA
+    // stays below 2^32, so the queue end is always seen
+    const long long f = (long long)(unsigned)misc[S_FRAME];
     if (f >= P.batch) break;
 
     // ---------------- init 1: y -> smem, hard decisions, guard statistics -------

@@ -198,6 +198,7 @@ class BatchResult:
     counters: "object"          # int64 [NCOUNTERS]
     fliplog: "object" = None    # int32 [B, stride]
     fliplog_counts: "object" = None  # int32 [B, k_max]
+    iter_hist: "object" = None  # int64 [k_max + 1]: frames that stopped after k iterations
 
     def z(self) -> np.ndarray:
         w = self.z_bits.cpu().numpy().astype(np.uint32)
@@ -243,6 +244,8 @@ def _outputs(res: BatchResult, stride: int = 0, codeword_t=None) -> nat.Outputs:
     o.flips_total = res.flips_total.data_ptr()
     o.bit_errors = res.bit_errors.data_ptr()
     o.counters = res.counters.data_ptr()
+    if res.iter_hist is not None:
+        o.iter_hist = res.iter_hist.data_ptr()
     if res.fliplog is not None:
         o.fliplog = res.fliplog.data_ptr()
         o.fliplog_counts = res.fliplog_counts.data_ptr()
@@ -261,6 +264,28 @@ def pack_bits(c: np.ndarray, n: int) -> np.ndarray:
     buf = np.zeros(words * 32, np.uint8)
     buf[:n] = c
     return np.packbits(buf, bitorder="little").view(np.uint32)
+
+
+def _launch_stream(dev, stream, tensors):
+    """The stream the C call is enqueued on.  A caller-supplied stream first
+    waits for the current stream (where the inputs were copied and the outputs
+    zero-filled), and every tensor is recorded on it so the caching allocator
+    keeps the memory until that stream has consumed it."""
+    torch = _torch()
+    cur = torch.cuda.current_stream(dev)
+    if stream is None or stream == cur:
+        return cur
+    stream.wait_stream(cur)
+    for t in tensors:
+        if t is not None:
+            t.record_stream(stream)
+    return stream
+
+
+def _result_tensors(res: "BatchResult"):
+    return [res.z_bits, res.iterations, res.flags, res.flips_total, res.bit_errors, res.counters,
+            res.fliplog, res.fliplog_counts, res.iter_hist, getattr(res, "batch_word_err", None),
+            getattr(res, "y", None)]
 
 
 def decode_batch(h, y, cfg: DecoderConfig, algorithm: str = "fwbf", *, flip_log: bool = False,
@@ -288,7 +313,8 @@ def decode_batch(h, y, cfg: DecoderConfig, algorithm: str = "fwbf", *, flip_log:
     y = y.to(dev)
     if y.stride(1) != 1:
         y = y.contiguous()
-    dc = device_code(h, dev.index if dev.index is not None else 0)
+    with torch.cuda.device(dev):
+        dc = device_code(h, dev.index if dev.index is not None else 0)
     if y.shape[1] < dc.n:
         raise ValueError(f"expected a length-{dc.n} frame")
     if y.shape[1] != dc.n and y.stride(0) != y.shape[1]:
@@ -307,7 +333,8 @@ def decode_batch(h, y, cfg: DecoderConfig, algorithm: str = "fwbf", *, flip_log:
         flags=torch.zeros(B, dtype=torch.uint8, **kw),
         flips_total=torch.zeros(B, dtype=torch.int32, **kw),
         bit_errors=torch.zeros(B, dtype=torch.int32, **kw),
-        counters=torch.zeros(nat.NCOUNTERS, dtype=torch.int64, **kw))
+        counters=torch.zeros(nat.NCOUNTERS, dtype=torch.int64, **kw),
+        iter_hist=torch.zeros(cfg.k_max + 1, dtype=torch.int64, **kw))
     stride = 0
     if flip_log:
         maxf = int(L.fwbf_max_flips_per_iter(dc.handle, C.byref(p)))
@@ -318,7 +345,7 @@ def decode_batch(h, y, cfg: DecoderConfig, algorithm: str = "fwbf", *, flip_log:
     if codeword is not None:
         cw_t = torch.from_numpy(pack_bits(codeword, dc.n).view(np.int32)).to(dev)
     out = _outputs(res, stride, cw_t)
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    st = _launch_stream(dev, stream, _result_tensors(res) + [y, cw_t])
     fn = L.fwbf_decode_f32 if y.dtype == torch.float32 else L.fwbf_decode_f64
     with torch.cuda.device(dev):
         nat.check(fn(dc.handle, C.byref(p), C.c_void_p(y.data_ptr()), B, ld, C.byref(out),
@@ -344,7 +371,8 @@ def metric_batch(h, y, cfg: DecoderConfig = DecoderConfig(), algorithm: str = "f
         y = y.unsqueeze(0)
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     y = y.to(dev).contiguous()
-    dc = device_code(h, dev.index if dev.index is not None else 0)
+    with torch.cuda.device(dev):
+        dc = device_code(h, dev.index if dev.index is not None else 0)
     if y.shape[1] != dc.n:
         raise ValueError(f"expected a length-{dc.n} frame")
     B = int(y.shape[0])
@@ -378,10 +406,14 @@ def decode_awgn(h, cfg: DecoderConfig, algorithm: str, seed: int, first_frame: i
         raise ValueError("block_len_p is required for block-parallel decoding")
     if seed < 0 or first_frame < 0:
         raise ValueError("seed and frame index must be nonnegative")
+    if seed >= 1 << 64:
+        # the device keys Philox with the low 64-bit key word only (channel.py:44)
+        raise ValueError("seed must be below 2**64")
     if sigma < 0:
         raise ValueError("sigma must be nonnegative")
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    dc = device_code(h, dev.index if dev.index is not None else 0)
+    with torch.cuda.device(dev):
+        dc = device_code(h, dev.index if dev.index is not None else 0)
     p = make_params(cfg, algorithm, force_ordered)
     L = nat.lib()
     B = int(count)
@@ -394,7 +426,8 @@ def decode_awgn(h, cfg: DecoderConfig, algorithm: str, seed: int, first_frame: i
         flags=torch.zeros(B, dtype=torch.uint8, **kw),
         flips_total=torch.zeros(B, dtype=torch.int32, **kw),
         bit_errors=torch.zeros(B, dtype=torch.int32, **kw),
-        counters=torch.zeros(nat.NCOUNTERS, dtype=torch.int64, **kw))
+        counters=torch.zeros(nat.NCOUNTERS, dtype=torch.int64, **kw),
+        iter_hist=torch.zeros(cfg.k_max + 1, dtype=torch.int64, **kw))
     stride = 0
     if flip_log:
         maxf = int(L.fwbf_max_flips_per_iter(dc.handle, C.byref(p)))
@@ -414,7 +447,7 @@ def decode_awgn(h, cfg: DecoderConfig, algorithm: str, seed: int, first_frame: i
         out.y_out = res.y.data_ptr()
         out.y_out_ld = dc.n
     mode = {"f64": nat.NOISE_NUMPY_F64, "f32": nat.NOISE_NUMPY_F32}[noise]
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    st = _launch_stream(dev, stream, _result_tensors(res) + [cw_t])
     with torch.cuda.device(dev):
         nat.check(L.fwbf_decode_awgn(dc.handle, C.byref(p), C.c_uint64(int(seed)), int(first_frame), B,
                                      float(sigma), mode, C.byref(out), C.c_void_p(st.cuda_stream)),

@@ -56,6 +56,81 @@ def test_scale_parity_vs_c_oracle(cuda_device, code, alg, kw, ebn0, frames):
     _cmp(res, z, its, fl, ft, f"{code}/{alg}/{ebn0}")
 
 
+# -- at-scale parity of every config in the driver-run suite ----
+# C (the W = 64 filtered MODE 2 kernel, widest error bound) at p in {64, 128,
+# 256} x {3.5, 4.0, 4.5} dB; B at p in {31, 93} over the whole 3.0-5.0 dB
+# sweep; D at its config point.  Every frame is compared with the C oracle.
+SWEEP = ([("eg6", p, db, 1 << 12, 100) for p in (64, 128, 256) for db in (3.5, 4.0, 4.5)] +
+         [("eg5", p, db, 1 << 14, 100) for p in (31, 93) for db in (3.0, 3.5, 4.0, 4.5, 5.0)] +
+         [("qc4x32", 256, 5.0, 1 << 12, 50)])
+
+
+def _oracle_threads():
+    import os
+    return max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
+
+
+@pytest.mark.parametrize("code,p,ebn0,frames,kmax", SWEEP)
+def test_sweep_parity_vs_c_oracle(cuda_device, code, p, ebn0, frames, kmax):
+    import torch
+    from paper_1206_3362_b200 import device_code
+    h = build_code(code)
+    sigma = O.ebn0_to_sigma(ebn0, code_rate(code))
+    g = torch.Generator(device="cuda").manual_seed(int(ebn0 * 10) * 1000 + p)
+    y = (1.0 + sigma * torch.randn((frames, h.n_cols), generator=g, device="cuda")).float()
+    cfg = DecoderConfig(block_len_p=p, k_max=kmax)
+    dc = device_code(h, 0)
+    dc.filter_stats(reset=True)
+    res = decode_batch(h, y, cfg, "fwbf")
+    torch.cuda.synchronize()
+    fs = dc.filter_stats(reset=True)
+    z, its, fl, ft = COracle(h).decode_batch(y.cpu().numpy(), threads=_oracle_threads(), algorithm="fwbf",
+                                             alpha=0.2, k_max=kmax, p=p)
+    _cmp(res, z, its, fl, ft, f"{code}/p{p}/{ebn0}")
+    if code == "eg6" and p == 64 and ebn0 <= 4.0:
+        # the filtered metric had to resolve decisions exactly (the fallback ran)
+        assert fs[0] > 0, fs
+
+
+@pytest.mark.parametrize("noise", ["f32", "f64"])
+def test_sweep_parity_device_noise_64k(cuda_device, noise):
+    """Config E at 2^16 frames: on-device reference channel, every frame vs the C oracle."""
+    h = build_code("eg5")
+    sigma = O.ebn0_to_sigma(4.0, code_rate("eg5"))
+    cfg = DecoderConfig(block_len_p=31, k_max=100)
+    res = decode_awgn(h, cfg, "fwbf", 5, 1 << 30, 1 << 16, sigma, noise=noise, return_y=True)
+    z, its, fl, ft = COracle(h).decode_batch(res.y.cpu().numpy(), threads=_oracle_threads(), algorithm="fwbf",
+                                             alpha=0.2, k_max=100, p=31)
+    _cmp(res, z, its, fl, ft, f"E-{noise}")
+    hist = res.iter_hist.cpu().numpy()
+    assert np.array_equal(hist, np.bincount(its, minlength=101))
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_counters_equal_single_gpu(cuda_device, world):
+    """G = 1 vs G shards (run here sequentially on one GPU,
+    each shard a separate decode_awgn call over its frame_shard range).
+    Per-frame results and the summed counters equal the single call's: noise
+    is keyed by the global frame index."""
+    import torch
+    from paper_1206_3362_b200.sharding import frame_shard
+    h = build_code("eg5")
+    sigma = O.ebn0_to_sigma(3.5, code_rate("eg5"))
+    cfg = DecoderConfig(block_len_p=31, k_max=100)
+    first, count = 1000, 30011
+    one = decode_awgn(h, cfg, "fwbf", 9, first, count, sigma, noise="f32")
+    parts, cnt = [], torch.zeros_like(one.counters)
+    for r in range(world):
+        s0, n0 = frame_shard(first, count, r, world)
+        part = decode_awgn(h, cfg, "fwbf", 9, s0, n0, sigma, noise="f32")
+        parts.append(part)
+        cnt += part.counters
+    assert torch.equal(cnt, one.counters)
+    for name in ("iterations", "flags", "z_bits", "bit_errors"):
+        assert torch.equal(torch.cat([getattr(q, name) for q in parts]), getattr(one, name)), name
+    assert torch.equal(sum(q.iter_hist for q in parts), one.iter_hist)
+
+
 @pytest.mark.parametrize("noise", ["f32", "f64"])
 def test_scale_parity_device_noise(cuda_device, noise):
     """Config E path: the device draws the reference channel; the C oracle
