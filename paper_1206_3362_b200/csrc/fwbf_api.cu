@@ -354,7 +354,7 @@ struct Plan {
 };
 
 static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool circ, int cover, KParams &P,
-                   bool compact = false, bool fused = false, bool mode2 = false) {
+                   bool compact = false, bool fused = false, bool mode2 = false, bool ystage = false) {
   const int n = c->n, m = c->m;
   const int zw = (n + 31) / 32, sw = (m + 31) / 32;
   int nb = 1;
@@ -370,9 +370,17 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
     P.off_y = take(n * 8);
     P.off_e = P.off_y;
     P.alias_y = 1;
+  } else if (ystage) {
+    // the staging buffer below is the only copy of y in shared memory
+    P.off_e = take(n * 8);
   } else {
     P.off_y = take(n * ysize);
     P.off_e = fused ? P.off_y : take(n * 8); // fused: no metric buffer
+  }
+  if (ystage) {
+    P.ystage_bytes = (n * ysize + 15) & ~15;
+    P.off_ystage = take(P.ystage_bytes);
+    if (!compact) P.off_y = P.off_ystage;
   }
   // guarded path: doubled signed min1 plus zero pad up to the threads' column cover
   // check records: guarded path (circulant) = two doubled arrays sgn*min1,
@@ -654,10 +662,21 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     return fail(FWBF_EUNSUPPORTED, "%d checks exceed the 32 x %d per-thread syndrome registers", c->m,
                 std::min(T, 1024));
   const bool compact = circ && sizeof(YT) == 4 && c->w <= 32 && !getenv("FWBF_NO_COMPACT");
-  layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, P.fused, mode2);
+  // staged input rows (TMA bulk copy one frame ahead): compile-time-shape
+  // circulant float32 kernels; rows must be 16-byte aligned and hold the
+  // rounded-up copy size
+  const long long row_bytes = ld * (long long)sizeof(YT);
+  const bool ystage = circ && sizeof(YT) == 4 && kwt > 0 && !metric_out && !getenv("FWBF_NO_YSTAGE") &&
+                      ((uintptr_t)y % 16) == 0 && row_bytes % 16 == 0 &&
+                      ((c->n * (long long)sizeof(YT) + 15) & ~15LL) <= row_bytes;
+  layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, P.fused, mode2, ystage);
   if (P.fused && P.smem_bytes > c->smem_optin) { // y must stay resident for the fused pass
     P.fused = 0;
-    layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, false, mode2);
+    layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, false, mode2, ystage);
+  }
+  if (ystage) {
+    P.y_stage = 1;
+    P.alias_y = 1; // after frame init, y is re-read from HBM (the staging buffer holds the next frame)
   }
   {
     // FWBF block-argmax groups: odd p -> one thread per block (stride-p reads
@@ -688,7 +707,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     P.log2_tpb = 0;
     while ((1 << P.log2_tpb) < tpb) ++P.log2_tpb;
   }
-  if (P.smem_bytes > c->smem_optin && !compact) {
+  if (P.smem_bytes > c->smem_optin && !compact && !ystage) {
     // Alias the metric buffer over the y buffer: after init y is only needed
     // for alpha*|y|, which the kernel then re-reads from global memory.
     P.alias_y = 1;
@@ -696,7 +715,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     P.off_e = P.off_y;
     for (int *x : {&P.off_chk1, &P.off_chk2, &P.off_amin, &P.off_amask, &P.off_sbits, &P.off_zbits,
                    &P.off_blkv, &P.off_blki, &P.off_flips, &P.off_offs, &P.off_red, &P.off_misc,
-                   &P.off_fa, &P.off_fb, &P.off_m2s, &P.off_a2m, &P.off_corr, &P.off_ay})
+                   &P.off_fa, &P.off_fb, &P.off_m2s, &P.off_a2m, &P.off_corr, &P.off_ay, &P.off_ystage})
       *x += delta;
     P.smem_bytes += delta;
   }

@@ -216,6 +216,38 @@ template <int KK, int KC, int TB, bool CC> struct RefreshKK<KK, KC, TB, CC, fals
                                              int, int, bool) {}
 };
 
+// ---- TMA bulk copy of one frame row into shared memory (mbarrier completion) ----
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// Thread 0, after a CTA barrier that ends every generic access of `dst`:
+// order those accesses before the async-proxy write, arm the barrier with the
+// byte count and issue the copy.
+__device__ __forceinline__ void bulk_row_to_smem(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(b),
+      "r"(phase)
+      : "memory");
+}
+
 // Exact argmin corrections as two int32 limbs: D = lo + hi * 2^24 with
 // lo in [0, 2^24) (D an integer multiple of the frame quantum q).
 __device__ __forceinline__ void corr_add(int *corr, int col, long long D, int sign) {
@@ -282,7 +314,8 @@ decode_kernel(const __grid_constant__ KParams P) {
   const int N = P.n;
   const int M = P.m;
 
-  YT *ybuf = reinterpret_cast<YT *>(smem_raw + P.off_y);
+  // frame row: staged by a bulk copy (P.y_stage) or loaded element-wise
+  YT *ybuf = reinterpret_cast<YT *>(smem_raw + (P.y_stage ? P.off_ystage : P.off_y));
   double *Ebuf = reinterpret_cast<double *>(smem_raw + P.off_e);
   double *chk1 = reinterpret_cast<double *>(smem_raw + P.off_chk1); // min1 (signed); doubled on the guarded path
   double *chk2 = reinterpret_cast<double *>(smem_raw + P.off_chk2); // min2 (signed); doubled on the guarded path
@@ -352,15 +385,34 @@ decode_kernel(const __grid_constant__ KParams P) {
   const int nKy = (N + T - 1) / T; // rounds over columns
   const int nKm = (M + T - 1) / T; // rounds over checks
 
+  // Staged input: the frame queue is claimed one frame ahead and that frame's
+  // y row is copied into ybuf by the TMA engine while the current frame
+  // iterates (issued after the current frame's last read of ybuf).
+  __shared__ __align__(8) uint64_t ystage_bar;
+  unsigned ystage_phase = 0;
+  const bool ystage = P.y_stage != 0;
+  if (ystage && tid == 0) {
+    mbar_init(&ystage_bar, 1);
+    const unsigned t0 = atomicAdd(P.work_counter, 1u);
+    misc[S_FRAME] = (int)t0;
+    if ((long long)t0 < P.batch)
+      bulk_row_to_smem(ybuf, reinterpret_cast<const YT *>(P.y) + (long long)t0 * P.ld, (unsigned)P.ystage_bytes,
+                       &ystage_bar);
+  }
+
   for (;;) {
     __syncthreads();
-    if (tid == 0) misc[S_FRAME] = (int)atomicAdd(P.work_counter, 1u);
+    if (!ystage && tid == 0) misc[S_FRAME] = (int)atomicAdd(P.work_counter, 1u);
     __syncthreads();
     FWBF_PH(0)
     // tickets are unsigned: batch <= 2^31 - 1 plus one extra ticket per CTA
     // stays below 2^32, so the queue end is always seen
     const long long f = (long long)(unsigned)misc[S_FRAME];
     if (f >= P.batch) break;
+    if (ystage) { // this frame's row has landed in ybuf
+      mbar_wait(&ystage_bar, ystage_phase);
+      ystage_phase ^= 1u;
+    }
 
     // ---------------- init 1: y -> smem, hard decisions, guard statistics -------
     float lmin = INFINITY, lmax = 0.f;
@@ -368,7 +420,7 @@ decode_kernel(const __grid_constant__ KParams P) {
     for (int k = 0; k < nKy; ++k) {
       const int n = tid + k * T;
       const bool ok = n < N;
-      YT v = ok ? load_y<YT>(P, f, n) : YT(0);
+      YT v = ok ? (ystage ? ybuf[n] : load_y<YT>(P, f, n)) : YT(0);
       if (ok) ybuf[n] = v + YT(0); // -0.0 -> +0.0: the sign bit of ybuf is the hard decision (y < 0)
       const uint32_t b = __ballot_sync(FULL_MASK, ok && (v < YT(0)));
       if (lane == 0 && (k * T + warp * 32) < N) zbits[(k * T + warp * 32) >> 5] = b;
@@ -821,9 +873,18 @@ decode_kernel(const __grid_constant__ KParams P) {
     if (FILT && split) {
       float *ya = reinterpret_cast<float *>(Ebuf) + ((N + 1) & ~1);
       for (int n = tid; n < N; n += T)
-        ya[n] = fabsf((float)(P.alias_y ? load_y<YT>(P, f, n) : ybuf[n]));
+        ya[n] = fabsf((float)((P.alias_y && !ystage) ? load_y<YT>(P, f, n) : ybuf[n]));
     }
     if (P.alias_y || (FILT && split)) __syncthreads(); // amask / ybuf may overlay Ebuf (compact layout); MODE 2 tables
+    if (ystage && tid == 0) {
+      // ybuf is dead for this frame (alias_y: later reads of y go to HBM):
+      // claim the next frame and start its copy
+      const unsigned t1 = atomicAdd(P.work_counter, 1u);
+      misc[S_FRAME] = (int)t1;
+      if ((long long)t1 < P.batch)
+        bulk_row_to_smem(ybuf, reinterpret_cast<const YT *>(P.y) + (long long)t1 * P.ld,
+                         (unsigned)P.ystage_bytes, &ystage_bar);
+    }
 
     // ---------------- iterations -----------------------------------------------
     int k = 0;

@@ -90,6 +90,13 @@ struct KParams {
   int no_split; // disable the split-fp32 path (testing)
   int filter;   // FWBF on the split path: approximate fp32 gather + exact resolution of close decisions
   unsigned long long *filter_stats; // optional [2]: blocks resolved exactly, stall argmaxes resolved exactly
+  // Input staging (circulant float32 kernels): the next frame's y row is
+  // fetched by one cp.async.bulk (TMA bulk copy, completion on an mbarrier)
+  // into a shared staging buffer while the current frame iterates; frame init
+  // then reads y from shared memory instead of HBM.
+  int y_stage;      // 1: enabled (16-byte aligned rows; ybuf = the staging buffer)
+  int off_ystage;   // staging buffer byte offset (16-byte aligned)
+  int ystage_bytes; // bytes per copy: N * sizeof(YT) rounded up to 16 (<= ld * sizeof(YT))
 };
 
 } // namespace fwbf
