@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <list>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -26,6 +27,7 @@ __global__ void decode_kernel(const __grid_constant__ KParams P);
 template <typename YT>
 __global__ void noise_kernel(unsigned long long seed, long long first, long long count, double sigma,
                              const uint32_t *codeword, YT *y, long long ld, int n, int pm);
+__global__ void xdecode_kernel(const __grid_constant__ XParams P);
 template <typename T> __global__ void stage_hard_decision(const T *, long long, uint8_t *);
 __global__ void stage_syndrome(const int *, const int *, int, int, const uint8_t *, long long, uint8_t *);
 __global__ void stage_weights(const int *, const int *, int, long long, const double *, long long, long long,
@@ -74,6 +76,19 @@ struct DeviceGuard {
   }
 };
 
+// One-frame-per-warp explicit-code plan (fwbf_explicit.cu), built per (code, p).
+struct XPlan {
+  int p = 0, nb = 0, lg_g = 0, rounds = 0, slots = 0;
+  unsigned long long *d_tab = nullptr;
+  uint32_t *d_rtab = nullptr;
+  uint16_t *d_cpos = nullptr;
+  int tables_bytes = 0, warp_bytes = 0;
+  int wo_rec = 0, wo_ys = 0, wo_am = 0, wo_sb = 0, wo_zw = 0, wo_bf = 0;
+  int off_tab = 0, off_rtab = 0, off_rptr = 0, off_cpos = 0;
+  int wpc = 0, per_sm = 0, smem = 0; // warps per CTA, CTAs per SM, dynamic smem bytes
+  bool ok = false;
+};
+
 struct fwbf_code {
   int device = 0;
   int n = 0, m = 0;
@@ -104,6 +119,10 @@ struct fwbf_code {
   void *noise_buf = nullptr;
   size_t noise_bytes = 0;
   cudaEvent_t noise_evt = nullptr; // last use of noise_buf (device-side ordering across streams)
+  // explicit-code warp-per-frame plans, one per block length p
+  std::mutex xplan_mu;
+  std::list<XPlan> xplans; // stable addresses: launches hold a plan pointer outside the lock
+  std::vector<int> h_row_ptr, h_row_idx, h_col_ptr, h_col_idx; // host copies for plan building
 };
 
 // Each decode launch takes the next of kWorkRing frame-queue counters of its
@@ -195,6 +214,12 @@ extern "C" int fwbf_code_create(const fwbf_code_desc *desc, int device, fwbf_cod
   c->dv_max = dvm;
   c->dc_max = dcm;
   c->min_row_w = minrw;
+  if (!desc->circulant) {
+    c->h_row_ptr = row_ptr;
+    c->h_row_idx = row_idx;
+    c->h_col_ptr = col_ptr;
+    c->h_col_idx = col_idx;
+  }
   std::vector<uint8_t> i0tab, jwtab;
   std::vector<int16_t> offpos;
   if (desc->circulant) {
@@ -295,6 +320,11 @@ extern "C" int fwbf_code_destroy(fwbf_code *c) {
   cudaFree(c->pipe_counters);
   cudaFree(c->noise_buf);
   if (c->noise_evt) cudaEventDestroy(c->noise_evt);
+  for (XPlan &x : c->xplans) {
+    cudaFree(x.d_tab);
+    cudaFree(x.d_rtab);
+    cudaFree(x.d_cpos);
+  }
   delete c;
   return FWBF_OK;
 }
@@ -483,6 +513,173 @@ static int plan_occupancy(int device, const void *kern, int threads, int smem, i
   return FWBF_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Explicit codes, FWBF: one frame per warp (fwbf_explicit.cu)
+// ---------------------------------------------------------------------------
+// Slot tables: blocks of p columns go to groups of G = 2^lg lanes; lane `sub`
+// of the group for block b scans columns b p + sub + G c (c < S) in ascending
+// order.  G minimises the per-iteration cost model (slots per lane x ~22
+// instructions + butterfly levels per round).  Returns a plan with ok=false
+// when the code does not fit the kernel's limits (dv <= 4, 16-bit indices,
+// shared memory), in which case the CTA-per-frame kernel decodes it.
+static int build_xplan(fwbf_code *c, int p, XPlan *out) {
+  XPlan x;
+  x.p = p;
+  const int n = c->n, m = c->m;
+  x.nb = (n + p - 1) / p;
+  if (c->dv_max > 4 || m > 2048 || n > 0xffff || c->n_edges > (1 << 24)) { *out = x; return FWBF_OK; }
+  long best_cost = -1;
+  for (int lg = 0; lg <= 5; ++lg) {
+    const int G = 1 << lg;
+    const long R = ((long)x.nb * G + 31) / 32, S = (p + G - 1) / G;
+    const long cost = R * S * 22 + R * lg * 8 + R * 6;
+    if (R * S * 32 > 0xffff) continue;
+    if (best_cost < 0 || cost < best_cost) { best_cost = cost; x.lg_g = lg; x.rounds = (int)R; x.slots = (int)S; }
+  }
+  if (best_cost < 0) { *out = x; return FWBF_OK; }
+  const int G = 1 << x.lg_g, R = x.rounds, S = x.slots, nslot = R * S * 32;
+  std::vector<unsigned long long> tab(nslot, ~0ull);
+  std::vector<uint16_t> cpos(n, 0);
+  for (int r = 0; r < R; ++r)
+    for (int cc = 0; cc < S; ++cc)
+      for (int l = 0; l < 32; ++l) {
+        const int b = r * (32 / G) + l / G, sub = l % G;
+        if (b >= x.nb) continue;
+        const int base = b * p, lim = std::min(p, n - base);
+        if (sub + G * cc >= lim) continue;
+        const int col = base + sub + G * cc, pos = (r * S + cc) * 32 + l;
+        unsigned long long w = ~0ull;
+        const int e0 = c->h_col_ptr[col], e1 = c->h_col_ptr[col + 1];
+        for (int e = e0; e < e1; ++e) {
+          w &= ~(0xffffull << (16 * (e - e0)));
+          w |= (unsigned long long)c->h_col_idx[e] << (16 * (e - e0));
+        }
+        if (e0 == e1) w = (w & ~0xffffull) | 0xfffeull; // a column without checks
+        tab[pos] = w;
+        cpos[col] = (uint16_t)pos;
+      }
+  std::vector<uint32_t> rtab(c->n_edges);
+  for (int r = 0; r < m; ++r)
+    for (int e = c->h_row_ptr[r]; e < c->h_row_ptr[r + 1]; ++e) {
+      const int col = c->h_row_idx[e];
+      int q = 0;
+      while (c->h_col_idx[c->h_col_ptr[col] + q] != r) ++q;
+      rtab[e] = (uint32_t)cpos[col] | ((uint32_t)q << 16);
+    }
+  // shared memory: CTA tables, then one region per warp
+  int o = 0;
+  auto take = [&](int bytes) { int r0 = o; o = align16(o + bytes); return r0; };
+  x.off_tab = take(nslot * 8);
+  x.off_rtab = take((int)c->n_edges * 4);
+  x.off_rptr = take((m + 1) * 4);
+  x.off_cpos = take(n * 2);
+  x.tables_bytes = o;
+  int w = 0;
+  auto wtake = [&](int bytes) { int r0 = w; w = align16(w + bytes); return r0; };
+  x.wo_rec = wtake(m * 16);
+  x.wo_ys = wtake(nslot * 4);
+  x.wo_am = wtake(nslot);
+  x.wo_sb = wtake(((m + 31) / 32) * 4);
+  x.wo_zw = wtake(((n + 31) / 32) * 4);
+  x.wo_bf = wtake(x.nb * 4);
+  x.warp_bytes = w;
+  // warps per CTA: the most resident warps per SM
+  const void *kern = (const void *)fwbf::xdecode_kernel;
+  int best_warps = 0;
+  for (int wpc : {8, 4, 2, 1}) {
+    const int smem = x.tables_bytes + wpc * x.warp_bytes;
+    if (smem > c->smem_optin) continue;
+    int occ = 0;
+    if (plan_occupancy(c->device, kern, 32 * wpc, smem, &occ)) return FWBF_ECUDA;
+    if (occ * wpc > best_warps) { best_warps = occ * wpc; x.wpc = wpc; x.per_sm = occ; x.smem = smem; }
+  }
+  if (best_warps < 8) { *out = x; return FWBF_OK; } // too few frames in flight: the CTA kernel wins
+  int rc;
+  if ((rc = upload(&x.d_tab, tab)) || (rc = upload(&x.d_rtab, rtab)) || (rc = upload(&x.d_cpos, cpos))) {
+    cudaFree(x.d_tab);
+    cudaFree(x.d_rtab);
+    cudaFree(x.d_cpos);
+    return rc;
+  }
+  x.ok = true;
+  *out = x;
+  return FWBF_OK;
+}
+
+static int launch_explicit(fwbf_code *c, const fwbf_params *p, const XPlan &x, const float *y, long long batch,
+                           long long ld, const fwbf_outputs &o, cudaStream_t stream) {
+  fwbf::XParams P;
+  memset(&P, 0, sizeof P);
+  P.n = c->n;
+  P.m = c->m;
+  P.n_edges = (int)c->n_edges;
+  P.nb = x.nb;
+  P.p = x.p;
+  P.lg_g = x.lg_g;
+  P.rounds = x.rounds;
+  P.slots = x.slots;
+  P.kmax = p->k_max;
+  P.stall = p->stall;
+  P.wmode = p->weight_mode;
+  P.alpha = p->alpha;
+  P.tab = x.d_tab;
+  P.rtab = x.d_rtab;
+  P.row_ptr = c->d_row_ptr;
+  P.cpos = x.d_cpos;
+  P.off_tab = x.off_tab;
+  P.off_rtab = x.off_rtab;
+  P.off_rptr = x.off_rptr;
+  P.off_cpos = x.off_cpos;
+  P.off_warp0 = x.tables_bytes;
+  P.warp_bytes = x.warp_bytes;
+  P.wo_rec = x.wo_rec;
+  P.wo_ys = x.wo_ys;
+  P.wo_am = x.wo_am;
+  P.wo_sb = x.wo_sb;
+  P.wo_zw = x.wo_zw;
+  P.wo_bf = x.wo_bf;
+  P.y = y;
+  P.ld = ld;
+  P.batch = batch;
+  P.y_vec4 = ((uintptr_t)y % 16) == 0 && ld % 4 == 0;
+  P.z_bits = o.z_bits;
+  P.z_ld = o.z_ld;
+  P.iterations = o.iterations;
+  P.flags = o.flags;
+  P.flips_total = o.flips_total;
+  P.bit_errors = o.bit_errors;
+  P.fliplog = o.fliplog;
+  P.fliplog_counts = o.fliplog_counts;
+  P.fliplog_stride = o.fliplog_stride;
+  P.counters = (long long *)o.counters;
+  P.iter_hist = (long long *)o.iter_hist;
+  P.batch_word_err = o.batch_word_err;
+  P.batch_frames = o.batch_frames;
+  P.codeword_bits = o.codeword_bits;
+  const unsigned slot = c->work_slot.fetch_add(1) % kWorkRing;
+  P.work_counter = c->d_work + slot;
+  const long long grid = std::min<long long>((batch + x.wpc - 1) / x.wpc, (long long)x.per_sm * c->sm_count);
+  CUDA_TRY(cudaMemsetAsync(P.work_counter, 0, sizeof(unsigned), stream));
+  void *args[] = {&P};
+  CUDA_TRY(cudaLaunchKernel((const void *)fwbf::xdecode_kernel, dim3((unsigned)grid), dim3(32 * x.wpc), args,
+                            x.smem, stream));
+  CUDA_TRY(cudaGetLastError());
+  return FWBF_OK;
+}
+
+// The plan for (c, p), built on first use; nullptr when the kernel does not apply.
+static const XPlan *get_xplan(fwbf_code *c, int p, int *rc) {
+  *rc = FWBF_OK;
+  std::lock_guard<std::mutex> lock(c->xplan_mu);
+  for (const XPlan &x : c->xplans)
+    if (x.p == p) return x.ok ? &x : nullptr;
+  XPlan x;
+  *rc = build_xplan(c, p, &x);
+  if (*rc) return nullptr;
+  c->xplans.push_back(x);
+  return c->xplans.back().ok ? &c->xplans.back() : nullptr;
+}
+
 template <typename YT>
 static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long long batch,
                          long long ld, const fwbf_outputs *out, cudaStream_t stream,
@@ -506,6 +703,11 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
 
   DeviceGuard dg;
   CUDA_TRY(cudaSetDevice(c->device));
+  if (!c->circ && sizeof(YT) == 4 && p->algorithm == FWBF_ALG_FWBF && !metric_out && !getenv("FWBF_NO_WARP")) {
+    const XPlan *xp = get_xplan(c, p->block_len_p, &rc);
+    if (rc) return rc;
+    if (xp) return launch_explicit(c, p, *xp, (const float *)y, batch, ld, o, stream);
+  }
   KParams P;
   memset(&P, 0, sizeof P);
   P.n = c->n;

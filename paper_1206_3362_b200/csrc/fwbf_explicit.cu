@@ -1,0 +1,299 @@
+// fwbf_explicit.cu -- FWBF on small explicit (CSR/CSC) codes: one frame per warp.
+//
+// The CTA-per-frame kernel (fwbf_decode.cu) spends most of an iteration of a
+// short code (Gallager N = 504: 1,512 edges) in CTA barriers, dependent
+// index loads and bank-conflicted check reads.  Here a warp owns a whole
+// frame, so the loop needs only __syncwarp, and the code's structure is
+// compiled on the host into per-lane slot tables shared by every warp:
+//
+//   * blocks of p columns are assigned to groups of G lanes (G a power of
+//     two chosen on the host); lane `sub` of a group scans columns
+//     sub, sub + G, ... of its block in ascending order ("slots");
+//   * slot (round r, step c) of lane l lives at position pos = (r S + c) 32 + l,
+//     so every per-slot array is read conflict-free (consecutive lanes,
+//     consecutive words); tab[pos] packs the column's <= 4 check indices
+//     (ascending, 16 bits each);
+//   * per check one 16-byte record (sgn min1, sgn min2) in fp64: an edge is
+//     one LDS.64 whose address picks min1 or min2 by the column's argmin bit.
+//
+// Per frame (decoders.py:189-229): y (float4 loads when rows are 16-byte
+// aligned) -> signed y per slot + hard decisions; per check min1 / min2 /
+// argmin / parity (decoders.py:87-103) walking the row in ascending column
+// order; then per iteration the Eq.(1) metric in the reference's arithmetic
+// (fp64 adds in ascending check order from 0.0, minus fl(alpha |y|),
+// decoders.py:148-153), the block argmax with lowest-index ties and the > 0
+// threshold (decoders.py:156-167, 181-183), the stall policy
+// (decoders.py:214-222), and the flips: z and syndrome bits toggled by
+// atomic XOR, the checks' record signs by 64-bit atomic XOR of the sign bits
+// (XOR commutes, so two flips toggling one check cancel exactly).  (An
+// owner-lane refresh of the records instead of the sign atomics -- every lane
+// rescans its checks' syndrome words -- measured 7 % slower on Gallager(504).)
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "fwbf_b200.h"
+#include "fwbf_internal.h"
+
+namespace fwbf {
+
+#define XFULL 0xffffffffu
+
+__device__ __forceinline__ double xdinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+
+__global__ void __launch_bounds__(256) xdecode_kernel(const __grid_constant__ XParams P) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int N = P.n, M = P.m, R = P.rounds, S = P.slots, G = 1 << P.lg_g;
+  const int nslot = R * S * 32;
+
+  // ---- CTA-shared code tables (same for every frame) ----
+  unsigned long long *tab = reinterpret_cast<unsigned long long *>(sm + P.off_tab);
+  uint32_t *rtab = reinterpret_cast<uint32_t *>(sm + P.off_rtab);
+  int *rptr = reinterpret_cast<int *>(sm + P.off_rptr);
+  uint16_t *cpos = reinterpret_cast<uint16_t *>(sm + P.off_cpos);
+  for (int i = tid; i < nslot; i += blockDim.x) tab[i] = __ldg(P.tab + i);
+  for (int i = tid; i < P.n_edges; i += blockDim.x) rtab[i] = __ldg(P.rtab + i);
+  for (int i = tid; i <= M; i += blockDim.x) rptr[i] = __ldg(P.row_ptr + i);
+  for (int i = tid; i < N; i += blockDim.x) cpos[i] = __ldg(P.cpos + i);
+  __syncthreads();
+
+  // ---- this warp's frame state ----
+  unsigned char *W = sm + P.off_warp0 + warp * P.warp_bytes;
+  double *rec = reinterpret_cast<double *>(W + P.wo_rec);      // [2M]: sgn*min1, sgn*min2
+  float *ys = reinterpret_cast<float *>(W + P.wo_ys);           // [nslot] signed y per slot (-0 -> +0)
+  uint8_t *am = W + P.wo_am;                                    // [nslot] argmin bits per slot
+  uint32_t *sb = reinterpret_cast<uint32_t *>(W + P.wo_sb);     // syndrome bits
+  uint32_t *zw = reinterpret_cast<uint32_t *>(W + P.wo_zw);     // hard decisions by column
+  int *bflip = reinterpret_cast<int *>(W + P.wo_bf);            // per block: flipped column or -1
+  const int zwords = (N + 31) >> 5;
+  const bool imw = P.wmode == FWBF_WEIGHTS_IMWBF;
+  const double alpha = P.alpha;
+
+  long long c_frames = 0, c_biterr = 0, c_worderr = 0, c_iters = 0, c_flips = 0, c_stalls = 0, c_conv = 0,
+            c_edges = 0;
+
+  for (;;) {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(P.work_counter, 1u);
+    t = __shfl_sync(XFULL, t, 0);
+    const long long f = (long long)t; // unsigned tickets: see decode_kernel
+    if (f >= P.batch) break;
+
+    // ---- init: y -> signed y per slot, hard decisions by column ----
+    for (int i = lane; i < (nslot >> 2); i += 32) reinterpret_cast<uint32_t *>(am)[i] = 0u;
+    const float *yr = P.y + f * P.ld;
+    bool nonfin = false;
+    if (P.y_vec4) {
+      for (int i = lane; i < zwords; i += 32) zw[i] = 0u;
+      __syncwarp();
+      for (int n0 = 4 * lane; n0 < N; n0 += 128) {
+        const float4 v4 = __ldg(reinterpret_cast<const float4 *>(yr + n0));
+        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+        uint32_t nib = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int n = n0 + u;
+          if (n < N) {
+            const float v = vv[u] + 0.0f; // -0.0 -> +0.0: the sign bit is the hard decision
+            ys[cpos[n]] = v;
+            nib |= (v < 0.0f ? 1u : 0u) << u;
+            nonfin |= !isfinite(v);
+          }
+        }
+        if (nib) atomicOr(&zw[n0 >> 5], nib << (n0 & 31));
+      }
+    } else {
+      for (int n0 = 0; n0 < N; n0 += 32) {
+        const int n = n0 + lane;
+        float v = n < N ? __ldg(yr + n) + 0.0f : 0.0f;
+        const uint32_t b = __ballot_sync(XFULL, n < N && v < 0.0f);
+        if (lane == 0) zw[n0 >> 5] = b;
+        if (n < N) {
+          ys[cpos[n]] = v;
+          nonfin |= !isfinite(v);
+        }
+      }
+    }
+    nonfin = __any_sync(XFULL, nonfin);
+    __syncwarp();
+
+    // ---- per-check minima, argmin, parity (ascending columns, strict <) ----
+    int swt = 0;
+    for (int m0 = 0; m0 < M; m0 += 32) {
+      const int m = m0 + lane;
+      uint32_t par = 0;
+      if (m < M) {
+        float min1 = INFINITY, min2 = INFINITY;
+        int ae = -1;
+        const int e1 = rptr[m + 1];
+        for (int e = rptr[m]; e < e1; ++e) {
+          const float v = ys[rtab[e] & 0xffffu];
+          par ^= __float_as_uint(v);
+          const float a = fabsf(v);
+          const bool lt = a < min1;
+          min2 = fminf(min2, fmaxf(min1, a));
+          min1 = fminf(min1, a);
+          ae = lt ? e : ae;
+        }
+        par >>= 31;
+        const double sg = par ? 1.0 : -1.0;
+        // MWBF (include-self minimum): every edge reads min1
+        *reinterpret_cast<double2 *>(rec + 2 * m) =
+            make_double2(sg * (double)min1, sg * (double)(imw ? min2 : min1));
+        if (imw && ae >= 0) { // the argmin column reads min2 at this check's position in its list
+          const uint32_t pe = rtab[ae];
+          const uint32_t pos = pe & 0xffffu;
+          atomicOr(reinterpret_cast<uint32_t *>(am) + (pos >> 2), (1u << (pe >> 16)) << (8 * (pos & 3)));
+        }
+      }
+      const uint32_t b = __ballot_sync(XFULL, par != 0);
+      if (lane == 0) sb[m0 >> 5] = b;
+      swt += __popc(b);
+    }
+    __syncwarp();
+
+    // ---- iterations ----
+    int k = 0, conv = 0, stalled = 0;
+    long long logpos = 0, flips_total = 0;
+    for (;;) {
+      if (swt == 0) { conv = 1; break; }
+      if (k >= P.kmax) break;
+      double gbest = -xdinf(); // this lane's best block maximum (stall policy)
+      int gcol = 0x7fffffff;
+      int nflip = 0;
+      for (int r = 0; r < R; ++r) {
+        double best = -xdinf();
+        int bc = -1;
+        const int pos0 = r * S * 32 + lane;
+#pragma unroll 2
+        for (int c = 0; c < S; ++c) {
+          const int pos = pos0 + c * 32;
+          const unsigned long long w = tab[pos];
+          if ((uint32_t)(w & 0xffffu) != 0xffffu) { // a column (0xfffe: a column without checks)
+            const uint32_t amk = am[pos];
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t idx = (uint32_t)(w >> (16 * q)) & 0xffffu;
+              if (idx < 0xfffeu) acc = __dadd_rn(acc, rec[2 * idx + ((amk >> q) & 1u)]);
+            }
+            const double e = __dsub_rn(acc, __dmul_rn(alpha, (double)fabsf(ys[pos])));
+            if (e > best) { best = e; bc = c; }
+          }
+        }
+        // group butterfly: value desc, column asc (column = base + sub + G c)
+        const int b = r * (32 >> P.lg_g) + (lane >> P.lg_g);
+        const int sub = lane & (G - 1);
+        int col = bc >= 0 ? b * P.p + sub + G * bc : 0x7fffffff;
+        for (int off = G >> 1; off; off >>= 1) {
+          const double v2 = __shfl_xor_sync(XFULL, best, off);
+          const int c2 = __shfl_xor_sync(XFULL, col, off);
+          if (v2 > best || (v2 == best && c2 < col)) { best = v2; col = c2; }
+        }
+        const bool leader = sub == 0 && b < P.nb;
+        if (leader) {
+          if (best > gbest || (best == gbest && col < gcol)) { gbest = best; gcol = col; }
+          bflip[b] = best > 0.0 ? col : -1; // decoders.py:181-183
+        }
+        nflip += __popc(__ballot_sync(XFULL, leader && best > 0.0));
+      }
+      __syncwarp(); // every metric read of rec / sb precedes the flips
+      int F = nflip;
+      if (F == 0) {
+        // nothing selected with a nonzero syndrome (decoders.py:214-222)
+        stalled = 1;
+        if (P.stall == FWBF_STALL_TERMINATE) {
+          if (lane == 0 && P.fliplog_counts) P.fliplog_counts[f * P.kmax + k] = 0;
+          k += 1;
+          break;
+        }
+        // flip the global first maximum: the largest block maximum, lowest column
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+          const double v2 = __shfl_xor_sync(XFULL, gbest, off);
+          const int c2 = __shfl_xor_sync(XFULL, gcol, off);
+          if (v2 > gbest || (v2 == gbest && c2 < gcol)) { gbest = v2; gcol = c2; }
+        }
+        // every block maximum was <= 0, so every bflip entry is already -1
+        if (lane == 0 && gcol < N) bflip[gcol / P.p] = gcol;
+        F = 1;
+        __syncwarp();
+      }
+      // apply the flips in block order (= ascending columns); log them
+      int dsw = 0, cnt = 0;
+      for (int b0 = 0; b0 < P.nb; b0 += 32) {
+        const int b = b0 + lane;
+        const int c = b < P.nb ? bflip[b] : -1;
+        const uint32_t msk = __ballot_sync(XFULL, c >= 0);
+        if (c >= 0) {
+          if (P.fliplog) P.fliplog[f * P.fliplog_stride + logpos + cnt + __popc(msk & ((1u << lane) - 1u))] = c;
+          atomicXor(&zw[c >> 5], 1u << (c & 31));
+          const unsigned long long w = tab[cpos[c]];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t m = (uint32_t)(w >> (16 * q)) & 0xffffu;
+            if (m < 0xfffeu) {
+              const uint32_t old = atomicXor(&sb[m >> 5], 1u << (m & 31));
+              dsw += ((old >> (m & 31)) & 1u) ? -1 : 1;
+              // negate sgn*min1 and sgn*min2 of the toggled check
+              unsigned long long *r2 = reinterpret_cast<unsigned long long *>(rec + 2 * m);
+              atomicXor(r2, 0x8000000000000000ull);
+              atomicXor(r2 + 1, 0x8000000000000000ull);
+            }
+          }
+        }
+        cnt += __popc(msk);
+      }
+      if (lane == 0 && P.fliplog) P.fliplog_counts[f * P.kmax + k] = F;
+      swt += __reduce_add_sync(XFULL, dsw);
+      __syncwarp();
+      logpos += F;
+      flips_total += F;
+      k += 1;
+    }
+
+    // ---- outputs ----
+    int be = 0;
+    for (int i = lane; i < zwords; i += 32) {
+      const uint32_t z = zw[i];
+      if (P.z_bits) P.z_bits[f * P.z_ld + i] = z;
+      const uint32_t cw = P.codeword_bits ? __ldg(P.codeword_bits + i) : 0u;
+      be += __popc(z ^ cw);
+    }
+    be = __reduce_add_sync(XFULL, be);
+    if (lane == 0) {
+      const int flags = (conv ? FWBF_FLAG_CONVERGED : 0) | (stalled ? FWBF_FLAG_STALLED : 0) | FWBF_FLAG_ORDERED |
+                        (nonfin ? FWBF_FLAG_NONFINITE : 0);
+      if (P.iterations) P.iterations[f] = k;
+      if (P.flags) P.flags[f] = (uint8_t)flags;
+      if (P.flips_total) P.flips_total[f] = (int)flips_total;
+      if (P.bit_errors) P.bit_errors[f] = be;
+      if (P.iter_hist) atomicAdd((unsigned long long *)&P.iter_hist[k], 1ull);
+      if (be && P.batch_word_err) atomicAdd(&P.batch_word_err[f / P.batch_frames], 1);
+      c_frames += 1;
+      c_biterr += be;
+      c_worderr += be ? 1 : 0;
+      c_iters += k;
+      c_flips += flips_total;
+      c_stalls += stalled;
+      c_conv += conv;
+      c_edges += (long long)P.n_edges * k;
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && P.counters && c_frames) {
+    unsigned long long *c = (unsigned long long *)P.counters;
+    atomicAdd(c + FWBF_CNT_FRAMES, (unsigned long long)c_frames);
+    atomicAdd(c + FWBF_CNT_BIT_ERRORS, (unsigned long long)c_biterr);
+    atomicAdd(c + FWBF_CNT_WORD_ERRORS, (unsigned long long)c_worderr);
+    atomicAdd(c + FWBF_CNT_ITER_SUM, (unsigned long long)c_iters);
+    atomicAdd(c + FWBF_CNT_FLIP_SUM, (unsigned long long)c_flips);
+    atomicAdd(c + FWBF_CNT_STALLS, (unsigned long long)c_stalls);
+    atomicAdd(c + FWBF_CNT_CONVERGED, (unsigned long long)c_conv);
+    atomicAdd(c + FWBF_CNT_ORDERED_FRAMES, (unsigned long long)c_frames);
+    atomicAdd(c + FWBF_CNT_EDGE_VISITS, (unsigned long long)c_edges);
+  }
+}
+
+} // namespace fwbf

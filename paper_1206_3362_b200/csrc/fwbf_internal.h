@@ -99,4 +99,39 @@ struct KParams {
   int ystage_bytes; // bytes per copy: N * sizeof(YT) rounded up to 16 (<= ld * sizeof(YT))
 };
 
+// One-frame-per-warp FWBF kernel for small explicit codes (fwbf_explicit.cu).
+struct XParams {
+  int n, m, n_edges;
+  int nb, p, lg_g, rounds, slots; // blocks; lanes per block = 2^lg_g; slots per lane per round
+  int kmax, stall, wmode;
+  double alpha;
+  // code tables built on the host per (code, p), copied to shared memory
+  const unsigned long long *tab; // [rounds * slots * 32] per slot: 4 x u16 checks (0xffff none; first 0xfffe: no checks)
+  const uint32_t *rtab;          // [E] row-major edge: slot of its column | (check position in the column) << 16
+  const int *row_ptr;            // [m + 1]
+  const uint16_t *cpos;          // [n] slot of column n
+  int off_tab, off_rtab, off_rptr, off_cpos, off_warp0, warp_bytes;
+  int wo_rec, wo_ys, wo_am, wo_sb, wo_zw, wo_bf;
+  // input / outputs (as KParams)
+  const float *y;
+  long long ld;
+  long long batch;
+  int y_vec4;
+  uint32_t *z_bits;
+  long long z_ld;
+  int *iterations;
+  uint8_t *flags;
+  int *flips_total;
+  int *bit_errors;
+  int *fliplog;
+  int *fliplog_counts;
+  long long fliplog_stride;
+  long long *counters;
+  long long *iter_hist;
+  int *batch_word_err;
+  int batch_frames;
+  const uint32_t *codeword_bits;
+  unsigned int *work_counter;
+};
+
 } // namespace fwbf

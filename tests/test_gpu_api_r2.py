@@ -204,3 +204,31 @@ def test_decode_on_side_stream_orders_inputs(cuda_device):
     res = P.decode_batch(h, yh, cfg, stream=s)    # H2D copy on the current stream
     s.synchronize()
     assert torch.equal(res.iterations, ref.iterations) and torch.equal(res.z_bits, ref.z_bits)
+
+
+@pytest.mark.parametrize("code,alg,kw", [
+    ("eg4", "fwbf", dict(block_len_p=16, k_max=30)), ("eg5", "fwbf", dict(block_len_p=31, k_max=100)),
+    ("eg5", "fwbf", dict(block_len_p=93, k_max=100, stall_policy="terminate")),
+    ("eg5", "imwbf", dict(k_max=60)), ("eg5", "mlp", dict(lam=10, k_max=60)),
+    ("eg5", "imwbf", dict(k_max=60, weight_mode="mwbf", alpha=0.0)), ("eg6", "fwbf", dict(block_len_p=64, k_max=60))])
+@pytest.mark.parametrize("frames", [1, 37, 5000])
+def test_staged_rows_equal_unstaged(cuda_device, monkeypatch, code, alg, kw, frames):
+    """Rows with a 16-byte-multiple stride are staged into shared memory by a
+    TMA bulk copy one frame ahead (row 27 of the scope table); the results
+    must equal the element-wise load path, frame by frame and in the flip log."""
+    import torch
+    h = build_code(code)
+    n = h.n_cols
+    ld = (n + 3) // 4 * 4
+    sigma = O.ebn0_to_sigma(3.5, code_rate(code))
+    g = torch.Generator(device="cuda").manual_seed(frames)
+    buf = torch.full((frames, ld), float("nan"), dtype=torch.float32, device="cuda")  # pad never read as data
+    y = buf[:, :n]
+    y.copy_(1.0 + sigma * torch.randn((frames, n), generator=g, device="cuda"))
+    cfg = P.DecoderConfig(**kw)
+    a = P.decode_batch(h, y, cfg, alg, flip_log=True)
+    monkeypatch.setenv("FWBF_NO_YSTAGE", "1")
+    b = P.decode_batch(h, y, cfg, alg, flip_log=True)
+    for name in ("z_bits", "iterations", "flags", "flips_total", "counters", "iter_hist"):
+        assert torch.equal(getattr(a, name), getattr(b, name)), name
+    assert a.flip_logs() == b.flip_logs()

@@ -1,0 +1,89 @@
+"""The one-frame-per-warp FWBF kernel for small explicit codes (fwbf_explicit.cu):
+bit-exact against the C oracle and against the CTA-per-frame kernel
+(FWBF_NO_WARP=1) -- hard decisions, iterations, flags, flip logs, counters --
+over block lengths (groups of 1..32 lanes per block), stall policies, weight
+modes, float4 and scalar row loads, and a dv = 4 code."""
+
+import numpy as np
+import pytest
+
+from oracle import wbf_oracle as O
+from oracle.c_oracle import COracle
+from paper_1206_3362_b200 import DecoderConfig, ParityCheckMatrix, decode_batch, gallager_rc
+from tests.golden.codebook import build_code, code_rate
+
+pytestmark = pytest.mark.gpu
+
+
+def _y(h, frames, ebn0, rate, seed, pad):
+    import torch
+    n = h.n_cols
+    sigma = O.ebn0_to_sigma(ebn0, rate)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    ld = (n + 3) // 4 * 4 + (4 if pad else 0)
+    buf = torch.zeros((frames, ld if pad else n), dtype=torch.float32, device="cuda")
+    y = buf[:, :n]
+    y.copy_(1.0 + sigma * torch.randn((frames, n), generator=g, device="cuda"))
+    return y
+
+
+def _same(a, b):
+    import torch
+    for name in ("z_bits", "iterations", "flags", "flips_total", "bit_errors", "counters", "iter_hist"):
+        assert torch.equal(getattr(a, name), getattr(b, name)), name
+
+
+@pytest.mark.parametrize("p", [1, 3, 7, 24, 32, 63, 96, 252, 504, 1000])
+@pytest.mark.parametrize("stall", ["flip-global-max", "terminate"])
+def test_warp_kernel_matches_cta_kernel_and_oracle(cuda_device, monkeypatch, p, stall):
+    h = build_code("gal504")
+    y = _y(h, 3000, 3.5, code_rate("gal504"), p, pad=(p % 2 == 0))
+    cfg = DecoderConfig(block_len_p=p, k_max=50, stall_policy=stall)
+    a = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+    monkeypatch.setenv("FWBF_NO_WARP", "1")
+    b = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+    _same(a, b)
+    assert a.flip_logs() == b.flip_logs()
+    z, its, fl, ft = COracle(h).decode_batch(y.cpu().numpy(), algorithm="fwbf", alpha=0.2, k_max=50, p=p,
+                                             stall=stall)
+    assert np.array_equal(a.iterations.cpu().numpy(), its)
+    assert np.array_equal(a.z(), z)
+    assert np.array_equal(a.flips_total.cpu().numpy(), ft)
+
+
+@pytest.mark.parametrize("weight_mode,alpha", [("mwbf", 0.0), ("mwbf", 0.3), ("imwbf", 1.0), ("imwbf", 0.0)])
+def test_warp_kernel_weight_modes(cuda_device, weight_mode, alpha):
+    h = build_code("gal504")
+    y = _y(h, 512, 4.0, code_rate("gal504"), 7, pad=True)
+    cfg = DecoderConfig(block_len_p=24, k_max=40, alpha=alpha, weight_mode=weight_mode)
+    res = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+    logs = res.flip_logs()
+    g = O.Graph.of(h)
+    yy = y.cpu().numpy()
+    for i in range(0, 512, 16):
+        r = O.decode(g, yy[i], "fwbf", alpha=alpha, k_max=40, p=24, weight_mode=weight_mode)
+        assert int(res.iterations[i]) == r.iterations and logs[i] == r.flip_log, i
+
+
+def test_warp_kernel_dv4_and_columns_without_checks(cuda_device):
+    """A (4, 8)-regular code, and an irregular code whose last columns belong to
+    no check (metric = -alpha|y|)."""
+    h = gallager_rc(512, 4, 8, seed=3)
+    y = _y(h, 2000, 4.0, 0.5, 1, pad=True)
+    cfg = DecoderConfig(block_len_p=16, k_max=30)
+    res = decode_batch(h, y, cfg, "fwbf")
+    z, its, fl, ft = COracle(h).decode_batch(y.cpu().numpy(), algorithm="fwbf", alpha=0.2, k_max=30, p=16)
+    assert np.array_equal(res.iterations.cpu().numpy(), its) and np.array_equal(res.z(), z)
+    rng = np.random.default_rng(4)
+    rows = [np.sort(rng.choice(90, size=5, replace=False)) for _ in range(50)]
+    h2 = ParityCheckMatrix(rows, 100)                  # columns 90..99 are in no check
+    y2 = (1.0 + 0.7 * rng.standard_normal((300, 100))).astype(np.float32)
+    y2[:, 95] = -0.5                                   # a hard error no check can see
+    for p in (5, 10, 100):
+        cfg = DecoderConfig(block_len_p=p, k_max=20, alpha=0.5)
+        res = decode_batch(h2, y2, cfg, "fwbf", flip_log=True)
+        logs = res.flip_logs()
+        g = O.Graph.of(h2)
+        for i in range(0, 300, 7):
+            r = O.decode(g, y2[i], "fwbf", alpha=0.5, k_max=20, p=p)
+            assert int(res.iterations[i]) == r.iterations and logs[i] == r.flip_log, (p, i)

@@ -77,7 +77,12 @@ def test_sweep_parity_vs_c_oracle(cuda_device, code, p, ebn0, frames, kmax):
     h = build_code(code)
     sigma = O.ebn0_to_sigma(ebn0, code_rate(code))
     g = torch.Generator(device="cuda").manual_seed(int(ebn0 * 10) * 1000 + p)
-    y = (1.0 + sigma * torch.randn((frames, h.n_cols), generator=g, device="cuda")).float()
+    # rows padded to a 16-byte multiple (ld = 1024 / 4096): the circulant
+    # kernels then stage each frame's row with a TMA bulk copy one frame ahead
+    ld = (h.n_cols + 3) // 4 * 4
+    ybuf = torch.zeros((frames, ld), dtype=torch.float32, device="cuda")
+    y = ybuf[:, :h.n_cols]
+    y.copy_(1.0 + sigma * torch.randn((frames, h.n_cols), generator=g, device="cuda"))
     cfg = DecoderConfig(block_len_p=p, k_max=kmax)
     dc = device_code(h, 0)
     dc.filter_stats(reset=True)
