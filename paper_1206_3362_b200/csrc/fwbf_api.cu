@@ -27,7 +27,7 @@ __global__ void decode_kernel(const __grid_constant__ KParams P);
 template <typename YT>
 __global__ void noise_kernel(unsigned long long seed, long long first, long long count, double sigma,
                              const uint32_t *codeword, YT *y, long long ld, int n, int pm);
-__global__ void xdecode_kernel(const __grid_constant__ XParams P);
+template <int DV> __global__ void xdecode_kernel(const __grid_constant__ XParams P);
 template <typename T> __global__ void stage_hard_decision(const T *, long long, uint8_t *);
 __global__ void stage_syndrome(const int *, const int *, int, int, const uint8_t *, long long, uint8_t *);
 __global__ void stage_weights(const int *, const int *, int, long long, const double *, long long, long long,
@@ -78,13 +78,16 @@ struct DeviceGuard {
 
 // One-frame-per-warp explicit-code plan (fwbf_explicit.cu), built per (code, p).
 struct XPlan {
-  int p = 0, nb = 0, lg_g = 0, rounds = 0, slots = 0;
+  int p = 0, nb = 0, lg_g = 0, rounds = 0, slots = 0, dv = 0;
+  const void *kern = nullptr;
   unsigned long long *d_tab = nullptr;
   uint32_t *d_rtab = nullptr;
   uint16_t *d_cpos = nullptr;
+  int *d_invp = nullptr;
+  int s2sh = 0;
   int tables_bytes = 0, warp_bytes = 0;
   int wo_rec = 0, wo_ys = 0, wo_am = 0, wo_sb = 0, wo_zw = 0, wo_bf = 0;
-  int off_tab = 0, off_rtab = 0, off_rptr = 0, off_cpos = 0;
+  int off_tab = 0, off_cpos = 0;
   int wpc = 0, per_sm = 0, smem = 0; // warps per CTA, CTAs per SM, dynamic smem bytes
   bool ok = false;
 };
@@ -324,6 +327,7 @@ extern "C" int fwbf_code_destroy(fwbf_code *c) {
     cudaFree(x.d_tab);
     cudaFree(x.d_rtab);
     cudaFree(x.d_cpos);
+    cudaFree(x.d_invp);
   }
   delete c;
   return FWBF_OK;
@@ -527,7 +531,10 @@ static int build_xplan(fwbf_code *c, int p, XPlan *out) {
   x.p = p;
   const int n = c->n, m = c->m;
   x.nb = (n + p - 1) / p;
-  if (c->dv_max > 4 || m > 2048 || n > 0xffff || c->n_edges > (1 << 24)) { *out = x; return FWBF_OK; }
+  // record byte offsets (16 * check, two constant records after the M
+  // checks) must fit 16 bits
+  if (c->dv_max > 4 || m + 2 > 4096 || n > 0xffff || c->n_edges > (1 << 24)) { *out = x; return FWBF_OK; }
+  x.dv = std::max(2, c->dv_max);
   long best_cost = -1;
   for (int lg = 0; lg <= 5; ++lg) {
     const int G = 1 << lg;
@@ -538,7 +545,61 @@ static int build_xplan(fwbf_code *c, int p, XPlan *out) {
   }
   if (best_cost < 0) { *out = x; return FWBF_OK; }
   const int G = 1 << x.lg_g, R = x.rounds, S = x.slots, nslot = R * S * 32;
-  std::vector<unsigned long long> tab(nslot, ~0ull);
+  // slot -> column (or -1) first; the check labels depend on which checks
+  // share a load instruction
+  std::vector<int> scol(nslot, -1);
+  for (int r = 0; r < R; ++r)
+    for (int cc = 0; cc < S; ++cc)
+      for (int l = 0; l < 32; ++l) {
+        const int b = r * (32 / G) + l / G, sub = l % G;
+        if (b >= x.nb) continue;
+        const int base = b * p, lim = std::min(p, n - base);
+        if (sub + G * cc < lim) scol[(r * S + cc) * 32 + l] = base + sub + G * cc;
+      }
+  // Labels: the q-th check of the 32 slots (r, c, *) is one LDS.64 of 32
+  // lanes; an 8-byte record at label j sits in bank pair j mod 16.  Greedy:
+  // checks by decreasing number of loads, each to the bank pair (with labels
+  // left) least used by the loads it takes part in.
+  std::vector<int> lab(m, -1);
+  {
+    const int ninstr = R * S * 4;
+    std::vector<std::vector<int>> loads(m); // instructions per check
+    for (int r = 0; r < R; ++r)
+      for (int cc = 0; cc < S; ++cc)
+        for (int l = 0; l < 32; ++l) {
+          const int col = scol[(r * S + cc) * 32 + l];
+          if (col < 0) continue;
+          for (int e = c->h_col_ptr[col], q = 0; e < c->h_col_ptr[col + 1]; ++e, ++q)
+            loads[c->h_col_idx[e]].push_back((r * S + cc) * 4 + q);
+        }
+    std::vector<int> order(m);
+    for (int i = 0; i < m; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b2) { return loads[a].size() > loads[b2].size(); });
+    std::vector<int> cnt((size_t)ninstr * 16, 0), cap(16, 0), next(16, 0);
+    for (int j = 0; j < m; ++j) cap[j % 16]++;
+    for (int k = 0; k < 16; ++k) next[k] = k;
+    for (int chk : order) {
+      int bestk = -1;
+      long bestc = 0;
+      for (int k = 0; k < 16; ++k) {
+        if (!cap[k]) continue;
+        long cst = 0;
+        for (int ins : loads[chk]) cst += cnt[(size_t)ins * 16 + k];
+        if (bestk < 0 || cst < bestc) { bestk = k; bestc = cst; }
+      }
+      for (int ins : loads[chk]) cnt[(size_t)ins * 16 + bestk]++;
+      cap[bestk]--;
+      lab[chk] = next[bestk];
+      next[bestk] += 16;
+    }
+  }
+  std::vector<int> invp(m);
+  for (int i = 0; i < m; ++i) invp[lab[i]] = i;
+  // padding slots read the (-inf, -inf) label m on every edge
+  unsigned long long padw = 0;
+  for (int q = 0; q < 4; ++q) padw |= (unsigned long long)(8 * m) << (16 * q);
+  std::vector<unsigned long long> tab(nslot, padw);
   std::vector<uint16_t> cpos(n, 0);
   for (int r = 0; r < R; ++r)
     for (int cc = 0; cc < S; ++cc)
@@ -548,13 +609,14 @@ static int build_xplan(fwbf_code *c, int p, XPlan *out) {
         const int base = b * p, lim = std::min(p, n - base);
         if (sub + G * cc >= lim) continue;
         const int col = base + sub + G * cc, pos = (r * S + cc) * 32 + l;
-        unsigned long long w = ~0ull;
+        // byte offsets of the column's check records, ascending checks; the
+        // (0, 0) label m + 1 fills the edges it does not have
+        unsigned long long w = 0;
         const int e0 = c->h_col_ptr[col], e1 = c->h_col_ptr[col + 1];
-        for (int e = e0; e < e1; ++e) {
-          w &= ~(0xffffull << (16 * (e - e0)));
-          w |= (unsigned long long)c->h_col_idx[e] << (16 * (e - e0));
+        for (int q = 0; q < 4; ++q) {
+          const int j = e0 + q < e1 ? lab[c->h_col_idx[e0 + q]] : m + 1;
+          w |= (unsigned long long)(8 * j) << (16 * q);
         }
-        if (e0 == e1) w = (w & ~0xffffull) | 0xfffeull; // a column without checks
         tab[pos] = w;
         cpos[col] = (uint16_t)pos;
       }
@@ -570,13 +632,13 @@ static int build_xplan(fwbf_code *c, int p, XPlan *out) {
   int o = 0;
   auto take = [&](int bytes) { int r0 = o; o = align16(o + bytes); return r0; };
   x.off_tab = take(nslot * 8);
-  x.off_rtab = take((int)c->n_edges * 4);
-  x.off_rptr = take((m + 1) * 4);
   x.off_cpos = take(n * 2);
   x.tables_bytes = o;
   int w = 0;
   auto wtake = [&](int bytes) { int r0 = w; w = align16(w + bytes); return r0; };
-  x.wo_rec = wtake(m * 16);
+  x.s2sh = 7;
+  while ((1 << x.s2sh) < 8 * (m + 2)) ++x.s2sh;
+  x.wo_rec = wtake((1 << x.s2sh) + 8 * (m + 2));
   x.wo_ys = wtake(nslot * 4);
   x.wo_am = wtake(nslot);
   x.wo_sb = wtake(((m + 31) / 32) * 4);
@@ -584,7 +646,9 @@ static int build_xplan(fwbf_code *c, int p, XPlan *out) {
   x.wo_bf = wtake(x.nb * 4);
   x.warp_bytes = w;
   // warps per CTA: the most resident warps per SM
-  const void *kern = (const void *)fwbf::xdecode_kernel;
+  const void *kern = x.dv == 2 ? (const void *)fwbf::xdecode_kernel<2>
+                     : x.dv == 3 ? (const void *)fwbf::xdecode_kernel<3> : (const void *)fwbf::xdecode_kernel<4>;
+  x.kern = kern;
   int best_warps = 0;
   for (int wpc : {8, 4, 2, 1}) {
     const int smem = x.tables_bytes + wpc * x.warp_bytes;
@@ -595,10 +659,12 @@ static int build_xplan(fwbf_code *c, int p, XPlan *out) {
   }
   if (best_warps < 8) { *out = x; return FWBF_OK; } // too few frames in flight: the CTA kernel wins
   int rc;
-  if ((rc = upload(&x.d_tab, tab)) || (rc = upload(&x.d_rtab, rtab)) || (rc = upload(&x.d_cpos, cpos))) {
+  if ((rc = upload(&x.d_tab, tab)) || (rc = upload(&x.d_rtab, rtab)) || (rc = upload(&x.d_cpos, cpos)) ||
+      (rc = upload(&x.d_invp, invp))) {
     cudaFree(x.d_tab);
     cudaFree(x.d_rtab);
     cudaFree(x.d_cpos);
+    cudaFree(x.d_invp);
     return rc;
   }
   x.ok = true;
@@ -626,9 +692,10 @@ static int launch_explicit(fwbf_code *c, const fwbf_params *p, const XPlan &x, c
   P.rtab = x.d_rtab;
   P.row_ptr = c->d_row_ptr;
   P.cpos = x.d_cpos;
+  P.invp = x.d_invp;
+  P.s2sh = x.s2sh;
+  P.s2off = 1 << x.s2sh;
   P.off_tab = x.off_tab;
-  P.off_rtab = x.off_rtab;
-  P.off_rptr = x.off_rptr;
   P.off_cpos = x.off_cpos;
   P.off_warp0 = x.tables_bytes;
   P.warp_bytes = x.warp_bytes;
@@ -661,8 +728,7 @@ static int launch_explicit(fwbf_code *c, const fwbf_params *p, const XPlan &x, c
   const long long grid = std::min<long long>((batch + x.wpc - 1) / x.wpc, (long long)x.per_sm * c->sm_count);
   CUDA_TRY(cudaMemsetAsync(P.work_counter, 0, sizeof(unsigned), stream));
   void *args[] = {&P};
-  CUDA_TRY(cudaLaunchKernel((const void *)fwbf::xdecode_kernel, dim3((unsigned)grid), dim3(32 * x.wpc), args,
-                            x.smem, stream));
+  CUDA_TRY(cudaLaunchKernel(x.kern, dim3((unsigned)grid), dim3(32 * x.wpc), args, x.smem, stream));
   CUDA_TRY(cudaGetLastError());
   return FWBF_OK;
 }

@@ -11,10 +11,19 @@
 //     sub, sub + G, ... of its block in ascending order ("slots");
 //   * slot (round r, step c) of lane l lives at position pos = (r S + c) 32 + l,
 //     so every per-slot array is read conflict-free (consecutive lanes,
-//     consecutive words); tab[pos] packs the column's <= 4 check indices
-//     (ascending, 16 bits each);
-//   * per check one 16-byte record (sgn min1, sgn min2) in fp64: an edge is
-//     one LDS.64 whose address picks min1 or min2 by the column's argmin bit.
+//     consecutive words); tab[pos] packs the byte offsets of the column's
+//     <= DV check records (ascending checks, 16 bits each);
+//   * per check sgn min1 and sgn min2 in fp64, in two arrays S2OFF bytes apart
+//     (S2OFF a power of two >= 128, so both copies of a check sit in the same
+//     bank): an edge is one LDS.64 whose address picks min2 (+S2OFF) by the
+//     column's argmin bit.  Checks are stored under a host-chosen label
+//     (a permutation): lanes of one load instruction read checks whose labels
+//     are spread over the 16 bank pairs, so most loads take the minimum two
+//     wavefronts instead of the ~3.7 of arbitrary labels.  Two constant
+//     labels end the arrays: (-inf, -inf) fills the edges of padding slots
+//     (their metric is -inf, never a maximum) and (0, 0) the missing edges of
+//     columns lighter than DV (adding +0.0 to a sum that started at +0.0
+//     changes nothing), so the loop has no branches.
 //
 // Per frame (decoders.py:189-229): y (float4 loads when rows are 16-byte
 // aligned) -> signed y per slot + hard decisions; per check min1 / min2 /
@@ -24,7 +33,7 @@
 // decoders.py:148-153), the block argmax with lowest-index ties and the > 0
 // threshold (decoders.py:156-167, 181-183), the stall policy
 // (decoders.py:214-222), and the flips: z and syndrome bits toggled by
-// atomic XOR, the checks' record signs by 64-bit atomic XOR of the sign bits
+// atomic XOR, the checks' record signs by atomic XOR of the sign bits
 // (XOR commutes, so two flips toggling one check cancel exactly).  (An
 // owner-lane refresh of the records instead of the sign atomics -- every lane
 // rescans its checks' syndrome words -- measured 7 % slower on Gallager(504).)
@@ -41,26 +50,25 @@ namespace fwbf {
 
 __device__ __forceinline__ double xdinf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
+template <int DV>
 __global__ void __launch_bounds__(256) xdecode_kernel(const __grid_constant__ XParams P) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N = P.n, M = P.m, R = P.rounds, S = P.slots, G = 1 << P.lg_g;
   const int nslot = R * S * 32;
 
-  // ---- CTA-shared code tables (same for every frame) ----
+  // ---- CTA-shared code tables (same for every frame); the row tables used
+  // only at frame init stay in global memory (L1/L2) ----
   unsigned long long *tab = reinterpret_cast<unsigned long long *>(sm + P.off_tab);
-  uint32_t *rtab = reinterpret_cast<uint32_t *>(sm + P.off_rtab);
-  int *rptr = reinterpret_cast<int *>(sm + P.off_rptr);
   uint16_t *cpos = reinterpret_cast<uint16_t *>(sm + P.off_cpos);
+  const uint32_t *rtab = P.rtab;
+  const int *rptr = P.row_ptr;
   for (int i = tid; i < nslot; i += blockDim.x) tab[i] = __ldg(P.tab + i);
-  for (int i = tid; i < P.n_edges; i += blockDim.x) rtab[i] = __ldg(P.rtab + i);
-  for (int i = tid; i <= M; i += blockDim.x) rptr[i] = __ldg(P.row_ptr + i);
   for (int i = tid; i < N; i += blockDim.x) cpos[i] = __ldg(P.cpos + i);
-  __syncthreads();
 
   // ---- this warp's frame state ----
   unsigned char *W = sm + P.off_warp0 + warp * P.warp_bytes;
-  double *rec = reinterpret_cast<double *>(W + P.wo_rec);      // [2M]: sgn*min1, sgn*min2
+  double *rec = reinterpret_cast<double *>(W + P.wo_rec);      // by label: sgn*min1; + S2OFF: sgn*min2
   float *ys = reinterpret_cast<float *>(W + P.wo_ys);           // [nslot] signed y per slot (-0 -> +0)
   uint8_t *am = W + P.wo_am;                                    // [nslot] argmin bits per slot
   uint32_t *sb = reinterpret_cast<uint32_t *>(W + P.wo_sb);     // syndrome bits
@@ -69,6 +77,15 @@ __global__ void __launch_bounds__(256) xdecode_kernel(const __grid_constant__ XP
   const int zwords = (N + 31) >> 5;
   const bool imw = P.wmode == FWBF_WEIGHTS_IMWBF;
   const double alpha = P.alpha;
+  if (lane == 0) { // the two constant records after the M check records
+    double *rec2 = rec + (P.s2off >> 3);
+    rec[M] = rec2[M] = -xdinf();
+    rec[M + 1] = rec2[M + 1] = 0.0;
+  }
+  __syncthreads();
+  const uint32_t recb = (uint32_t)__cvta_generic_to_shared(rec);
+  double *rec2 = rec + (P.s2off >> 3);
+  const int s2sh = P.s2sh; // S2OFF = 1 << s2sh
 
   long long c_frames = 0, c_biterr = 0, c_worderr = 0, c_iters = 0, c_flips = 0, c_stalls = 0, c_conv = 0,
             c_edges = 0;
@@ -118,17 +135,19 @@ __global__ void __launch_bounds__(256) xdecode_kernel(const __grid_constant__ XP
     nonfin = __any_sync(XFULL, nonfin);
     __syncwarp();
 
-    // ---- per-check minima, argmin, parity (ascending columns, strict <) ----
+    // ---- per-check minima, argmin, parity (ascending columns, strict <),
+    // lanes over labels j (check invp[j]) ----
     int swt = 0;
     for (int m0 = 0; m0 < M; m0 += 32) {
-      const int m = m0 + lane;
+      const int j = m0 + lane;
       uint32_t par = 0;
-      if (m < M) {
+      if (j < M) {
+        const int m = __ldg(P.invp + j);
         float min1 = INFINITY, min2 = INFINITY;
         int ae = -1;
-        const int e1 = rptr[m + 1];
-        for (int e = rptr[m]; e < e1; ++e) {
-          const float v = ys[rtab[e] & 0xffffu];
+        const int e1 = __ldg(rptr + m + 1);
+        for (int e = __ldg(rptr + m); e < e1; ++e) {
+          const float v = ys[__ldg(rtab + e) & 0xffffu];
           par ^= __float_as_uint(v);
           const float a = fabsf(v);
           const bool lt = a < min1;
@@ -139,10 +158,10 @@ __global__ void __launch_bounds__(256) xdecode_kernel(const __grid_constant__ XP
         par >>= 31;
         const double sg = par ? 1.0 : -1.0;
         // MWBF (include-self minimum): every edge reads min1
-        *reinterpret_cast<double2 *>(rec + 2 * m) =
-            make_double2(sg * (double)min1, sg * (double)(imw ? min2 : min1));
+        rec[j] = sg * (double)min1;
+        rec2[j] = sg * (double)(imw ? min2 : min1);
         if (imw && ae >= 0) { // the argmin column reads min2 at this check's position in its list
-          const uint32_t pe = rtab[ae];
+          const uint32_t pe = __ldg(rtab + ae);
           const uint32_t pos = pe & 0xffffu;
           atomicOr(reinterpret_cast<uint32_t *>(am) + (pos >> 2), (1u << (pe >> 16)) << (8 * (pos & 3)));
         }
@@ -170,17 +189,18 @@ __global__ void __launch_bounds__(256) xdecode_kernel(const __grid_constant__ XP
         for (int c = 0; c < S; ++c) {
           const int pos = pos0 + c * 32;
           const unsigned long long w = tab[pos];
-          if ((uint32_t)(w & 0xffffu) != 0xffffu) { // a column (0xfffe: a column without checks)
-            const uint32_t amk = am[pos];
-            double acc = 0.0;
+          const uint32_t amk = am[pos];
+          double acc = 0.0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint32_t idx = (uint32_t)(w >> (16 * q)) & 0xffffu;
-              if (idx < 0xfffeu) acc = __dadd_rn(acc, rec[2 * idx + ((amk >> q) & 1u)]);
-            }
-            const double e = __dsub_rn(acc, __dmul_rn(alpha, (double)fabsf(ys[pos])));
-            if (e > best) { best = e; bc = c; }
+          for (int q = 0; q < DV; ++q) {
+            // record byte offset, + S2OFF (min2) when this check's argmin is the column
+            const uint32_t off = ((uint32_t)(w >> (16 * q)) & 0xffffu) | ((amk << (s2sh - q)) & (1u << s2sh));
+            double v;
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(recb + off));
+            acc = __dadd_rn(acc, v);
           }
+          const double e = __dsub_rn(acc, __dmul_rn(alpha, (double)fabsf(ys[pos])));
+          if (e > best) { best = e; bc = c; }
         }
         // group butterfly: value desc, column asc (column = base + sub + G c)
         const int b = r * (32 >> P.lg_g) + (lane >> P.lg_g);
@@ -231,15 +251,16 @@ __global__ void __launch_bounds__(256) xdecode_kernel(const __grid_constant__ XP
           atomicXor(&zw[c >> 5], 1u << (c & 31));
           const unsigned long long w = tab[cpos[c]];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint32_t m = (uint32_t)(w >> (16 * q)) & 0xffffu;
-            if (m < 0xfffeu) {
+          for (int q = 0; q < DV; ++q) {
+            const uint32_t m = ((uint32_t)(w >> (16 * q)) & 0xffffu) >> 3; // label
+            if (m < (uint32_t)M) { // not the (0, 0) record of a missing edge
               const uint32_t old = atomicXor(&sb[m >> 5], 1u << (m & 31));
               dsw += ((old >> (m & 31)) & 1u) ? -1 : 1;
-              // negate sgn*min1 and sgn*min2 of the toggled check
-              unsigned long long *r2 = reinterpret_cast<unsigned long long *>(rec + 2 * m);
-              atomicXor(r2, 0x8000000000000000ull);
-              atomicXor(r2 + 1, 0x8000000000000000ull);
+              // negate sgn*min1 and sgn*min2 of the toggled check: XOR of the
+              // sign bit in each double's high word (32-bit shared atomics are
+              // native; 64-bit XOR would be a CAS loop)
+              atomicXor(reinterpret_cast<uint32_t *>(rec + m) + 1, 0x80000000u);
+              atomicXor(reinterpret_cast<uint32_t *>(rec2 + m) + 1, 0x80000000u);
             }
           }
         }
@@ -295,5 +316,9 @@ __global__ void __launch_bounds__(256) xdecode_kernel(const __grid_constant__ XP
     atomicAdd(c + FWBF_CNT_EDGE_VISITS, (unsigned long long)c_edges);
   }
 }
+
+template __global__ void xdecode_kernel<2>(const __grid_constant__ XParams);
+template __global__ void xdecode_kernel<3>(const __grid_constant__ XParams);
+template __global__ void xdecode_kernel<4>(const __grid_constant__ XParams);
 
 } // namespace fwbf

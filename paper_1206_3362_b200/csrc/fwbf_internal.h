@@ -106,11 +106,13 @@ struct XParams {
   int kmax, stall, wmode;
   double alpha;
   // code tables built on the host per (code, p), copied to shared memory
-  const unsigned long long *tab; // [rounds * slots * 32] per slot: 4 x u16 checks (0xffff none; first 0xfffe: no checks)
+  const unsigned long long *tab; // [rounds * slots * 32] per slot: 4 x u16 byte offsets of the column's check records
   const uint32_t *rtab;          // [E] row-major edge: slot of its column | (check position in the column) << 16
   const int *row_ptr;            // [m + 1]
   const uint16_t *cpos;          // [n] slot of column n
-  int off_tab, off_rtab, off_rptr, off_cpos, off_warp0, warp_bytes;
+  const int *invp;               // [m] check stored under label j (labels spread bank pairs)
+  int s2off, s2sh;               // min2 array offset in bytes (= 1 << s2sh) from the min1 array
+  int off_tab, off_cpos, off_warp0, warp_bytes;
   int wo_rec, wo_ys, wo_am, wo_sb, wo_zw, wo_bf;
   // input / outputs (as KParams)
   const float *y;
