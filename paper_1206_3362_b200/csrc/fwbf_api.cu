@@ -28,6 +28,7 @@ template <typename YT>
 __global__ void noise_kernel(unsigned long long seed, long long first, long long count, double sigma,
                              const uint32_t *codeword, YT *y, long long ld, int n, int pm);
 template <int DV> __global__ void xdecode_kernel(const __grid_constant__ XParams P);
+template <int TPC> __global__ void qdecode_kernel(const __grid_constant__ QParams P);
 template <typename T> __global__ void stage_hard_decision(const T *, long long, uint8_t *);
 __global__ void stage_syndrome(const int *, const int *, int, int, const uint8_t *, long long, uint8_t *);
 __global__ void stage_weights(const int *, const int *, int, long long, const double *, long long, long long,
@@ -733,6 +734,86 @@ static int launch_explicit(fwbf_code *c, const fwbf_params *p, const XPlan &x, c
   return FWBF_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Quasi-cyclic codes, FWBF with 32 | p, blocks inside block columns (fwbf_qc.cu)
+// ---------------------------------------------------------------------------
+static int launch_qc(fwbf_code *c, const fwbf_params *p, const float *y, long long batch, long long ld,
+                     const fwbf_outputs &o, cudaStream_t stream, bool *used) {
+  *used = false;
+  const int Z = c->qc_z, pp = p->block_len_p;
+  if (!Z || c->qc_jb > 4 || pp % 32 || pp > Z || Z % pp || c->n > 0xffff || c->m > 32 * 512) return FWBF_OK;
+  const int tpc = pp / 32;
+  const void *kern = tpc == 1 ? (const void *)fwbf::qdecode_kernel<1>
+                   : tpc == 2 ? (const void *)fwbf::qdecode_kernel<2>
+                   : tpc == 4 ? (const void *)fwbf::qdecode_kernel<4>
+                   : tpc == 8 ? (const void *)fwbf::qdecode_kernel<8>
+                   : tpc == 16 ? (const void *)fwbf::qdecode_kernel<16> : nullptr;
+  if (!kern) return FWBF_OK;
+  fwbf::QParams P;
+  memset(&P, 0, sizeof P);
+  P.n = c->n;
+  P.m = c->m;
+  P.n_edges = (int)c->n_edges;
+  P.z = Z;
+  P.lgz = 0;
+  while ((1 << P.lgz) < Z) ++P.lgz;
+  P.jb = c->qc_jb;
+  P.kb = c->qc_kb;
+  P.head = pp;
+  memcpy(P.shift, c->qc_shift, sizeof P.shift);
+  P.nb = c->n / pp;
+  P.kmax = p->k_max;
+  P.stall = p->stall;
+  P.wmode = p->weight_mode;
+  P.alpha = p->alpha;
+  int off = 0;
+  auto take = [&](int bytes) { int r0 = off; off = align16(off + bytes); return r0; };
+  P.off_y = take(c->n * 4);
+  P.off_rec = take(P.jb * (Z + pp) * 8);
+  P.off_amc = take(P.jb * (Z + pp) * 2);
+  P.off_zrec = take(pp * 8);
+  P.off_zamc = take(pp * 2);
+  P.off_sbits = take(((c->m + 31) / 32) * 4);
+  P.off_zbits = take(((c->n + 31) / 32) * 4);
+  P.off_blkv = take(P.nb * 8);
+  P.off_blki = take(P.nb * 4);
+  P.off_misc = take(16 * 4);
+  const int smem = off;
+  if (smem > c->smem_optin) return FWBF_OK;
+  const int T = 512;
+  int per_sm = 0;
+  int rc = plan_occupancy(c->device, kern, T, smem, &per_sm);
+  if (rc) return rc;
+  if (per_sm < 1) return FWBF_OK;
+  P.y = y;
+  P.ld = ld;
+  P.batch = batch;
+  P.y_vec4 = ((uintptr_t)y % 16) == 0 && ld % 4 == 0;
+  P.z_bits = o.z_bits;
+  P.z_ld = o.z_ld;
+  P.iterations = o.iterations;
+  P.flags = o.flags;
+  P.flips_total = o.flips_total;
+  P.bit_errors = o.bit_errors;
+  P.fliplog = o.fliplog;
+  P.fliplog_counts = o.fliplog_counts;
+  P.fliplog_stride = o.fliplog_stride;
+  P.counters = (long long *)o.counters;
+  P.iter_hist = (long long *)o.iter_hist;
+  P.batch_word_err = o.batch_word_err;
+  P.batch_frames = o.batch_frames;
+  P.codeword_bits = o.codeword_bits;
+  const unsigned slot = c->work_slot.fetch_add(1) % kWorkRing;
+  P.work_counter = c->d_work + slot;
+  const long long grid = std::min<long long>(batch, (long long)per_sm * c->sm_count);
+  CUDA_TRY(cudaMemsetAsync(P.work_counter, 0, sizeof(unsigned), stream));
+  void *args[] = {&P};
+  CUDA_TRY(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(T), args, smem, stream));
+  CUDA_TRY(cudaGetLastError());
+  *used = true;
+  return FWBF_OK;
+}
+
 // The plan for (c, p), built on first use; nullptr when the kernel does not apply.
 static const XPlan *get_xplan(fwbf_code *c, int p, int *rc) {
   *rc = FWBF_OK;
@@ -769,6 +850,12 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
 
   DeviceGuard dg;
   CUDA_TRY(cudaSetDevice(c->device));
+  if (!c->circ && c->qc_z && sizeof(YT) == 4 && p->algorithm == FWBF_ALG_FWBF && !metric_out &&
+      !getenv("FWBF_NO_QC") && !getenv("FWBF_NO_QCK")) {
+    bool used = false;
+    rc = launch_qc(c, p, (const float *)y, batch, ld, o, stream, &used);
+    if (rc || used) return rc;
+  }
   if (!c->circ && sizeof(YT) == 4 && p->algorithm == FWBF_ALG_FWBF && !metric_out && !getenv("FWBF_NO_WARP")) {
     const XPlan *xp = get_xplan(c, p->block_len_p, &rc);
     if (rc) return rc;

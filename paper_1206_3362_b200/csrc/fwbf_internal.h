@@ -136,4 +136,34 @@ struct XParams {
   unsigned int *work_counter;
 };
 
+// Quasi-cyclic FWBF kernel (fwbf_qc.cu): one frame per CTA, fused metric + block argmax.
+struct QParams {
+  int n, m, n_edges;
+  int z, lgz, jb, kb, head; // circulant size, log2, row / column blocks, doubled head (= p)
+  short shift[kMaxQcBlocks]; // [jb][kb], -1 = zero block
+  int nb;                    // blocks (p = 32 * TPC columns each)
+  int kmax, stall, wmode;
+  double alpha;
+  int off_y, off_rec, off_amc, off_zrec, off_zamc, off_sbits, off_zbits, off_blkv, off_blki, off_misc;
+  const float *y;
+  long long ld;
+  long long batch;
+  int y_vec4;
+  uint32_t *z_bits;
+  long long z_ld;
+  int *iterations;
+  uint8_t *flags;
+  int *flips_total;
+  int *bit_errors;
+  int *fliplog;
+  int *fliplog_counts;
+  long long fliplog_stride;
+  long long *counters;
+  long long *iter_hist;
+  int *batch_word_err;
+  int batch_frames;
+  const uint32_t *codeword_bits;
+  unsigned int *work_counter;
+};
+
 } // namespace fwbf

@@ -1,0 +1,332 @@
+// fwbf_qc.cu -- FWBF on quasi-cyclic codes (config D): one frame per CTA, the
+// Eq.(1) metric fused with the block argmax, H as circulant shifts only.
+//
+// H is jb x kb circulant blocks of size Z (Z a power of two): row r Z + i
+// holds column c Z + ((i + s_rc) mod Z) (qc_from_shifts; an absent block has
+// no shift).  Column c Z + o meets row block r at check r Z + ((o - s_rc) mod Z),
+// so the checks of a column ascend with r -- the reference's ascending check
+// order (decoders.py:148-153).
+//
+// A p-block (32 | p, inside one block column) belongs to one warp; lane l
+// takes columns base + l + 32 t (t < p / 32).  Its check in row block r is
+// i0 + 32 t with i0 = (o0 + l - s) mod Z, so with each row block's records
+// stored twice over their first p entries ("doubled head") the lane's
+// records are rec_r[i0 + 32 t]: a pointer per row block and an immediate
+// offset per t -- no index arithmetic per edge.  An absent block points at a
+// row of zero records.  Per edge: the check's argmin column (u16), its
+// (sgn min1, sgn min2) float pair, a select, float -> double, one DADD in
+// ascending check order from +0.0 (adding the +0.0 of an absent block to a
+// sum that started at +0.0 is the identity) -- the reference's fp64 sum.
+//
+// Flips toggle z and syndrome words (atomic XOR); after a CTA barrier every
+// thread negates the records of its own checks whose syndrome bit changed
+// (plain loads/stores, both copies of head entries).  Frame init computes
+// per check min1 / min2 / argmin / parity walking its columns in ascending
+// order (strict <: the first minimum, decoders.py:87-103).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "fwbf_b200.h"
+#include "fwbf_internal.h"
+
+namespace fwbf {
+
+#define QFULL 0xffffffffu
+
+__device__ __forceinline__ double qdinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+
+template <int TPC> // columns per lane per block (p / 32)
+__global__ void __launch_bounds__(512, 2) qdecode_kernel(const __grid_constant__ QParams P) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int T = blockDim.x;
+  const int N = P.n, M = P.m, Z = P.z, lgz = P.lgz, H = P.head, RS = P.z + P.head;
+  float *ys = reinterpret_cast<float *>(sm + P.off_y);           // signed y, -0 -> +0
+  float2 *rec = reinterpret_cast<float2 *>(sm + P.off_rec);      // [jb][Z + H] (sgn min1, sgn min2)
+  uint16_t *amc = reinterpret_cast<uint16_t *>(sm + P.off_amc);  // [jb][Z + H] argmin column
+  const float2 *rzero = reinterpret_cast<const float2 *>(sm + P.off_zrec); // [H] (0, 0)
+  const uint16_t *azero = reinterpret_cast<const uint16_t *>(sm + P.off_zamc); // [H] 0xffff
+  uint32_t *sbits = reinterpret_cast<uint32_t *>(sm + P.off_sbits);
+  uint32_t *zbits = reinterpret_cast<uint32_t *>(sm + P.off_zbits);
+  double *blk_v = reinterpret_cast<double *>(sm + P.off_blkv);
+  int *blk_i = reinterpret_cast<int *>(sm + P.off_blki);
+  int *misc = reinterpret_cast<int *>(sm + P.off_misc);
+  enum { Q_FRAME = 0, Q_SWT, Q_F, Q_FLIP, Q_BE };
+  const bool imw = P.wmode == FWBF_WEIGHTS_IMWBF;
+  const double alpha = P.alpha;
+  const int zw = (N + 31) >> 5, nKm = (M + T - 1) / T;
+
+  for (int i = tid; i < H; i += T) {
+    const_cast<float2 *>(rzero)[i] = make_float2(0.f, 0.f);
+    const_cast<uint16_t *>(azero)[i] = 0xffffu;
+  }
+  long long c_frames = 0, c_biterr = 0, c_worderr = 0, c_iters = 0, c_flips = 0, c_stalls = 0, c_conv = 0,
+            c_edges = 0;
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) misc[Q_FRAME] = (int)atomicAdd(P.work_counter, 1u);
+    __syncthreads();
+    const long long f = (long long)(unsigned)misc[Q_FRAME];
+    if (f >= P.batch) break;
+
+    // ---- init 1: y (float4 loads), hard decisions ----
+    const float *yr = P.y + f * P.ld;
+    bool nonfin = false;
+    if (P.y_vec4) {
+      for (int n0 = 4 * tid; n0 < N; n0 += 4 * T) {
+        const float4 v4 = __ldg(reinterpret_cast<const float4 *>(yr + n0));
+        const float vv[4] = {v4.x + 0.0f, v4.y + 0.0f, v4.z + 0.0f, v4.w + 0.0f}; // -0.0 -> +0.0
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (n0 + u < N) {
+            ys[n0 + u] = vv[u];
+            nonfin |= !isfinite(vv[u]);
+          }
+      }
+    } else {
+      for (int n = tid; n < N; n += T) {
+        const float v = __ldg(yr + n) + 0.0f;
+        ys[n] = v;
+        nonfin |= !isfinite(v);
+      }
+    }
+    if (tid == 0) { misc[Q_SWT] = 0; misc[Q_F] = 0; misc[Q_FLIP] = 0; }
+    nonfin = __syncthreads_or(nonfin);
+    for (int w0 = warp * 32; w0 < N; w0 += T) {
+      const int n = w0 + lane;
+      const uint32_t b = __ballot_sync(QFULL, n < N && ys[n] < 0.0f);
+      if (lane == 0) zbits[w0 >> 5] = b;
+    }
+    // ---- init 2: per check min1 / min2 / argmin (ascending columns) / parity ----
+    uint32_t sprev = 0;
+    for (int k = 0; k < nKm; ++k) {
+      const int m = tid + k * T;
+      uint32_t par = 0;
+      if (m < M) {
+        const int r = m >> lgz, i = m & (Z - 1);
+        float min1 = INFINITY, min2 = INFINITY;
+        int ac = 0xffff;
+        for (int cb = 0; cb < P.kb; ++cb) {
+          const int s = P.shift[r * P.kb + cb];
+          if (s < 0) continue;
+          const int c = cb * Z + ((i + s) & (Z - 1));
+          const float v = ys[c];
+          par ^= __float_as_uint(v);
+          const float a = fabsf(v);
+          const bool lt = a < min1;
+          min2 = fminf(min2, fmaxf(min1, a));
+          min1 = fminf(min1, a);
+          ac = lt ? c : ac;
+        }
+        par >>= 31;
+        const float sg = par ? 1.0f : -1.0f;
+        const float2 rv = make_float2(sg * min1, sg * (imw ? min2 : min1));
+        const uint16_t av = imw ? (uint16_t)ac : (uint16_t)0xffffu; // MWBF: every edge reads min1
+        rec[r * RS + i] = rv;
+        amc[r * RS + i] = av;
+        if (i < H) {
+          rec[r * RS + Z + i] = rv;
+          amc[r * RS + Z + i] = av;
+        }
+        sprev |= par << k;
+      }
+      const uint32_t b = __ballot_sync(QFULL, par != 0);
+      if (lane == 0 && k * T + warp * 32 < M) {
+        sbits[(k * T + warp * 32) >> 5] = b;
+        atomicAdd(&misc[Q_SWT], __popc(b));
+      }
+    }
+    __syncthreads();
+
+    // ---- iterations ----
+    int k = 0, conv = 0, stalled = 0;
+    long long logpos = 0, flips_total = 0;
+    for (;;) {
+      const int swt = misc[Q_SWT];
+      if (swt == 0) { conv = 1; break; }
+      if (k >= P.kmax) break;
+      const int fs = (k & 1) ? Q_FLIP : Q_F; // this iteration's flip counter (the other is reset)
+      if (tid == 0) misc[Q_F + Q_FLIP - fs] = 0;
+      // fused metric + block argmax + flips: warp w owns blocks w, w + nwarps, ...
+      for (int b = warp; b < P.nb; b += nwarps) {
+        const int base = b * TPC * 32, cb = base >> lgz, o0 = (base & (Z - 1)) + lane;
+        const float2 *pr[4];
+        const uint16_t *pa[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int s = r < P.jb ? P.shift[r * P.kb + cb] : -1;
+          const int i0 = (o0 - s) & (Z - 1);
+          pr[r] = s >= 0 ? rec + r * RS + i0 : rzero + lane;
+          pa[r] = s >= 0 ? amc + r * RS + i0 : azero + lane;
+        }
+        double v = -qdinf();
+        int vi = 0x7fffffff;
+#pragma unroll
+        for (int t = 0; t < TPC; ++t) {
+          const int n = base + lane + 32 * t;
+          double acc = 0.0;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const float2 w = pr[r][32 * t];
+            const bool am = pa[r][32 * t] == (uint16_t)n;
+            acc = __dadd_rn(acc, (double)(am ? w.y : w.x));
+          }
+          const double e = __dsub_rn(acc, __dmul_rn(alpha, (double)fabsf(ys[n])));
+          if (e > v) { v = e; vi = n; }
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+          const double v2 = __shfl_xor_sync(QFULL, v, off);
+          const int i2 = __shfl_xor_sync(QFULL, vi, off);
+          if (v2 > v || (v2 == v && i2 < vi)) { v = v2; vi = i2; }
+        }
+        if (lane == 0) { blk_v[b] = v; blk_i[b] = vi; }
+        if (v > 0.0) { // decoders.py:181-183: the warp applies its block's flip
+          if (lane == 0) {
+            atomicXor(&zbits[vi >> 5], 1u << (vi & 31));
+            atomicAdd(&misc[fs], 1);
+          }
+          if (lane < P.jb) {
+            const int cbv = vi >> lgz, o = vi & (Z - 1), s = P.shift[lane * P.kb + cbv];
+            if (s >= 0) {
+              const int m = (lane << lgz) + ((o - s) & (Z - 1));
+              atomicXor(&sbits[m >> 5], 1u << (m & 31));
+            }
+          }
+        }
+      }
+      __syncthreads();
+      int F = misc[fs];
+      if (F == 0) {
+        // nothing selected with a nonzero syndrome (decoders.py:214-222)
+        stalled = 1;
+        if (P.stall == FWBF_STALL_TERMINATE) {
+          if (tid == 0 && P.fliplog_counts) P.fliplog_counts[f * P.kmax + k] = 0;
+          k += 1;
+          break;
+        }
+        if (warp == 0) { // the global first maximum = the largest block maximum, lowest index
+          double gv = -qdinf();
+          int gi = 0x7fffffff;
+          for (int bb = lane; bb < P.nb; bb += 32) {
+            const double v2 = blk_v[bb];
+            const int i2 = blk_i[bb];
+            if (v2 > gv || (v2 == gv && i2 < gi)) { gv = v2; gi = i2; }
+          }
+#pragma unroll
+          for (int off = 16; off; off >>= 1) {
+            const double v2 = __shfl_xor_sync(QFULL, gv, off);
+            const int i2 = __shfl_xor_sync(QFULL, gi, off);
+            if (v2 > gv || (v2 == gv && i2 < gi)) { gv = v2; gi = i2; }
+          }
+          if (lane == 0) {
+            atomicXor(&zbits[gi >> 5], 1u << (gi & 31));
+            blk_v[gi / (TPC * 32)] = 1.0; // logged below as the single flip
+            blk_i[gi / (TPC * 32)] = gi;
+          }
+          if (lane < P.jb) {
+            const int cbv = gi >> lgz, o = gi & (Z - 1), s = P.shift[lane * P.kb + cbv];
+            if (s >= 0) {
+              const int m = (lane << lgz) + ((o - s) & (Z - 1));
+              atomicXor(&sbits[m >> 5], 1u << (m & 31));
+            }
+          }
+        }
+        F = 1;
+        __syncthreads();
+      }
+      if (P.fliplog && warp == 0) { // ascending = block order
+        int cnt = 0;
+        for (int b0 = 0; b0 < P.nb; b0 += 32) {
+          const int bb = b0 + lane;
+          const bool pos = bb < P.nb && blk_v[bb] > 0.0;
+          const uint32_t msk = __ballot_sync(QFULL, pos);
+          if (pos) P.fliplog[f * P.fliplog_stride + logpos + cnt + __popc(msk & ((1u << lane) - 1u))] = blk_i[bb];
+          cnt += __popc(msk);
+        }
+        if (lane == 0) P.fliplog_counts[f * P.kmax + k] = F;
+      }
+      logpos += F;
+      flips_total += F;
+      // refresh: negate the records of this thread's toggled checks; syndrome weight
+      if (tid == 0) misc[Q_SWT] = 0;
+      __syncthreads();
+      int pc = 0;
+      for (int kk = 0; kk < nKm; ++kk) {
+        const int m = tid + kk * T;
+        if (kk * T + warp * 32 < M) {
+          const uint32_t word = sbits[(kk * T + warp * 32) >> 5];
+          const uint32_t s = (word >> lane) & 1u;
+          if (m < M && s != ((sprev >> kk) & 1u)) {
+            const int r = m >> lgz, i = m & (Z - 1);
+            float2 *p0 = rec + r * RS + i;
+            const float2 w = *p0;
+            const float2 nw = make_float2(-w.x, -w.y);
+            *p0 = nw;
+            if (i < H) p0[Z] = nw;
+            sprev ^= 1u << kk;
+          }
+          pc += __popc(word);
+        }
+      }
+      if (lane == 0 && pc) atomicAdd(&misc[Q_SWT], pc);
+      k += 1;
+      __syncthreads();
+    }
+
+    // ---- outputs ----
+    if (tid == 0) misc[Q_BE] = 0;
+    __syncthreads();
+    int be = 0;
+    for (int w2 = tid; w2 < zw; w2 += T) {
+      const uint32_t z = zbits[w2];
+      if (P.z_bits) P.z_bits[f * P.z_ld + w2] = z;
+      const uint32_t cw = P.codeword_bits ? __ldg(P.codeword_bits + w2) : 0u;
+      be += __popc(z ^ cw);
+    }
+    be = __reduce_add_sync(QFULL, be);
+    if (lane == 0 && be) atomicAdd(&misc[Q_BE], be);
+    __syncthreads();
+    if (tid == 0) {
+      be = misc[Q_BE];
+      const int flags = (conv ? FWBF_FLAG_CONVERGED : 0) | (stalled ? FWBF_FLAG_STALLED : 0) | FWBF_FLAG_ORDERED |
+                        (nonfin ? FWBF_FLAG_NONFINITE : 0);
+      if (P.iterations) P.iterations[f] = k;
+      if (P.flags) P.flags[f] = (uint8_t)flags;
+      if (P.flips_total) P.flips_total[f] = (int)flips_total;
+      if (P.bit_errors) P.bit_errors[f] = be;
+      if (P.iter_hist) atomicAdd((unsigned long long *)&P.iter_hist[k], 1ull);
+      if (be && P.batch_word_err) atomicAdd(&P.batch_word_err[f / P.batch_frames], 1);
+      c_frames += 1;
+      c_biterr += be;
+      c_worderr += be ? 1 : 0;
+      c_iters += k;
+      c_flips += flips_total;
+      c_stalls += stalled;
+      c_conv += conv;
+      c_edges += (long long)P.n_edges * k;
+    }
+  }
+  if (tid == 0 && P.counters && c_frames) {
+    unsigned long long *c = (unsigned long long *)P.counters;
+    atomicAdd(c + FWBF_CNT_FRAMES, (unsigned long long)c_frames);
+    atomicAdd(c + FWBF_CNT_BIT_ERRORS, (unsigned long long)c_biterr);
+    atomicAdd(c + FWBF_CNT_WORD_ERRORS, (unsigned long long)c_worderr);
+    atomicAdd(c + FWBF_CNT_ITER_SUM, (unsigned long long)c_iters);
+    atomicAdd(c + FWBF_CNT_FLIP_SUM, (unsigned long long)c_flips);
+    atomicAdd(c + FWBF_CNT_STALLS, (unsigned long long)c_stalls);
+    atomicAdd(c + FWBF_CNT_CONVERGED, (unsigned long long)c_conv);
+    atomicAdd(c + FWBF_CNT_ORDERED_FRAMES, (unsigned long long)c_frames);
+    atomicAdd(c + FWBF_CNT_EDGE_VISITS, (unsigned long long)c_edges);
+  }
+}
+
+template __global__ void qdecode_kernel<1>(const __grid_constant__ QParams);
+template __global__ void qdecode_kernel<2>(const __grid_constant__ QParams);
+template __global__ void qdecode_kernel<4>(const __grid_constant__ QParams);
+template __global__ void qdecode_kernel<8>(const __grid_constant__ QParams);
+template __global__ void qdecode_kernel<16>(const __grid_constant__ QParams);
+
+} // namespace fwbf

@@ -87,3 +87,41 @@ def test_warp_kernel_dv4_and_columns_without_checks(cuda_device):
         for i in range(0, 300, 7):
             r = O.decode(g, y2[i], "fwbf", alpha=0.5, k_max=20, p=p)
             assert int(res.iterations[i]) == r.iterations and logs[i] == r.flip_log, (p, i)
+
+
+# ---- quasi-cyclic kernel (fwbf_qc.cu): config D's path ----
+
+def _qc_code(seed, jb, kb, z, absent):
+    from paper_1206_3362_b200.codes import qc_from_shifts
+    rng = np.random.default_rng(seed)
+    sh = rng.integers(0, z, size=(jb, kb))
+    if absent:
+        sh[rng.random((jb, kb)) < 0.2] = -1
+        sh[0, :] = np.maximum(sh[0, :], 0)        # every column keeps a check
+    return qc_from_shifts(sh, z)
+
+
+@pytest.mark.parametrize("code,p,stall,wmode", [
+    ("qc4x32", 256, "flip-global-max", "imwbf"), ("qc4x32", 512, "terminate", "imwbf"),
+    ("qc4x32", 32, "flip-global-max", "mwbf"), ("r3x16z64", 64, "flip-global-max", "imwbf"),
+    ("r4x12z32a", 32, "terminate", "imwbf"), ("r2x8z128a", 128, "flip-global-max", "imwbf"),
+    ("r4x20z16a", 16 * 2, "flip-global-max", "mwbf")])
+def test_qc_kernel_matches_cta_kernel_and_oracle(cuda_device, monkeypatch, code, p, stall, wmode):
+    if code == "qc4x32":
+        h = build_code(code)
+    else:
+        jb, rest = code[1:].split("x")
+        kb, zz = rest.split("z")
+        h = _qc_code(len(code) + p, int(jb), int(kb), int(zz.rstrip("a")), zz.endswith("a"))
+    frames = 256 if h.n_cols > 4000 else 2000
+    y = _y(h, frames, 5.0 if h.n_cols > 4000 else 3.5, 0.8 if h.n_cols > 4000 else 0.6, p, pad=True)
+    cfg = DecoderConfig(block_len_p=p, k_max=30, stall_policy=stall, weight_mode=wmode)
+    a = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+    monkeypatch.setenv("FWBF_NO_QCK", "1")
+    b = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+    _same(a, b)
+    assert a.flip_logs() == b.flip_logs()
+    z, its, fl, ft = COracle(h).decode_batch(y.cpu().numpy()[:128], algorithm="fwbf", alpha=0.2, k_max=30, p=p,
+                                             stall=stall, weight_mode=wmode)
+    assert np.array_equal(a.iterations.cpu().numpy()[:128], its)
+    assert np.array_equal(a.z()[:128], z)
