@@ -197,7 +197,9 @@ __global__ void __launch_bounds__(256) xdecode_kernel(const __grid_constant__ XP
             const uint32_t off = ((uint32_t)(w >> (16 * q)) & 0xffffu) | ((amk << (s2sh - q)) & (1u << s2sh));
             double v;
             asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(recb + off));
-            acc = __dadd_rn(acc, v);
+            // starting at the first term instead of +0.0 differs at most in
+            // the sign of a zero sum, which no comparison can see
+            acc = q == 0 ? v : __dadd_rn(acc, v);
           }
           const double e = __dsub_rn(acc, __dmul_rn(alpha, (double)fabsf(ys[pos])));
           if (e > best) { best = e; bc = c; }

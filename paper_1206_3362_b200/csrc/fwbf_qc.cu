@@ -166,12 +166,16 @@ __global__ void __launch_bounds__(512, 2) qdecode_kernel(const __grid_constant__
 #pragma unroll
         for (int t = 0; t < TPC; ++t) {
           const int n = base + lane + 32 * t;
+          // the reference's sum starts at +0.0; starting at the first term
+          // instead differs at most in the sign of a zero sum, which no
+          // comparison (> 0, argmax) can see
           double acc = 0.0;
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             const float2 w = pr[r][32 * t];
-            const bool am = pa[r][32 * t] == (uint16_t)n;
-            acc = __dadd_rn(acc, (double)(am ? w.y : w.x));
+            const bool am = (uint32_t)pa[r][32 * t] == (uint32_t)n; // zero-extended u16 vs n < 2^16
+            const double x = (double)(am ? w.y : w.x);
+            acc = r == 0 ? x : __dadd_rn(acc, x);
           }
           const double e = __dsub_rn(acc, __dmul_rn(alpha, (double)fabsf(ys[n])));
           if (e > v) { v = e; vi = n; }
