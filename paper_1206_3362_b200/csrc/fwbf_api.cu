@@ -389,12 +389,16 @@ struct Plan {
 };
 
 static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool circ, int cover, KParams &P,
-                   bool compact = false, bool fused = false, bool mode2 = false, bool ystage = false) {
+                   bool compact = false, bool fused = false, bool mode2 = false, bool ystage = false,
+                   int threads = 1024) {
   const int n = c->n, m = c->m;
   const int zw = (n + 31) / 32, sw = (m + 31) / 32;
   int nb = 1;
   if (p->algorithm == FWBF_ALG_FWBF) nb = (n + p->block_len_p - 1) / p->block_len_p;
-  const int nslots = std::max(nb, std::max(p->algorithm == FWBF_ALG_MLP ? p->lam : 1, 1));
+  // MLP: per-warp candidate lists [nwarps][lam] + per-warp counts (int slots)
+  const int nwarps = std::max(1, threads / 32);
+  const int nslots = std::max(nb, 1);
+  const int islots = std::max(nslots, p->algorithm == FWBF_ALG_MLP ? nwarps * (p->lam + 1) : 1);
   const int maxf = std::max(1, (int)fwbf_max_flips_per_iter(c, p));
   const int aw = (c->w > 32) ? 2 : 1;
   int o = 0;
@@ -475,7 +479,7 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
   P.off_sbits = take(sw * 4);
   P.off_zbits = take(zw * 4);
   P.off_blkv = take(nslots * 8);
-  P.off_blki = take((nslots + zw) * 4);
+  P.off_blki = take((islots + zw) * 4);
   P.off_flips = take(maxf * 4);
   P.off_offs = take(5 * fwbf::kMaxCircWeight * 4); // off[64], dneg doubled [128], rotated offsets [128]
   P.off_red = take(32 * 8 + 32 * 4);
@@ -1024,10 +1028,10 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   const bool ystage = circ && sizeof(YT) == 4 && kwt > 0 && !metric_out && !getenv("FWBF_NO_YSTAGE") &&
                       ((uintptr_t)y % 16) == 0 && row_bytes % 16 == 0 &&
                       ((c->n * (long long)sizeof(YT) + 15) & ~15LL) <= row_bytes;
-  layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, P.fused, mode2, ystage);
+  layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, P.fused, mode2, ystage, T);
   if (P.fused && P.smem_bytes > c->smem_optin) { // y must stay resident for the fused pass
     P.fused = 0;
-    layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, false, mode2, ystage);
+    layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, false, mode2, ystage, T);
   }
   if (ystage) {
     P.y_stage = 1;

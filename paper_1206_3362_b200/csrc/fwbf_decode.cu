@@ -70,6 +70,24 @@ __device__ __forceinline__ void warp_amax(double &v, int &i) {
   }
 }
 
+// Warp argmax (value desc, index asc) with three single-instruction integer
+// reductions (REDUX) instead of a 5-level shuffle butterfly: doubles map to
+// order-preserving 64-bit keys, the maximum key's high then low word is found,
+// and the lowest index among the lanes holding it.  Same result as warp_amax
+// for every non-NaN input (the index of -inf-only lanes is 0x7fffffff).
+__device__ __forceinline__ void warp_amax_redux(double &v, int &i) {
+  unsigned long long k = (unsigned long long)__double_as_longlong(v);
+  k = (k >> 63) ? ~k : (k | 0x8000000000000000ull);
+  const uint32_t hi = (uint32_t)(k >> 32), lo = (uint32_t)k;
+  const uint32_t mh = __reduce_max_sync(FULL_MASK, hi);
+  const uint32_t ml = __reduce_max_sync(FULL_MASK, hi == mh ? lo : 0u);
+  const bool top = hi == mh && lo == ml;
+  i = (int)__reduce_min_sync(FULL_MASK, top ? (uint32_t)i : 0xffffffffu);
+  unsigned long long km = ((unsigned long long)mh << 32) | ml;
+  km = (km >> 63) ? (km & 0x7fffffffffffffffull) : ~km;
+  v = __longlong_as_double((long long)km);
+}
+
 // ---------------------------------------------------------------------------
 // Shared-memory layout (byte offsets computed on the host, see plan_layout).
 // ---------------------------------------------------------------------------
@@ -946,13 +964,13 @@ decode_kernel(const __grid_constant__ KParams P) {
           const double e = __dsub_rn(__dmul_rn((double)S, qexp), aa);
           if (e > v) { v = e; i = n; }
         }
-        warp_amax(v, i);
+        warp_amax_redux(v, i); // finite metrics (split-path frames)
         if (lane == 0) { red_v[warp] = v; red_i[warp] = i; }
         __syncthreads();
         if (warp == 0) {
           v = lane < nwarps ? red_v[lane] : -dinf();
           i = lane < nwarps ? red_i[lane] : 0x7fffffff;
-          warp_amax(v, i);
+          warp_amax_redux(v, i); // finite metrics (split-path frames)
           const int c = i; // flipped unconditionally: IMWBF never stalls
           if (lane == 0) {
             zbits[c >> 5] ^= 1u << (c & 31);
@@ -1516,62 +1534,79 @@ decode_kernel(const __grid_constant__ KParams P) {
         }
         __syncthreads();
         F = misc[S_F];
-      } else { // MLP: lambda rounds of CTA argmax with exclusion, then ascending sort
-        // selected indices are marked in the E buffer by overwriting with -inf;
-        // their values are kept in blk_v/blk_i (sized lam on the host).
-        for (int r = 0; r < P.lam; ++r) {
-          double v = -dinf();
-          int i = 0x7fffffff;
-          for (int n = tid; n < N; n += T) amax_combine(v, i, Ebuf[n], n);
-          warp_amax(v, i);
-          if (lane == 0) { red_v[warp] = v; red_i[warp] = i; }
-          __syncthreads();
-          if (warp == 0) {
-            v = lane < nwarps ? red_v[lane] : -dinf();
-            i = lane < nwarps ? red_i[lane] : 0x7fffffff;
-            warp_amax(v, i);
-            if (lane == 0) {
-              blk_v[r] = v;
-              blk_i[r] = i;
-              Ebuf[i] = -dinf();
-              if (r == 0) { misc[S_GBEST] = i; flips[0] = i; }
+      } else { // MLP: top-lambda by (metric desc, index asc), then ascending order
+        // (decoders.py:174-178: stable argsort of -e, first lam, > 0 when
+        // thresholded, sorted).  Two barriers per iteration:
+        // (1) each warp lists its own top-L columns (L = min(lam, its column
+        //     count)), best first, by L rounds of warp argmax with exclusion
+        //     (a per-lane taken mask over its nKy columns) -- no barriers;
+        // (2) warp 0 merges the nwarps sorted lists (lane l walks list l),
+        //     stops after lam picks or at the first pick <= 0 when thresholded
+        //     (the lists are descending), marks the picks in a column bitmap
+        //     and compacts it in ascending order.
+        // The metric stays in Ebuf; lists hold column indices only.
+        int *cand = blk_i;                                        // [nwarps][L]
+        int *ccnt = blk_i + nwarps * P.lam;                       // [nwarps]
+        uint32_t *sel = reinterpret_cast<uint32_t *>(ccnt + nwarps); // [zw]
+        const int L = min(P.lam, 32 * nKy);
+        {
+          uint32_t taken = 0;
+          int cnt = 0;
+          for (int r = 0; r < L; ++r) {
+            double v = -dinf();
+            int i = 0x7fffffff;
+            for (int q = 0; q < nKy; ++q) {
+              const int n = tid + q * T;
+              if (n < N && !((taken >> q) & 1u)) amax_combine(v, i, Ebuf[n], n);
             }
+            warp_amax_redux(v, i);
+            if (i == 0x7fffffff) break; // the warp's columns are exhausted (warp-uniform)
+            if ((i & 31) == lane) taken |= 1u << (i / T);
+            if (lane == 0) cand[warp * P.lam + r] = i;
+            cnt = r + 1;
           }
-          __syncthreads();
-        }
-        // flips = selected (and positive when thresholded), ascending: mark in a
-        // bitmap over columns (scratch after blk_i[lam]), then compact in order.
-        uint32_t *sel = reinterpret_cast<uint32_t *>(blk_i + P.lam);
-        for (int w2 = tid; w2 < zw; w2 += T) sel[w2] = 0u;
-        __syncthreads();
-        for (int r = tid; r < P.lam; r += T) {
-          if (!P.mlp_thr || blk_v[r] > 0.0) {
-            const int i = blk_i[r];
-            atomicOr(&sel[i >> 5], 1u << (i & 31));
-          }
+          if (lane == 0) ccnt[warp] = cnt;
         }
         __syncthreads();
         if (warp == 0) {
-          int cnt = 0;
-          for (int base = 0; base < zw; base += 32) {
-            const int w2 = base + lane;
-            const uint32_t word = (w2 < zw) ? sel[w2] : 0u;
-            int c = __popc(word);
-            int incl = c;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-              const int t2 = __shfl_up_sync(FULL_MASK, incl, off);
-              if (lane >= off) incl += t2;
-            }
-            int pos = cnt + incl - c;
-            uint32_t wd = word;
-            while (wd) {
-              const int bit = __ffs(wd) - 1;
-              wd &= wd - 1;
-              flips[pos++] = w2 * 32 + bit;
-            }
-            cnt += __shfl_sync(FULL_MASK, incl, 31);
+          for (int w2 = lane; w2 < zw; w2 += 32) sel[w2] = 0u;
+          const int myc = lane < nwarps ? ccnt[lane] : 0;
+          int h = 0, picked = 0;
+          __syncwarp();
+          for (int r = 0; r < P.lam; ++r) {
+            double v = -dinf();
+            int i = 0x7fffffff;
+            if (h < myc) { i = cand[lane * P.lam + h]; v = Ebuf[i]; }
+            warp_amax_redux(v, i);
+            if (i == 0x7fffffff) break;
+            if (r == 0 && lane == 0) { misc[S_GBEST] = i; flips[0] = i; } // the global argmax (stall policy)
+            if (P.mlp_thr && !(v > 0.0)) break;                           // every later pick is <= v
+            if (h < myc && cand[lane * P.lam + h] == i) ++h;              // the owner list advances
+            if (lane == 0) sel[i >> 5] |= 1u << (i & 31);
+            ++picked;
           }
+          __syncwarp();
+          int cnt = 0;
+          if (picked)
+            for (int base = 0; base < zw; base += 32) {
+              const int w2 = base + lane;
+              const uint32_t word = (w2 < zw) ? sel[w2] : 0u;
+              int c = __popc(word);
+              int incl = c;
+#pragma unroll
+              for (int off = 1; off < 32; off <<= 1) {
+                const int t2 = __shfl_up_sync(FULL_MASK, incl, off);
+                if (lane >= off) incl += t2;
+              }
+              int pos = cnt + incl - c;
+              uint32_t wd = word;
+              while (wd) {
+                const int bit = __ffs(wd) - 1;
+                wd &= wd - 1;
+                flips[pos++] = w2 * 32 + bit;
+              }
+              cnt += __shfl_sync(FULL_MASK, incl, 31);
+            }
           if (lane == 0) misc[S_F] = cnt;
         }
         __syncthreads();

@@ -180,11 +180,18 @@ __global__ void __launch_bounds__(512, 2) qdecode_kernel(const __grid_constant__
           const double e = __dsub_rn(acc, __dmul_rn(alpha, (double)fabsf(ys[n])));
           if (e > v) { v = e; vi = n; }
         }
-#pragma unroll
-        for (int off = 16; off; off >>= 1) {
-          const double v2 = __shfl_xor_sync(QFULL, v, off);
-          const int i2 = __shfl_xor_sync(QFULL, vi, off);
-          if (v2 > v || (v2 == v && i2 < vi)) { v = v2; vi = i2; }
+        {
+          // block argmax (value desc, index asc) by three REDUX reductions on
+          // order-preserving 64-bit keys of the doubles
+          unsigned long long key = (unsigned long long)__double_as_longlong(v);
+          key = (key >> 63) ? ~key : (key | 0x8000000000000000ull);
+          const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
+          const uint32_t mh = __reduce_max_sync(QFULL, hi);
+          const uint32_t ml = __reduce_max_sync(QFULL, hi == mh ? lo : 0u);
+          vi = (int)__reduce_min_sync(QFULL, (hi == mh && lo == ml) ? (uint32_t)vi : 0xffffffffu);
+          unsigned long long km = ((unsigned long long)mh << 32) | ml;
+          km = (km >> 63) ? (km & 0x7fffffffffffffffull) : ~km;
+          v = __longlong_as_double((long long)km);
         }
         if (lane == 0) { blk_v[b] = v; blk_i[b] = vi; }
         if (v > 0.0) { // decoders.py:181-183: the warp applies its block's flip
