@@ -1025,9 +1025,23 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   // circulant float32 kernels; rows must be 16-byte aligned and hold the
   // rounded-up copy size
   const long long row_bytes = ld * (long long)sizeof(YT);
-  const bool ystage = circ && sizeof(YT) == 4 && kwt > 0 && !metric_out && !getenv("FWBF_NO_YSTAGE") &&
-                      ((uintptr_t)y % 16) == 0 && row_bytes % 16 == 0 &&
-                      ((c->n * (long long)sizeof(YT) + 15) & ~15LL) <= row_bytes;
+  bool ystage = circ && sizeof(YT) == 4 && kwt > 0 && !metric_out && !getenv("FWBF_NO_YSTAGE") &&
+                ((uintptr_t)y % 16) == 0 && row_bytes % 16 == 0 &&
+                ((c->n * (long long)sizeof(YT) + 15) & ~15LL) <= row_bytes;
+  if (ystage && !compact) {
+    // non-compact layouts swap their y buffer for the staging buffer: same size
+  } else if (ystage) {
+    // compact layouts add the staging buffer: only where it costs no CTA per SM
+    // (the MODE 2 layout keeps 5 CTAs/SM; the exact-path layouts would drop from 4 to 3)
+    KParams Q0 = P, Q1 = P;
+    layout(c, p, (int)sizeof(YT), circ, T * kc, Q0, compact, P.fused, mode2, false, T);
+    layout(c, p, (int)sizeof(YT), circ, T * kc, Q1, compact, P.fused, mode2, true, T);
+    int occ0 = 0, occ1 = 0;
+    rc = plan_occupancy(c->device, kern, T, Q0.smem_bytes, &occ0);
+    if (!rc && Q1.smem_bytes <= c->smem_optin) rc = plan_occupancy(c->device, kern, T, Q1.smem_bytes, &occ1);
+    if (rc) return rc;
+    ystage = occ1 >= occ0 && occ1 > 0;
+  }
   layout(c, p, (int)sizeof(YT), circ, T * kc, P, compact, P.fused, mode2, ystage, T);
   if (P.fused && P.smem_bytes > c->smem_optin) { // y must stay resident for the fused pass
     P.fused = 0;

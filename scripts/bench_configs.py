@@ -50,12 +50,14 @@ def run_y(code, alg, cfg, ebn0, frames, steps, warmup, seed=1):
                       flips_total=torch.zeros(frames, dtype=torch.int32, device=dev),
                       bit_errors=torch.zeros(frames, dtype=torch.int32, device=dev),
                       counters=torch.zeros(nat.NCOUNTERS, dtype=torch.int64, device=dev))
+    res.iter_hist = torch.zeros(cfg.k_max + 1, dtype=torch.int64, device=dev)
     out = _outputs(res)
     st = torch.cuda.current_stream(dev)
     L = nat.lib()
 
     def step():
         res.counters.zero_()
+        res.iter_hist.zero_()
         nat.check(L.fwbf_decode_f32(dc.handle, C.byref(prm), C.c_void_p(y.data_ptr()), frames, ld,
                                     C.byref(out), C.c_void_p(st.cuda_stream)), "decode")
     return _time(step, steps, warmup, res, frames, code, h)
@@ -81,7 +83,7 @@ def run_awgn(code, alg, cfg, ebn0, frames, steps, warmup, noise="f32", seed=1):
     ev1.record()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / steps
-    return _summ(holder["r"], frames, ms, code, h)
+    return _summ(holder["r"], frames, ms, code, h, device_noise=True)
 
 
 def _time(step, steps, warmup, res, frames, code, h):
@@ -97,15 +99,36 @@ def _time(step, steps, warmup, res, frames, code, h):
     return _summ(res, frames, ev0.elapsed_time(ev1) / steps, code, h)
 
 
-def _summ(res, frames, ms, code, h):
+def _peaks():
+    props = torch.cuda.get_device_properties(0)
+    try:
+        mp = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except OSError:
+        mp = {}
+    return props.multi_processor_count, mp.get("sm_max_mhz", 1965.0), mp.get("hbm_gbs", 6548.2)
+
+
+def _summ(res, frames, ms, code, h, device_noise=False):
     c = res.counters.cpu().numpy()
     fr = int(c[nat.CNT_FRAMES])
     it = c[nat.CNT_ITER_SUM] / fr
-    return {"frames": frames, "ms_per_step": ms, "info_gbit_s": frames * code_k(code) / (ms / 1e3) / 1e9,
-            "frames_per_s": frames / (ms / 1e3), "mean_iters": float(it),
-            "fer": float(c[nat.CNT_WORD_ERRORS] / fr), "ber": float(c[nat.CNT_BIT_ERRORS] / (fr * h.n_cols)),
-            "ordered_frames": int(c[nat.CNT_ORDERED_FRAMES]),
-            "edge_visits_per_s": h.n_edges * (1 + it) * frames / (ms / 1e3)}
+    sms, mhz, hbm = _peaks()
+    ev = h.n_edges * (1 + it) * frames / (ms / 1e3)
+    zw = (h.n_cols + 31) // 32
+    bpf = (0 if device_noise else 4 * h.n_cols) + 4 * zw + 8   # SURVEY 8(d) algorithmic bytes per frame
+    out = {"frames": frames, "ms_per_step": ms, "info_gbit_s": frames * code_k(code) / (ms / 1e3) / 1e9,
+           "frames_per_s": frames / (ms / 1e3), "mean_iters": float(it),
+           "fer": float(c[nat.CNT_WORD_ERRORS] / fr), "ber": float(c[nat.CNT_BIT_ERRORS] / (fr * h.n_cols)),
+           "ordered_frames": int(c[nat.CNT_ORDERED_FRAMES]),
+           "edge_visits_per_s": ev,
+           # the binding roofline of SURVEY 8(d): one fp64 add per lane per clock
+           "roofline": {"bound": "issue", "achieved": ev, "peak": sms * 64 * mhz * 1e6, "unit": "edge-visits/s",
+                        "frac": ev / (sms * 64 * mhz * 1e6),
+                        "hbm": {"bytes_per_frame": bpf, "achieved_GBps": bpf * frames / (ms / 1e3) / 1e9,
+                                "frac": bpf * frames / (ms / 1e3) / 1e9 / hbm}}}
+    if getattr(res, "iter_hist", None) is not None:
+        out["iter_hist"] = [int(v) for v in res.iter_hist.cpu().tolist()]
+    return out
 
 
 def main():
