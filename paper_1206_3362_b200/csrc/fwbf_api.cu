@@ -1025,9 +1025,13 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   // circulant float32 kernels; rows must be 16-byte aligned and hold the
   // rounded-up copy size
   const long long row_bytes = ld * (long long)sizeof(YT);
+  // Staging claims the frame queue one frame ahead, so a CTA holding a slow
+  // frame also holds its next one: only worth it when the batch is many
+  // frames per CTA (small batches are latency-bound and lose their tail).
   bool ystage = circ && sizeof(YT) == 4 && kwt > 0 && !metric_out && !getenv("FWBF_NO_YSTAGE") &&
                 ((uintptr_t)y % 16) == 0 && row_bytes % 16 == 0 &&
-                ((c->n * (long long)sizeof(YT) + 15) & ~15LL) <= row_bytes;
+                ((c->n * (long long)sizeof(YT) + 15) & ~15LL) <= row_bytes &&
+                (batch >= 128LL * c->sm_count || getenv("FWBF_FORCE_YSTAGE"));
   if (ystage && !compact) {
     // non-compact layouts swap their y buffer for the staging buffer: same size
   } else if (ystage) {

@@ -226,6 +226,7 @@ def test_staged_rows_equal_unstaged(cuda_device, monkeypatch, code, alg, kw, fra
     y = buf[:, :n]
     y.copy_(1.0 + sigma * torch.randn((frames, n), generator=g, device="cuda"))
     cfg = P.DecoderConfig(**kw)
+    monkeypatch.setenv("FWBF_FORCE_YSTAGE", "1")   # staging also for the small batches
     a = P.decode_batch(h, y, cfg, alg, flip_log=True)
     monkeypatch.setenv("FWBF_NO_YSTAGE", "1")
     b = P.decode_batch(h, y, cfg, alg, flip_log=True)
