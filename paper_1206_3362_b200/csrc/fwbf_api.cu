@@ -561,10 +561,10 @@ static int build_xplan(fwbf_code *c, int p, XPlan *out) {
         const int base = b * p, lim = std::min(p, n - base);
         if (sub + G * cc < lim) scol[(r * S + cc) * 32 + l] = base + sub + G * cc;
       }
-  // Labels: the q-th check of the 32 slots (r, c, *) is one LDS.64 of 32
-  // lanes; an 8-byte record at label j sits in bank pair j mod 16.  Greedy:
-  // checks by decreasing number of loads, each to the bank pair (with labels
-  // left) least used by the loads it takes part in.
+  // Labels: the q-th check of the 32 slots (r, c, *) is one 4-byte load of
+  // 32 lanes; the record at label j sits in bank j mod 32.  Greedy: checks by
+  // decreasing number of loads, each to the bank (with labels left) least
+  // used by the loads it takes part in.
   std::vector<int> lab(m, -1);
   {
     const int ninstr = R * S * 4;
@@ -581,29 +581,30 @@ static int build_xplan(fwbf_code *c, int p, XPlan *out) {
     for (int i = 0; i < m; ++i) order[i] = i;
     std::stable_sort(order.begin(), order.end(),
                      [&](int a, int b2) { return loads[a].size() > loads[b2].size(); });
-    std::vector<int> cnt((size_t)ninstr * 16, 0), cap(16, 0), next(16, 0);
-    for (int j = 0; j < m; ++j) cap[j % 16]++;
-    for (int k = 0; k < 16; ++k) next[k] = k;
+    constexpr int NB = 32; // banks
+    std::vector<int> cnt((size_t)ninstr * NB, 0), cap(NB, 0), next(NB, 0);
+    for (int j = 0; j < m; ++j) cap[j % NB]++;
+    for (int k = 0; k < NB; ++k) next[k] = k;
     for (int chk : order) {
       int bestk = -1;
       long bestc = 0;
-      for (int k = 0; k < 16; ++k) {
+      for (int k = 0; k < NB; ++k) {
         if (!cap[k]) continue;
         long cst = 0;
-        for (int ins : loads[chk]) cst += cnt[(size_t)ins * 16 + k];
+        for (int ins : loads[chk]) cst += cnt[(size_t)ins * NB + k];
         if (bestk < 0 || cst < bestc) { bestk = k; bestc = cst; }
       }
-      for (int ins : loads[chk]) cnt[(size_t)ins * 16 + bestk]++;
+      for (int ins : loads[chk]) cnt[(size_t)ins * NB + bestk]++;
       cap[bestk]--;
       lab[chk] = next[bestk];
-      next[bestk] += 16;
+      next[bestk] += NB;
     }
   }
   std::vector<int> invp(m);
   for (int i = 0; i < m; ++i) invp[lab[i]] = i;
   // padding slots read the (-inf, -inf) label m on every edge
   unsigned long long padw = 0;
-  for (int q = 0; q < 4; ++q) padw |= (unsigned long long)(8 * m) << (16 * q);
+  for (int q = 0; q < 4; ++q) padw |= (unsigned long long)(4 * m) << (16 * q);
   std::vector<unsigned long long> tab(nslot, padw);
   std::vector<uint16_t> cpos(n, 0);
   for (int r = 0; r < R; ++r)
@@ -620,7 +621,7 @@ static int build_xplan(fwbf_code *c, int p, XPlan *out) {
         const int e0 = c->h_col_ptr[col], e1 = c->h_col_ptr[col + 1];
         for (int q = 0; q < 4; ++q) {
           const int j = e0 + q < e1 ? lab[c->h_col_idx[e0 + q]] : m + 1;
-          w |= (unsigned long long)(8 * j) << (16 * q);
+          w |= (unsigned long long)(4 * j) << (16 * q);
         }
         tab[pos] = w;
         cpos[col] = (uint16_t)pos;
@@ -642,8 +643,8 @@ static int build_xplan(fwbf_code *c, int p, XPlan *out) {
   int w = 0;
   auto wtake = [&](int bytes) { int r0 = w; w = align16(w + bytes); return r0; };
   x.s2sh = 7;
-  while ((1 << x.s2sh) < 8 * (m + 2)) ++x.s2sh;
-  x.wo_rec = wtake((1 << x.s2sh) + 8 * (m + 2));
+  while ((1 << x.s2sh) < 4 * (m + 2)) ++x.s2sh;
+  x.wo_rec = wtake((1 << x.s2sh) + 4 * (m + 2));
   x.wo_ys = wtake(nslot * 4);
   x.wo_am = wtake(nslot);
   x.wo_sb = wtake(((m + 31) / 32) * 4);

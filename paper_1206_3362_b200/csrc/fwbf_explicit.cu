@@ -13,13 +13,14 @@
 //     so every per-slot array is read conflict-free (consecutive lanes,
 //     consecutive words); tab[pos] packs the byte offsets of the column's
 //     <= DV check records (ascending checks, 16 bits each);
-//   * per check sgn min1 and sgn min2 in fp64, in two arrays S2OFF bytes apart
-//     (S2OFF a power of two >= 128, so both copies of a check sit in the same
-//     bank): an edge is one LDS.64 whose address picks min2 (+S2OFF) by the
-//     column's argmin bit.  Checks are stored under a host-chosen label
-//     (a permutation): lanes of one load instruction read checks whose labels
-//     are spread over the 16 bank pairs, so most loads take the minimum two
-//     wavefronts instead of the ~3.7 of arbitrary labels.  Two constant
+//   * per check sgn min1 and sgn min2 as float32 (the exact minima), in two
+//     arrays S2OFF bytes apart (S2OFF a power of two >= 128, so both copies
+//     of a check sit in the same bank): an edge is one 4-byte load whose
+//     address picks min2 (+S2OFF) by the column's argmin bit, converted to
+//     fp64 exactly.  Checks are stored under a host-chosen label (a
+//     permutation): lanes of one load instruction read checks whose labels
+//     are spread over the 32 banks, so most loads take one or two wavefronts
+//     instead of the ~3.7 of arbitrary labels.  Two constant
 //     labels end the arrays: (-inf, -inf) fills the edges of padding slots
 //     (their metric is -inf, never a maximum) and (0, 0) the missing edges of
 //     columns lighter than DV (adding +0.0 to a sum that started at +0.0
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(256) xdecode_kernel(const __grid_constant__ XP
 
   // ---- this warp's frame state ----
   unsigned char *W = sm + P.off_warp0 + warp * P.warp_bytes;
-  double *rec = reinterpret_cast<double *>(W + P.wo_rec);      // by label: sgn*min1; + S2OFF: sgn*min2
+  float *rec = reinterpret_cast<float *>(W + P.wo_rec);        // by label: sgn*min1; + S2OFF: sgn*min2
   float *ys = reinterpret_cast<float *>(W + P.wo_ys);           // [nslot] signed y per slot (-0 -> +0)
   uint8_t *am = W + P.wo_am;                                    // [nslot] argmin bits per slot
   uint32_t *sb = reinterpret_cast<uint32_t *>(W + P.wo_sb);     // syndrome bits
@@ -78,13 +79,13 @@ __global__ void __launch_bounds__(256) xdecode_kernel(const __grid_constant__ XP
   const bool imw = P.wmode == FWBF_WEIGHTS_IMWBF;
   const double alpha = P.alpha;
   if (lane == 0) { // the two constant records after the M check records
-    double *rec2 = rec + (P.s2off >> 3);
-    rec[M] = rec2[M] = -xdinf();
-    rec[M + 1] = rec2[M + 1] = 0.0;
+    float *rec2 = rec + (P.s2off >> 2);
+    rec[M] = rec2[M] = -INFINITY;
+    rec[M + 1] = rec2[M + 1] = 0.0f;
   }
   __syncthreads();
   const uint32_t recb = (uint32_t)__cvta_generic_to_shared(rec);
-  double *rec2 = rec + (P.s2off >> 3);
+  float *rec2 = rec + (P.s2off >> 2);
   const int s2sh = P.s2sh; // S2OFF = 1 << s2sh
 
   long long c_frames = 0, c_biterr = 0, c_worderr = 0, c_iters = 0, c_flips = 0, c_stalls = 0, c_conv = 0,
@@ -156,10 +157,10 @@ __global__ void __launch_bounds__(256) xdecode_kernel(const __grid_constant__ XP
           ae = lt ? e : ae;
         }
         par >>= 31;
-        const double sg = par ? 1.0 : -1.0;
+        const float sg = par ? 1.0f : -1.0f;
         // MWBF (include-self minimum): every edge reads min1
-        rec[j] = sg * (double)min1;
-        rec2[j] = sg * (double)(imw ? min2 : min1);
+        rec[j] = sg * min1; // float32 minima: exact; converted to fp64 per edge
+        rec2[j] = sg * (imw ? min2 : min1);
         if (imw && ae >= 0) { // the argmin column reads min2 at this check's position in its list
           const uint32_t pe = __ldg(rtab + ae);
           const uint32_t pos = pe & 0xffffu;
@@ -195,8 +196,9 @@ __global__ void __launch_bounds__(256) xdecode_kernel(const __grid_constant__ XP
           for (int q = 0; q < DV; ++q) {
             // record byte offset, + S2OFF (min2) when this check's argmin is the column
             const uint32_t off = ((uint32_t)(w >> (16 * q)) & 0xffffu) | ((amk << (s2sh - q)) & (1u << s2sh));
-            double v;
-            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(recb + off));
+            float vf;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(vf) : "r"(recb + off));
+            const double v = (double)vf;
             // starting at the first term instead of +0.0 differs at most in
             // the sign of a zero sum, which no comparison can see
             acc = q == 0 ? v : __dadd_rn(acc, v);
@@ -254,15 +256,15 @@ __global__ void __launch_bounds__(256) xdecode_kernel(const __grid_constant__ XP
           const unsigned long long w = tab[cpos[c]];
 #pragma unroll
           for (int q = 0; q < DV; ++q) {
-            const uint32_t m = ((uint32_t)(w >> (16 * q)) & 0xffffu) >> 3; // label
+            const uint32_t m = ((uint32_t)(w >> (16 * q)) & 0xffffu) >> 2; // label
             if (m < (uint32_t)M) { // not the (0, 0) record of a missing edge
               const uint32_t old = atomicXor(&sb[m >> 5], 1u << (m & 31));
               dsw += ((old >> (m & 31)) & 1u) ? -1 : 1;
               // negate sgn*min1 and sgn*min2 of the toggled check: XOR of the
               // sign bit in each double's high word (32-bit shared atomics are
               // native; 64-bit XOR would be a CAS loop)
-              atomicXor(reinterpret_cast<uint32_t *>(rec + m) + 1, 0x80000000u);
-              atomicXor(reinterpret_cast<uint32_t *>(rec2 + m) + 1, 0x80000000u);
+              atomicXor(reinterpret_cast<uint32_t *>(rec + m), 0x80000000u);
+              atomicXor(reinterpret_cast<uint32_t *>(rec2 + m), 0x80000000u);
             }
           }
         }
