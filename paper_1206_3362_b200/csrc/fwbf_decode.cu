@@ -76,7 +76,8 @@ __device__ __forceinline__ void warp_amax(double &v, int &i) {
 // and the lowest index among the lanes holding it.  Same result as warp_amax
 // for every non-NaN input (the index of -inf-only lanes is 0x7fffffff).
 __device__ __forceinline__ void warp_amax_redux(double &v, int &i) {
-  unsigned long long k = (unsigned long long)__double_as_longlong(v);
+  // -0.0 and +0.0 compare equal: normalise so their keys tie too
+  unsigned long long k = (unsigned long long)__double_as_longlong(v + 0.0);
   k = (k >> 63) ? ~k : (k | 0x8000000000000000ull);
   const uint32_t hi = (uint32_t)(k >> 32), lo = (uint32_t)k;
   const uint32_t mh = __reduce_max_sync(FULL_MASK, hi);

@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(512, 2) qdecode_kernel(const __grid_constant__
         {
           // block argmax (value desc, index asc) by three REDUX reductions on
           // order-preserving 64-bit keys of the doubles
-          unsigned long long key = (unsigned long long)__double_as_longlong(v);
+          unsigned long long key = (unsigned long long)__double_as_longlong(v + 0.0); // -0.0 -> +0.0: keys must tie
           key = (key >> 63) ? ~key : (key | 0x8000000000000000ull);
           const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
           const uint32_t mh = __reduce_max_sync(QFULL, hi);

@@ -125,3 +125,24 @@ def test_qc_kernel_matches_cta_kernel_and_oracle(cuda_device, monkeypatch, code,
                                              stall=stall, weight_mode=wmode)
     assert np.array_equal(a.iterations.cpu().numpy()[:128], its)
     assert np.array_equal(a.z()[:128], z)
+
+
+@pytest.mark.parametrize("quant", [0.25, 0.5])
+@pytest.mark.parametrize("p,alpha", [(256, 0.2), (64, 1.0), (512, 0.0)])
+def test_qc_kernel_quantised_ties(cuda_device, monkeypatch, quant, p, alpha):
+    """Quantised y: many exact ties between metrics, and metrics that are +0.0
+    in the reference but -0.0 in a sum started at its first term -- the
+    REDUX block argmax must key them equally (lowest index wins)."""
+    import torch
+    h = build_code("qc4x32")
+    y = _y(h, 384, 5.0, 0.875, 11 + p, pad=True)
+    y.copy_(torch.round(y / quant) * quant)
+    cfg = DecoderConfig(block_len_p=p, k_max=25, alpha=alpha)
+    a = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+    monkeypatch.setenv("FWBF_NO_QCK", "1")
+    b = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+    _same(a, b)
+    assert a.flip_logs() == b.flip_logs()
+    z, its, fl, ft = COracle(h).decode_batch(y.cpu().numpy()[:96], algorithm="fwbf", alpha=alpha, k_max=25, p=p)
+    assert np.array_equal(a.iterations.cpu().numpy()[:96], its)
+    assert np.array_equal(a.z()[:96], z)
