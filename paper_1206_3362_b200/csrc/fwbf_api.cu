@@ -397,7 +397,7 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
   if (p->algorithm == FWBF_ALG_FWBF) nb = (n + p->block_len_p - 1) / p->block_len_p;
   // MLP: per-warp candidate lists [nwarps][lam] + per-warp counts (int slots)
   const int nwarps = std::max(1, threads / 32);
-  const int nslots = std::max(nb, 1);
+  const int nslots = std::max(nb, p->algorithm == FWBF_ALG_MLP ? nwarps * p->lam : 1); // MLP: list values
   const int islots = std::max(nslots, p->algorithm == FWBF_ALG_MLP ? nwarps * (p->lam + 1) : 1);
   const int maxf = std::max(1, (int)fwbf_max_flips_per_iter(c, p));
   const int aw = (c->w > 32) ? 2 : 1;

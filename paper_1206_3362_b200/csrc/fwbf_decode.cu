@@ -1545,12 +1545,50 @@ decode_kernel(const __grid_constant__ KParams P) {
         //     stops after lam picks or at the first pick <= 0 when thresholded
         //     (the lists are descending), marks the picks in a column bitmap
         //     and compacts it in ascending order.
-        // The metric stays in Ebuf; lists hold column indices only.
+        // Lists hold (value, column) pairs, so the merge reads no metric.
         int *cand = blk_i;                                        // [nwarps][L]
         int *ccnt = blk_i + nwarps * P.lam;                       // [nwarps]
         uint32_t *sel = reinterpret_cast<uint32_t *>(ccnt + nwarps); // [zw]
+        double *candv = blk_v;                                    // [nwarps][L]
         const int L = min(P.lam, 32 * nKy);
-        {
+        if (TB > 0) {
+          // compile-time columns per thread: each lane sorts its KC values once
+          // (value desc, index asc); a round's candidate is then the lane's
+          // head, and the winning lane shifts its list -- no rescans
+          constexpr int KS = TB > 0 ? KC : 1;
+          double sv[KS];
+          int si[KS];
+#pragma unroll
+          for (int q = 0; q < KS; ++q) {
+            const int n = tid + q * T;
+            sv[q] = n < N ? Ebuf[n] : -dinf();
+            si[q] = n < N ? n : 0x7fffffff;
+          }
+#pragma unroll
+          for (int a2 = 0; a2 < KS; ++a2)
+#pragma unroll
+            for (int b2 = 0; b2 + 1 < KS - a2; ++b2)
+              if (sv[b2 + 1] > sv[b2] || (sv[b2 + 1] == sv[b2] && si[b2 + 1] < si[b2])) {
+                const double tv = sv[b2]; sv[b2] = sv[b2 + 1]; sv[b2 + 1] = tv;
+                const int ti = si[b2]; si[b2] = si[b2 + 1]; si[b2 + 1] = ti;
+              }
+          int cnt = 0;
+          for (int r = 0; r < L; ++r) {
+            double v = sv[0];
+            int i = si[0];
+            warp_amax_redux(v, i);
+            if (i == 0x7fffffff) break; // the warp's columns are exhausted (warp-uniform)
+            if (si[0] == i) { // this lane's head won: pop it
+#pragma unroll
+              for (int q = 0; q + 1 < KS; ++q) { sv[q] = sv[q + 1]; si[q] = si[q + 1]; }
+              sv[KS - 1] = -dinf();
+              si[KS - 1] = 0x7fffffff;
+            }
+            if (lane == 0) { cand[warp * P.lam + r] = i; candv[warp * P.lam + r] = v; }
+            cnt = r + 1;
+          }
+          if (lane == 0) ccnt[warp] = cnt;
+        } else {
           uint32_t taken = 0;
           int cnt = 0;
           for (int r = 0; r < L; ++r) {
@@ -1563,7 +1601,7 @@ decode_kernel(const __grid_constant__ KParams P) {
             warp_amax_redux(v, i);
             if (i == 0x7fffffff) break; // the warp's columns are exhausted (warp-uniform)
             if ((i & 31) == lane) taken |= 1u << (i / T);
-            if (lane == 0) cand[warp * P.lam + r] = i;
+            if (lane == 0) { cand[warp * P.lam + r] = i; candv[warp * P.lam + r] = v; }
             cnt = r + 1;
           }
           if (lane == 0) ccnt[warp] = cnt;
@@ -1573,16 +1611,21 @@ decode_kernel(const __grid_constant__ KParams P) {
           for (int w2 = lane; w2 < zw; w2 += 32) sel[w2] = 0u;
           const int myc = lane < nwarps ? ccnt[lane] : 0;
           int h = 0, picked = 0;
+          double hv = myc > 0 ? candv[lane * P.lam] : -dinf(); // this lane's list head
+          int hi = myc > 0 ? cand[lane * P.lam] : 0x7fffffff;
           __syncwarp();
           for (int r = 0; r < P.lam; ++r) {
-            double v = -dinf();
-            int i = 0x7fffffff;
-            if (h < myc) { i = cand[lane * P.lam + h]; v = Ebuf[i]; }
+            double v = hv;
+            int i = hi;
             warp_amax_redux(v, i);
             if (i == 0x7fffffff) break;
             if (r == 0 && lane == 0) { misc[S_GBEST] = i; flips[0] = i; } // the global argmax (stall policy)
             if (P.mlp_thr && !(v > 0.0)) break;                           // every later pick is <= v
-            if (h < myc && cand[lane * P.lam + h] == i) ++h;              // the owner list advances
+            if (hi == i) { // the owner list advances
+              ++h;
+              hv = h < myc ? candv[lane * P.lam + h] : -dinf();
+              hi = h < myc ? cand[lane * P.lam + h] : 0x7fffffff;
+            }
             if (lane == 0) sel[i >> 5] |= 1u << (i & 31);
             ++picked;
           }
@@ -1612,6 +1655,7 @@ decode_kernel(const __grid_constant__ KParams P) {
         }
         __syncthreads();
         F = misc[S_F];
+        FWBF_PH(4)
       }
 
       if (F == 0) {
