@@ -1578,6 +1578,10 @@ decode_kernel(const __grid_constant__ KParams P) {
             int i = si[0];
             warp_amax_redux(v, i);
             if (i == 0x7fffffff) break; // the warp's columns are exhausted (warp-uniform)
+            // thresholded: a value <= 0 is never picked, so a warp's list ends at
+            // its first one -- kept only as entry 0 (the global argmax of the
+            // stall policy is the best of the warps' first entries)
+            if (P.mlp_thr && r > 0 && !(v > 0.0)) break;
             if (si[0] == i) { // this lane's head won: pop it
 #pragma unroll
               for (int q = 0; q + 1 < KS; ++q) { sv[q] = sv[q + 1]; si[q] = si[q + 1]; }
@@ -1600,6 +1604,7 @@ decode_kernel(const __grid_constant__ KParams P) {
             }
             warp_amax_redux(v, i);
             if (i == 0x7fffffff) break; // the warp's columns are exhausted (warp-uniform)
+            if (P.mlp_thr && r > 0 && !(v > 0.0)) break; // see above
             if ((i & 31) == lane) taken |= 1u << (i / T);
             if (lane == 0) { cand[warp * P.lam + r] = i; candv[warp * P.lam + r] = v; }
             cnt = r + 1;
