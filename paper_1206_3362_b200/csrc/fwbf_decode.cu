@@ -1613,9 +1613,11 @@ decode_kernel(const __grid_constant__ KParams P) {
         }
         __syncthreads();
         if (warp == 0) {
-          for (int w2 = lane; w2 < zw; w2 += 32) sel[w2] = 0u;
+          const bool small = P.lam <= 32; // picks fit the lanes: ascending order by ranking
+          if (!small)
+            for (int w2 = lane; w2 < zw; w2 += 32) sel[w2] = 0u;
           const int myc = lane < nwarps ? ccnt[lane] : 0;
-          int h = 0, picked = 0;
+          int h = 0, picked = 0, mypick = 0x7fffffff;
           double hv = myc > 0 ? candv[lane * P.lam] : -dinf(); // this lane's list head
           int hi = myc > 0 ? cand[lane * P.lam] : 0x7fffffff;
           __syncwarp();
@@ -1631,31 +1633,43 @@ decode_kernel(const __grid_constant__ KParams P) {
               hv = h < myc ? candv[lane * P.lam + h] : -dinf();
               hi = h < myc ? cand[lane * P.lam + h] : 0x7fffffff;
             }
-            if (lane == 0) sel[i >> 5] |= 1u << (i & 31);
+            if (small) {
+              if (lane == r) mypick = i;
+            } else if (lane == 0) {
+              sel[i >> 5] |= 1u << (i & 31);
+            }
             ++picked;
           }
-          __syncwarp();
           int cnt = 0;
-          if (picked)
-            for (int base = 0; base < zw; base += 32) {
-              const int w2 = base + lane;
-              const uint32_t word = (w2 < zw) ? sel[w2] : 0u;
-              int c = __popc(word);
-              int incl = c;
+          if (small) {
+            // lane r holds pick r; its place in ascending order = picks below it
+            int pos = 0;
+            for (int l = 0; l < picked; ++l) pos += __shfl_sync(FULL_MASK, mypick, l) < mypick;
+            if (lane < picked) flips[pos] = mypick;
+            cnt = picked;
+          } else {
+            __syncwarp();
+            if (picked)
+              for (int base = 0; base < zw; base += 32) {
+                const int w2 = base + lane;
+                const uint32_t word = (w2 < zw) ? sel[w2] : 0u;
+                int c = __popc(word);
+                int incl = c;
 #pragma unroll
-              for (int off = 1; off < 32; off <<= 1) {
-                const int t2 = __shfl_up_sync(FULL_MASK, incl, off);
-                if (lane >= off) incl += t2;
+                for (int off = 1; off < 32; off <<= 1) {
+                  const int t2 = __shfl_up_sync(FULL_MASK, incl, off);
+                  if (lane >= off) incl += t2;
+                }
+                int pos = cnt + incl - c;
+                uint32_t wd = word;
+                while (wd) {
+                  const int bit = __ffs(wd) - 1;
+                  wd &= wd - 1;
+                  flips[pos++] = w2 * 32 + bit;
+                }
+                cnt += __shfl_sync(FULL_MASK, incl, 31);
               }
-              int pos = cnt + incl - c;
-              uint32_t wd = word;
-              while (wd) {
-                const int bit = __ffs(wd) - 1;
-                wd &= wd - 1;
-                flips[pos++] = w2 * 32 + bit;
-              }
-              cnt += __shfl_sync(FULL_MASK, incl, 31);
-            }
+          }
           if (lane == 0) misc[S_F] = cnt;
         }
         __syncthreads();
