@@ -17,8 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.dirname(HERE)
 REPO = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libfwbf_b200.so")
-SOURCES = ["fwbf_decode.cu", "fwbf_explicit.cu", "fwbf_qc.cu", "fwbf_noise.cu", "fwbf_stage.cu", "fwbf_api.cu"]
-HEADERS = ["fwbf_internal.h", "fwbf_noise.cuh"]
+SOURCES = ["fwbf_decode.cu", "fwbf_circ.cu", "fwbf_explicit.cu", "fwbf_qc.cu", "fwbf_noise.cu", "fwbf_stage.cu", "fwbf_api.cu"]
+HEADERS = ["fwbf_internal.h", "fwbf_noise.cuh", "fwbf_device.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -28,6 +28,7 @@ template <typename YT>
 __global__ void noise_kernel(unsigned long long seed, long long first, long long count, double sigma,
                              const uint32_t *codeword, YT *y, long long ld, int n, int pm);
 template <int DV> __global__ void xdecode_kernel(const __grid_constant__ XParams P);
+template <int KC, int TB, int WT, int NN> __global__ void cdecode_kernel(const __grid_constant__ KParams P);
 template <int TPC> __global__ void qdecode_kernel(const __grid_constant__ QParams P);
 template <typename T> __global__ void stage_hard_decision(const T *, long long, uint8_t *);
 __global__ void stage_syndrome(const int *, const int *, int, int, const uint8_t *, long long, uint8_t *);
@@ -485,6 +486,31 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
   P.off_red = take(32 * 8 + 32 * 4);
   P.off_misc = take(16 * 4 + 64 * 4);
   P.smem_bytes = o;
+}
+
+// Shared memory of the filtered circulant kernel (fwbf_circ.cu): the kernel's
+// compile-time layout (CLayout), copied into the parameter block so the gather
+// offsets (uoff) can be computed from it.  EG(1023): 40 KB, 5 CTAs/SM.
+template <int KC, int TB, int WT, int NN> static void layout_c(KParams &P) {
+  using L = fwbf::CLayout<NN, KC * TB, WT>;
+  P.ystage_bytes = L::YSTB;
+  P.off_ystage = L::YST;
+  P.off_y = L::YST;
+  P.off_e = L::E;
+  P.off_fa = L::FA;
+  P.off_fb = L::FB;
+  P.off_m2s = L::M2;
+  P.off_a2m = L::A2;
+  P.off_corr = L::CORR;
+  P.off_sbits = L::SB;
+  P.off_zbits = L::ZB;
+  P.fd_words = L::FDW;
+  P.off_fd = L::FD;
+  P.off_blkv = L::BV;
+  P.off_blki = L::BI;
+  P.off_offs = L::ROT;
+  P.off_misc = L::MISC;
+  P.smem_bytes = L::BYTES;
 }
 
 // Launch-plan cache: the dynamic shared-memory attribute and the occupancy of
@@ -1021,6 +1047,21 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   if (c->m > 32 * T || T > 1024)
     return fail(FWBF_EUNSUPPORTED, "%d checks exceed the 32 x %d per-thread syndrome registers", c->m,
                 std::min(T, 1024));
+  // FWBF on float32 y, circulant weight compiled in, filtered metric: the
+  // round-3 kernel (fwbf_circ.cu) decodes every frame its guard admits and
+  // defers the rest to this MODE 2 kernel, which then runs over that list.
+  const void *ckern = nullptr;
+  void (*clayout)(KParams &) = nullptr;
+  if (mode2 && sizeof(YT) == 4 && kwt > 0 && c->m == c->n && p->weight_mode == FWBF_WEIGHTS_IMWBF &&
+      p->block_len_p >= 16 && !P.force_ordered && !getenv("FWBF_NO_CDEC")) {
+#define FWBF_PICK_C(KC_, TB_, WT_, NN_)                                        \
+    if (kc == KC_ && T == TB_ && kwt == WT_ && c->n == NN_) {                  \
+      ckern = (const void *)fwbf::cdecode_kernel<KC_, TB_, WT_, NN_>;          \
+      clayout = layout_c<KC_, TB_, WT_, NN_>;                                  \
+    }
+    FWBF_CIRC_CONFIGS(FWBF_PICK_C)
+#undef FWBF_PICK_C
+  }
   const bool compact = circ && sizeof(YT) == 4 && c->w <= 32 && !getenv("FWBF_NO_COMPACT");
   // staged input rows (TMA bulk copy one frame ahead): compile-time-shape
   // circulant float32 kernels; rows must be 16-byte aligned and hold the
@@ -1029,7 +1070,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   // Staging claims the frame queue one frame ahead, so a CTA holding a slow
   // frame also holds its next one: only worth it when the batch is many
   // frames per CTA (small batches are latency-bound and lose their tail).
-  bool ystage = circ && sizeof(YT) == 4 && kwt > 0 && !metric_out && !getenv("FWBF_NO_YSTAGE") &&
+  bool ystage = !ckern && circ && sizeof(YT) == 4 && kwt > 0 && !metric_out && !getenv("FWBF_NO_YSTAGE") &&
                 ((uintptr_t)y % 16) == 0 && row_bytes % 16 == 0 &&
                 ((c->n * (long long)sizeof(YT) + 15) & ~15LL) <= row_bytes &&
                 (batch >= 128LL * c->sm_count || getenv("FWBF_FORCE_YSTAGE"));
@@ -1121,6 +1162,58 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     if (!phase_buf) CUDA_TRY(cudaMalloc((void **)&phase_buf, 8 * sizeof(long long)));
     CUDA_TRY(cudaMemsetAsync(phase_buf, 0, 8 * sizeof(long long), stream));
     P.phase_cycles = phase_buf;
+  }
+  if (ckern) {
+    KParams Q = P; // the filtered circulant kernel's own layout, TMA-staged rows when they qualify
+    clayout(Q);
+    const long long row_bytes = ld * (long long)sizeof(YT);
+    Q.y_stage = !getenv("FWBF_NO_YSTAGE") && ((uintptr_t)y % 16) == 0 && row_bytes % 16 == 0 &&
+                (long long)Q.ystage_bytes <= row_bytes &&
+                (batch >= 128LL * c->sm_count || getenv("FWBF_FORCE_YSTAGE"));
+    Q.alias_y = 0;
+    for (int j = 0; j < c->w; ++j) {
+      const int d = c->n - c->off[j];
+      Q.uoff[j] = ((d & 1) ? Q.off_fb + 4 : Q.off_fa) + 4 * d;
+    }
+    int cper = 0;
+    if (Q.smem_bytes <= c->smem_optin) {
+      rc = plan_occupancy(c->device, ckern, T, Q.smem_bytes, &cper);
+      if (rc) return rc;
+    }
+    if (cper >= 1) {
+      // frames outside the filtered guard: appended to a list (count in a
+      // second queue slot), decoded by decode_kernel afterwards (third slot)
+      unsigned *dcount = c->d_work + (c->work_slot.fetch_add(1) % kWorkRing);
+      unsigned *lwork = c->d_work + (c->work_slot.fetch_add(1) % kWorkRing);
+      CUDA_TRY(cudaMemsetAsync(dcount, 0, sizeof(unsigned), stream));
+      CUDA_TRY(cudaMemsetAsync(lwork, 0, sizeof(unsigned), stream));
+      int *dlist = nullptr;
+      static std::once_flag pool_once[64];
+      std::call_once(pool_once[c->device & 63], [&] {
+        // keep freed blocks in the device's default pool: the per-launch
+        // defer list is then a pool hit, not a fresh mapping every call
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
+          uint64_t keep = ~0ull;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+      });
+      CUDA_TRY(cudaMallocAsync((void **)&dlist, (size_t)batch * sizeof(int), stream));
+      Q.defer_list = dlist;
+      Q.defer_count = dcount;
+      const long long cgrid = std::min<long long>(batch, (long long)cper * c->sm_count);
+      void *cargs[] = {&Q};
+      CUDA_TRY(cudaLaunchKernel(ckern, dim3((unsigned)cgrid), dim3(T), cargs, Q.smem_bytes, stream));
+      CUDA_TRY(cudaGetLastError());
+      P.frame_list = dlist;
+      P.frame_count = dcount;
+      P.work_counter = lwork;
+      void *args[] = {&P};
+      CUDA_TRY(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(T), args, P.smem_bytes, stream));
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaFreeAsync(dlist, stream));
+      return FWBF_OK;
+    }
   }
   void *args[] = {&P};
   CUDA_TRY(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(T), args, P.smem_bytes, stream));

@@ -1,0 +1,560 @@
+// fwbf_circ.cu -- filtered FWBF decoding of circulant (EG) codes on B200 (round 3).
+//
+// The headline path: FWBF (decoders.py:156-167, :181-183) on float32 y for a
+// cyclic EG code whose length and weight are compiled in.  One persistent CTA
+// decodes one frame at a time (frames from an atomic queue, the next frame's y
+// row staged by a TMA bulk copy).  Same arithmetic contract as decode_kernel's
+// MODE 2: the metric is summed in fp32 (within a
+// per-frame bound fdelta of the exact one) and every block decision the bound
+// leaves open is re-decided on exact column sums, so flips, iterations and
+// flags equal the reference's.  Frames outside the filtered path's guard
+// (non-finite y, all-zero |y|, a dynamic range beyond the fp64 guard) are
+// appended to a defer list that decode_kernel then decodes on its exact paths.
+//
+// What differs from decode_kernel MODE 2 is the iteration's structure, built
+// for the regime that dominates the run time (frames that fail to converge
+// flip ~30 of 33 blocks per iteration and toggle ~40 % of the checks):
+//   * selection: one warp per p-block, lanes over its columns; block maximum,
+//     first index and the band test by REDUX on order-preserving keys (no
+//     shuffle butterflies, every warp busy); lane jj of a warp keeps its jj-th
+//     block's result and the warp applies all its flips in one lane pass;
+//   * flips: the winning column n sets bits n and n + N of a doubled flip
+//     bitmap (two RED.OR per flip instead of W syndrome atomics);
+//   * toggles: the warp that owns syndrome word w computes which of its 32
+//     checks toggled as XOR_j window(flips, 32 w + c_j) -- per lane one
+//     offset c_j, a funnel shift of two bitmap words, one REDUX.XOR -- and
+//     rewrites its own syndrome word, hard-decision word and the toggled
+//     checks' signed minima and argmin corrections (no atomics on the
+//     syndrome, no compare against remembered syndrome bits).
+// The shared-memory layout is a compile-time function of the code (CLayout,
+// fwbf_internal.h), so every shared access is [base + immediate].  Three CTA
+// barriers per iteration (metric ready, flips chosen, state refreshed); the
+// flip bitmap, flip count and syndrome weight alternate between two slots by
+// iteration parity so no extra barrier clears them.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "fwbf_b200.h"
+#include "fwbf_internal.h"
+#include "fwbf_device.cuh"
+
+#ifndef FWBF_CMINB_256
+#define FWBF_CMINB_256 5
+#endif
+
+namespace fwbf {
+
+// order-preserving 32-bit key of a float (-0.0 and +0.0 tie; no NaN here)
+__device__ __forceinline__ uint32_t fkey(float v) {
+  const uint32_t u = __float_as_uint(v + 0.0f);
+  return (u >> 31) ? ~u : (u | 0x80000000u);
+}
+// 2^e for a normal exponent (|e| <= 1022), without ldexp's range handling
+__device__ __forceinline__ double pow2d(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
+__device__ __forceinline__ float fkey_val(uint32_t k) {
+  return __uint_as_float((k >> 31) ? (k & 0x7fffffffu) : ~k);
+}
+
+// Refresh of toggled check m = tid + KK TB (compile-time KK): negate its signed
+// min1 in both doubled copies and move its argmin column's coarse correction
+// by +-2 Dc (the new sign); shared addresses in registers, KK TB as immediates.
+template <int KK, int KC, int TB, int NN, bool GO = (KK < KC)> struct CRefresh {
+  static __device__ __forceinline__ void run(const uint32_t (&tg)[KC], int lane, uint32_t aFA, uint32_t aFB,
+                                             uint32_t aM2, uint32_t aA2, uint32_t aC, float invG) {
+    if ((tg[KK] >> lane) & 1u) {
+      float v, mn2;
+      unsigned short a2;
+      asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(aFA), "n"(4 * KK * TB));
+      v = -v;
+      asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(aFA), "n"(4 * KK * TB), "f"(v));
+      asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(aFA), "n"(4 * (KK * TB + NN)), "f"(v));
+      asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(aFB), "n"(4 * KK * TB), "f"(v));
+      asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(aFB), "n"(4 * (KK * TB + NN)), "f"(v));
+      asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(mn2) : "r"(aM2), "n"(4 * KK * TB));
+      asm volatile("ld.shared.u16 %0, [%1+%2];" : "=h"(a2) : "r"(aA2), "n"(2 * KK * TB));
+      const int dc = coarse_dc(mn2, fabsf(v), invG);
+      asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(aC + 4u * (uint32_t)a2), "r"(signbit(v) ? -2 * dc : 2 * dc));
+    }
+    CRefresh<KK + 1, KC, TB, NN>::run(tg, lane, aFA, aFB, aM2, aA2, aC, invG);
+  }
+};
+template <int KK, int KC, int TB, int NN> struct CRefresh<KK, KC, TB, NN, false> {
+  static __device__ __forceinline__ void run(const uint32_t (&)[KC], int, uint32_t, uint32_t, uint32_t, uint32_t,
+                                             uint32_t, float) {}
+};
+
+template <int KC, int TB, int WT, int NN>
+__global__ void __launch_bounds__(TB, TB == 256 ? FWBF_CMINB_256 : 1024 / TB)
+cdecode_kernel(const __grid_constant__ KParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using L = CLayout<NN, KC * TB, WT>;
+  constexpr int NW = TB / 32;
+  constexpr int NP = KC / 2; // column pairs per thread in the gather
+  constexpr int N = NN;      // cyclic code: N columns, N checks
+  constexpr int ZW = L::ZW;  // words of a bit vector over N
+  constexpr uint32_t LASTW = (N & 31) ? (1u << (N & 31)) - 1u : 0xffffffffu;
+  static_assert(KC % 2 == 0 && WT > 0 && WT <= 64 && KC * TB >= N && KC * NW >= ZW, "shape");
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+
+  float *ybuf = reinterpret_cast<float *>(smem_raw + L::YST); // y row (staged or loaded)
+  float *Efl = reinterpret_cast<float *>(smem_raw + L::E);    // filtered metric
+  float *yabs = Efl + L::EP;                                  // |y_n| (exact, float)
+  float *sFA = reinterpret_cast<float *>(smem_raw + L::FA);   // signed min1, doubled
+  float *sFB = reinterpret_cast<float *>(smem_raw + L::FB);   // the same, shifted one element
+  float *sM2 = reinterpret_cast<float *>(smem_raw + L::M2);   // min2 per check
+  uint16_t *sA2 = reinterpret_cast<uint16_t *>(smem_raw + L::A2); // argmin column per check
+  int *sCorr = reinterpret_cast<int *>(smem_raw + L::CORR);   // coarse argmin correction per column
+  uint32_t *sbits = reinterpret_cast<uint32_t *>(smem_raw + L::SB);
+  uint32_t *zbits = reinterpret_cast<uint32_t *>(smem_raw + L::ZB);
+  uint32_t *fdb = reinterpret_cast<uint32_t *>(smem_raw + L::FD); // [2][FDW] doubled flip bitmaps
+  double *blk_v = reinterpret_cast<double *>(smem_raw + L::BV);
+  int *blk_i = reinterpret_cast<int *>(smem_raw + L::BI);
+  int *rot = reinterpret_cast<int *>(smem_raw + L::ROT);      // rotated offsets (ascending row walk)
+  int *misc = reinterpret_cast<int *>(smem_raw + L::MISC);
+  float *redf = reinterpret_cast<float *>(misc + 16);
+  enum { S_FRAME = 0, S_SWT0, S_SWT1, S_F0, S_F1, S_PATH, S_EQ, S_VMAX, S_YMAX, S_NONFIN };
+
+  for (int j = tid; j < WT; j += TB) {
+    rot[j] = P.off[j] - N; // check m's columns in ascending order: the wrapped
+    rot[WT + j] = P.off[j]; // ones (m + c_j - N) first, from jwtab[m] on
+  }
+  if (tid == 0) misc[S_NONFIN] = 0;
+  // this lane's offsets for the toggle windows: j = lane (and lane + 32)
+  const int c0 = lane < WT ? P.off[lane] : 0;
+  const int c1 = (WT > 32 && lane + 32 < WT) ? P.off[lane + 32] : 0;
+
+  // per-CTA counters (FWBF_CNT_* order), flushed once at the end
+  __shared__ unsigned long long ctr[FWBF_CNT_EDGE_VISITS + 1];
+  if (tid <= FWBF_CNT_EDGE_VISITS) ctr[tid] = 0ull;
+
+  __shared__ __align__(8) uint64_t ystage_bar;
+  unsigned ystage_phase = 0;
+  const bool ystage = P.y_stage != 0;
+  if (ystage && tid == 0) {
+    mbar_init(&ystage_bar, 1);
+    const unsigned t0 = atomicAdd(P.work_counter, 1u);
+    misc[S_FRAME] = (int)t0;
+    if ((long long)t0 < P.batch)
+      bulk_row_to_smem(ybuf, reinterpret_cast<const float *>(P.y) + (long long)t0 * P.ld, (unsigned)L::YSTB,
+                       &ystage_bar);
+  }
+
+  for (;;) {
+    __syncthreads();
+    if (!ystage && tid == 0) misc[S_FRAME] = (int)atomicAdd(P.work_counter, 1u);
+    __syncthreads();
+    const unsigned fu = (unsigned)misc[S_FRAME];
+    if ((long long)fu >= P.batch) break;
+    const int f = (int)fu; // batch <= 2^31 - 1
+    if (ystage) {
+      mbar_wait(&ystage_bar, ystage_phase);
+      ystage_phase ^= 1u;
+    }
+
+    // ---------------- init 1: y, hard decisions, guard statistics ----------------
+    float lmin = INFINITY, lmax = 0.f;
+    bool nonfin = false;
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+      const int n = tid + k * TB;
+      const bool ok = n < N;
+      float v = 0.f;
+      if (ok) v = ystage ? ybuf[n] : __ldg(reinterpret_cast<const float *>(P.y) + (long long)f * P.ld + n);
+      if (ok) ybuf[n] = v + 0.f; // -0.0 -> +0.0: the sign bit is the hard decision (y < 0)
+      const uint32_t b = __ballot_sync(FULL_MASK, ok && v < 0.f);
+      if (lane == 0 && k * TB + warp * 32 < N) zbits[(k * TB + warp * 32) >> 5] = b;
+      if (ok) {
+        nonfin |= !isfinite(v);
+        const float a = fabsf(v);
+        if (a > 0.f) lmin = fminf(lmin, a);
+        lmax = fmaxf(lmax, a);
+        sCorr[n] = 0;
+      }
+    }
+    if (tid < 2 * L::FDW) fdb[tid] = 0u;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      lmin = fminf(lmin, __shfl_xor_sync(FULL_MASK, lmin, off));
+      lmax = fmaxf(lmax, __shfl_xor_sync(FULL_MASK, lmax, off));
+    }
+    nonfin = __any_sync(FULL_MASK, nonfin);
+    if (lane == 0) {
+      redf[warp] = lmin;
+      redf[32 + warp] = lmax;
+      if (nonfin) misc[S_NONFIN] = 1;
+    }
+    if (tid == 0) {
+      misc[S_SWT0] = 0;
+      misc[S_SWT1] = 0;
+      misc[S_F0] = 0;
+      misc[S_F1] = 0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      float mn = INFINITY, mx = 0.f;
+      for (int w2 = 0; w2 < NW; ++w2) { mn = fminf(mn, redf[w2]); mx = fmaxf(mx, redf[32 + w2]); }
+      // decode_kernel MODE 2's filtered-path condition: finite y, some |y| > 0,
+      // every sum of 2 W weights exact in fp64 (2 W max|y| < 2^53 q with
+      // q = 2^(e_min - 23)), and the quantum within the float range the
+      // filter's grid needs.  Everything else goes to the exact kernel.
+      int keep = 0, eq = 0;
+      if (!misc[S_NONFIN] && mn < INFINITY) {
+        int e = ((__float_as_int(mn) >> 23) & 0xff) - 127;
+        if (e < -126) e = -126;
+        eq = e - 23;
+        keep = (2.0 * (double)WT * (double)mx < ldexp(1.0, 30 + e)) && eq >= -123 && eq <= 77;
+      }
+      misc[S_NONFIN] = 0;
+      misc[S_PATH] = keep;
+      misc[S_EQ] = eq;
+      misc[S_YMAX] = __float_as_int(mx);
+      misc[S_VMAX] = 0;
+      if (!keep) P.defer_list[atomicAdd(P.defer_count, 1u)] = f;
+    }
+    __syncthreads();
+    if (!misc[S_PATH]) {
+      if (ystage && tid == 0) { // every read of ybuf for this frame is done
+        const unsigned t1 = atomicAdd(P.work_counter, 1u);
+        misc[S_FRAME] = (int)t1;
+        if ((long long)t1 < P.batch)
+          bulk_row_to_smem(ybuf, reinterpret_cast<const float *>(P.y) + (long long)t1 * P.ld, (unsigned)L::YSTB,
+                           &ystage_bar);
+      }
+      continue;
+    }
+
+    // ---------------- init 2: check minima, syndrome, signed weights -------------
+    const int eq = misc[S_EQ]; // quantum q = 2^eq
+    const float ymaxf = __int_as_float(misc[S_YMAX]);
+    // coarse grid G = 2^gsh q for the argmin corrections: |Dc| <= 2^24
+    const int gbits = ilogbf(ymaxf) + 1 - eq;
+    const int gsh = gbits > 24 ? gbits - 24 : 0;
+    const float Gf = ldexpf(1.f, gsh + eq);
+    const float invGf = ldexpf(1.f, -(gsh + eq));
+    {
+      float wmax = 0.f;
+      int swt = 0;
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        const int m = tid + kk * TB;
+        const bool ok = m < N;
+        float min1 = INFINITY, min2 = INFINITY;
+        int ac = 0x7fffffff;
+        uint32_t sgn = 0;
+        if (ok) {
+          // columns in ascending order, so strict < keeps the lowest column
+          // on ties (decoders.py:94-103); min2 = second smallest of the
+          // multiset; parity = XOR of the sign bits
+          const int *orr = rot + __ldg(P.jwtab + m);
+#pragma unroll 8
+          for (int t = 0; t < WT; ++t) {
+            const int c = m + orr[t];
+            const float yv = ybuf[c];
+            sgn ^= __float_as_uint(yv);
+            const float a = fabsf(yv);
+            const bool lt = a < min1;
+            min2 = fminf(min2, fmaxf(min1, a));
+            min1 = fminf(min1, a);
+            ac = lt ? c : ac;
+          }
+        }
+        const bool par = ok && (sgn >> 31);
+        const uint32_t b = __ballot_sync(FULL_MASK, par);
+        if (lane == 0 && kk * TB + warp * 32 < N) {
+          sbits[(kk * TB + warp * 32) >> 5] = b;
+          swt += __popc(b);
+        }
+        if (ok) {
+          wmax = fmaxf(wmax, min1);
+          const float s1v = par ? min1 : -min1;
+          sFA[m] = s1v;
+          sFA[m + N] = s1v;
+          sFB[m + 1] = s1v;
+          sFB[m + N + 1] = s1v;
+          sA2[m] = (uint16_t)ac;
+          sM2[m] = min2;
+          const int Dc = coarse_dc(min2, min1, invGf);
+          atomicAdd(&sCorr[ac], par ? Dc : -Dc);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KC; ++k)
+        if (tid + k * TB < N) yabs[tid + k * TB] = fabsf(ybuf[tid + k * TB]);
+#pragma unroll
+      for (int off = 16; off; off >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(FULL_MASK, wmax, off));
+      if (lane == 0) {
+        atomicMax(&misc[S_VMAX], __float_as_int(wmax));
+        if (swt) atomicAdd(&misc[S_SWT0], swt);
+      }
+    }
+    __syncthreads();
+    if (ystage && tid == 0) { // ybuf is dead for this frame: claim the next one and start its copy
+      const unsigned t1 = atomicAdd(P.work_counter, 1u);
+      misc[S_FRAME] = (int)t1;
+      if ((long long)t1 < P.batch)
+        bulk_row_to_smem(ybuf, reinterpret_cast<const float *>(P.y) + (long long)t1 * P.ld, (unsigned)L::YSTB,
+                         &ystage_bar);
+    }
+    // filter bound (decode_kernel MODE 2): W sequential
+    // fp32 adds of partial sums <= k vmax, the float finalize, the coarse
+    // correction grid; fd2 = the band width 2 fdelta plus the rounding of
+    // (max - fd2), both rounded outwards
+    float fdp, fd2;
+    {
+      const double vmax = (double)__int_as_float(misc[S_VMAX]);
+      const double ymax = (double)ymaxf;
+      const double fdelta = ldexp(vmax * (0.5 * (double)WT * (double)(WT + 1)) * 1.001, -24) +
+                            ldexp(((double)WT + P.alpha + 1.0) * ymax, -22) + 0.5 * (double)WT * (double)Gf +
+                            ldexp((double)WT * ymax, -23);
+      fdp = __double2float_ru(fdelta);
+      fd2 = __double2float_ru(2.0 * fdelta + ldexp(((double)WT + P.alpha + 1.0) * ymax, -22));
+    }
+
+    // ---------------- iterations (decoders.py:204-229) -------------------------
+    int k = 0, conv = 0, stalled = 0;
+    int nflips = 0; // flips so far = this frame's flip-log position
+    const float alf = (float)P.alpha;
+    const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    for (;;) {
+      if (misc[S_SWT0 + (k & 1)] == 0) { conv = 1; break; }
+      if (k >= P.kmax) break;
+
+      // ---- filtered Eq.(1) metric: thread tid owns column pairs (2 tid + 2 TB q, +1);
+      // per offset one 8-byte LDS [base + uoff_j] brings both columns' signed
+      // min1, one FADD2 sums them
+      {
+        unsigned long long hs[NP];
+#pragma unroll
+        for (int qp = 0; qp < NP; ++qp) hs[qp] = 0ull;
+        const uint32_t baseT = s0 + 8u * (uint32_t)tid;
+#pragma unroll
+        for (int j = 0; j < WT; ++j) GatherF2<0, NP, TB>::run(hs, baseT + (uint32_t)P.uoff[j]);
+#pragma unroll
+        for (int qp = 0; qp < NP; ++qp) {
+          const float2 h = f2unpack(hs[qp]);
+          const int n = 2 * tid + 2 * TB * qp;
+          if (n + 1 < N) {
+            const int2 cc = *reinterpret_cast<const int2 *>(sCorr + n);
+            const float2 ya = *reinterpret_cast<const float2 *>(yabs + n);
+            *reinterpret_cast<float2 *>(Efl + n) =
+                make_float2(__fsub_rn(__fmaf_rn((float)cc.x, Gf, h.x), __fmul_rn(alf, ya.x)),
+                            __fsub_rn(__fmaf_rn((float)cc.y, Gf, h.y), __fmul_rn(alf, ya.y)));
+          } else if (n < N) {
+            Efl[n] = __fsub_rn(__fmaf_rn((float)sCorr[n], Gf, h.x), __fmul_rn(alf, yabs[n]));
+          }
+        }
+      }
+      __syncthreads(); // B1: metric complete
+      if (tid == 0) misc[S_SWT0 + ((k + 1) & 1)] = 0; // read at the top of iteration k - 1
+
+      // ---- selection: warp per p-block (decoders.py:156-167, :181-183) ----
+      // warp w takes blocks w + NW jj; lane jj keeps block jj's result, and
+      // the warp applies all its flips with one pass of its lanes
+      uint32_t *fdc = fdb + (k & 1) * L::FDW;
+      {
+        const int p = P.p;
+        const uint32_t sE = s0 + L::E;
+        double rv = 0.0;
+        int ri = 0;
+        int jj = 0;
+        for (int base = warp * p; base < N; base += NW * p, ++jj) {
+          const int lim = min(p, N - base);
+          float fv, fv2 = -INFINITY;
+          int fi;
+          if (lim <= 32) {
+            fi = base + lane;
+            float e; // (lanes past the block read inside the metric region; masked)
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e) : "r"(sE + 4u * (uint32_t)fi));
+            fv = lane < lim ? e : -INFINITY;
+          } else {
+            fv = -INFINITY;
+            fi = 0x7fffffff;
+            for (int o = lane; o < lim; o += 32) { // ascending per lane, strict >
+              const float e = Efl[base + o];
+              fv2 = fmaxf(fv2, fminf(fv, e));
+              if (e > fv) { fv = e; fi = base + o; }
+            }
+          }
+          const uint32_t ka = fkey(fv);
+          const uint32_t kmx = __reduce_max_sync(FULL_MASK, ka);
+          const int imin = (int)__reduce_min_sync(FULL_MASK, ka == kmx ? (uint32_t)fi : 0xffffffffu);
+          const float fmx = fkey_val(kmx);
+          const float thr = fmx - fd2;
+          // the block's runner-up: the winning lane's second value, every
+          // other lane's first.  Settled when it is more than 2 fdelta below
+          // the maximum (then the approximate argmax is the exact first
+          // maximum) and the maximum is farther than fdelta from 0 (then its
+          // sign is exact); otherwise the columns in the band are re-decided
+          // on exact sums.
+          const float r = fi == imin ? fv2 : fv;
+          if (__any_sync(FULL_MASK, r >= thr) || (fmx > -fdp && fmx <= fdp)) {
+            const double qexp = pow2d(misc[S_EQ]), qinv = pow2d(-misc[S_EQ]);
+            double ve = -dinf();
+            int ie = 0x7fffffff;
+            for (int o = lane; o < lim; o += 32) {
+              const int n = base + o;
+              if (Efl[n] >= thr) amax_combine(ve, ie, exact_split_metric(P, sFA, sA2, sM2, yabs, n, WT, qexp, qinv), n);
+            }
+            warp_amax_redux(ve, ie);
+            if (lane == jj) { rv = ve; ri = ie; }
+            if (lane == 0 && P.filter_stats) atomicAdd((unsigned long long *)P.filter_stats, 1ull);
+          } else if (lane == jj) {
+            rv = (double)fmx;
+            ri = imin;
+          }
+        }
+        const bool mine = lane < jj;
+        const bool flip = mine && rv > 0.0;
+        if (mine) {
+          const int b = warp + lane * NW;
+          blk_v[b] = rv;
+          blk_i[b] = ri;
+        }
+        if (flip) {
+          const int i2 = ri + N;
+          atomicOr(fdc + (ri >> 5), 1u << (ri & 31));
+          atomicOr(fdc + (i2 >> 5), 1u << (i2 & 31));
+        }
+        const uint32_t fm = __ballot_sync(FULL_MASK, flip);
+        if (lane == 0 && fm) atomicAdd(&misc[S_F0 + (k & 1)], __popc(fm));
+      }
+      __syncthreads(); // B2: flips chosen
+      int F = misc[S_F0 + (k & 1)];
+      if (F == 0) {
+        // nothing selected while the syndrome is nonzero (decoders.py:214-222)
+        stalled = 1;
+        if (P.stall == FWBF_STALL_TERMINATE) {
+          if (tid == 0 && P.fliplog_counts) P.fliplog_counts[(long long)f * P.kmax + k] = 0;
+          k += 1;
+          break;
+        }
+        if (warp == 0) {
+          const int nb = P.nblocks;
+          double gv = -dinf();
+          int gi = 0x7fffffff;
+          for (int bb = lane; bb < nb; bb += 32) amax_combine(gv, gi, blk_v[bb], blk_i[bb]);
+          warp_amax(gv, gi);
+          // the block maxima are exact argmaxes, their values within fdelta
+          const double thr = gv - (double)fd2;
+          int nc = 0;
+          for (int bb = lane; bb < nb; bb += 32) nc += blk_v[bb] >= thr;
+          nc = __reduce_add_sync(FULL_MASK, nc);
+          if (nc > 1) {
+            const double qexp = pow2d(misc[S_EQ]), qinv = pow2d(-misc[S_EQ]);
+            double ve = -dinf();
+            int ie = 0x7fffffff;
+            for (int bb = lane; bb < nb; bb += 32)
+              if (blk_v[bb] >= thr)
+                amax_combine(ve, ie, exact_split_metric(P, sFA, sA2, sM2, yabs, blk_i[bb], WT, qexp, qinv), blk_i[bb]);
+            warp_amax(ve, ie);
+            gi = ie;
+            if (lane == 0 && P.filter_stats) atomicAdd((unsigned long long *)P.filter_stats + 1, 1ull);
+          }
+          if (lane == 0) {
+            const int g2 = gi + N;
+            fdc[gi >> 5] |= 1u << (gi & 31);
+            fdc[g2 >> 5] |= 1u << (g2 & 31);
+            if (P.fliplog) P.fliplog[(long long)f * P.fliplog_stride + nflips] = gi;
+          }
+        }
+        F = 1;
+        __syncthreads();
+      } else if (P.fliplog && warp == 0) { // ascending = block order
+        const int nb = P.nblocks;
+        int cnt = 0;
+        for (int base = 0; base < nb; base += 32) {
+          const int bb = base + lane;
+          const bool pos = bb < nb && blk_v[bb] > 0.0;
+          const uint32_t msk = __ballot_sync(FULL_MASK, pos);
+          if (pos)
+            P.fliplog[(long long)f * P.fliplog_stride + nflips + cnt + __popc(msk & ((1u << lane) - 1u))] = blk_i[bb];
+          cnt += __popc(msk);
+        }
+      }
+      if (P.fliplog && tid == 0) P.fliplog_counts[(long long)f * P.kmax + k] = F;
+
+      // ---- toggles and refresh: warp w owns syndrome words w + NW kk ----
+      {
+        if (tid < L::FDW) fdb[((k + 1) & 1) * L::FDW + tid] = 0u; // last read in iteration k - 1
+        if (tid == 0) misc[S_F0 + ((k + 1) & 1)] = 0;
+        // bit b of word wd: check m = 32 wd + b toggles iff an odd number of
+        // its columns m + c_j flipped = XOR over j of the doubled flip
+        // bitmap's window starting at bit 32 wd + c_j (lane j: offset c_j)
+        const uint32_t *fw0 = fdc + warp + (c0 >> 5);
+        const uint32_t *fw1 = fdc + warp + (c1 >> 5);
+        uint32_t tg[KC];
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+          uint32_t win = lane < WT ? __funnelshift_r(fw0[kk * NW], fw0[kk * NW + 1], c0 & 31) : 0u;
+          if (WT > 32) win ^= __funnelshift_r(fw1[kk * NW], fw1[kk * NW + 1], c1 & 31);
+          tg[kk] = __reduce_xor_sync(FULL_MASK, win);
+          if ((kk + 1) * NW > ZW && kk * NW + warp >= ZW) tg[kk] = 0u;          // no such word
+          if ((kk + 1) * NW >= ZW && kk * NW + warp == ZW - 1) tg[kk] &= LASTW; // checks < N
+        }
+        // lane kk rewrites word kk's syndrome and hard decisions
+        uint32_t mine = 0u;
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) mine = lane == kk ? tg[kk] : mine;
+        int pcnt = 0;
+        if (lane < KC) {
+          const int wd = lane * NW + warp;
+          if (wd < ZW) {
+            const uint32_t snew = sbits[wd] ^ mine;
+            sbits[wd] = snew;
+            pcnt = __popc(snew);
+            zbits[wd] ^= fdc[wd] & (wd == ZW - 1 ? LASTW : 0xffffffffu);
+          }
+        }
+        pcnt = __reduce_add_sync(FULL_MASK, pcnt);
+        if (lane == 0 && pcnt) atomicAdd(&misc[S_SWT0 + ((k + 1) & 1)], pcnt);
+        // toggled checks m = tid + kk TB
+        CRefresh<0, KC, TB, NN>::run(tg, lane, s0 + L::FA + 4u * tid, s0 + L::FB + 4u * (tid + 1),
+                                     s0 + L::M2 + 4u * tid, s0 + L::A2 + 2u * tid, s0 + L::CORR, invGf);
+      }
+      nflips += F;
+      k += 1;
+      __syncthreads(); // B3: records, corrections, syndrome weight
+    }
+
+    // ---------------- outputs -----------------------------------------------------
+    if (warp == 0) {
+      int be = 0;
+      for (int w2 = lane; w2 < ZW; w2 += 32) {
+        const uint32_t z = zbits[w2];
+        if (P.z_bits) P.z_bits[(long long)f * P.z_ld + w2] = z;
+        const uint32_t c = P.codeword_bits ? __ldg(P.codeword_bits + w2) : 0u;
+        be += __popc(z ^ c);
+      }
+      be = __reduce_add_sync(FULL_MASK, be);
+      if (lane == 0) {
+        const int flags = (conv ? FWBF_FLAG_CONVERGED : 0) | (stalled ? FWBF_FLAG_STALLED : 0) | FWBF_FLAG_SPLIT32;
+        if (P.iterations) P.iterations[f] = k;
+        if (P.flags) P.flags[f] = (uint8_t)flags;
+        if (P.flips_total) P.flips_total[f] = nflips;
+        if (P.bit_errors) P.bit_errors[f] = be;
+        if (P.iter_hist) atomicAdd((unsigned long long *)&P.iter_hist[k], 1ull);
+        if (be && P.batch_word_err) atomicAdd(&P.batch_word_err[f / P.batch_frames], 1);
+        ctr[FWBF_CNT_FRAMES] += 1ull;
+        ctr[FWBF_CNT_BIT_ERRORS] += (unsigned long long)be;
+        ctr[FWBF_CNT_WORD_ERRORS] += be ? 1ull : 0ull;
+        ctr[FWBF_CNT_ITER_SUM] += (unsigned long long)k;
+        ctr[FWBF_CNT_FLIP_SUM] += (unsigned long long)nflips;
+        ctr[FWBF_CNT_STALLS] += (unsigned long long)stalled;
+        ctr[FWBF_CNT_CONVERGED] += (unsigned long long)conv;
+        ctr[FWBF_CNT_EDGE_VISITS] += (unsigned long long)(P.n_edges * k);
+      }
+    }
+  }
+
+  if (P.counters && tid <= FWBF_CNT_EDGE_VISITS && tid != FWBF_CNT_ORDERED_FRAMES && ctr[FWBF_CNT_FRAMES])
+    atomicAdd((unsigned long long *)P.counters + tid, ctr[tid]);
+}
+
+#define FWBF_INST_CIRC(KC, TB, WT, NN) template __global__ void cdecode_kernel<KC, TB, WT, NN>(const __grid_constant__ KParams);
+FWBF_CIRC_CONFIGS(FWBF_INST_CIRC)
+
+} // namespace fwbf

@@ -32,6 +32,43 @@ constexpr int kMaxQcBlocks = 256;  // quasi-cyclic shift table entries in the pa
   X(double, true, 4, 256, 32)   \
   X(double, true, 4, 1024, 64)
 
+// Filtered FWBF kernel for cyclic EG codes (fwbf_circ.cu): (KC, TB, WT, N),
+// the code length and weight compiled in (EG(255), EG(1023), EG(4095)).
+#define FWBF_CIRC_CONFIGS(X) \
+  X(2, 128, 16, 255)         \
+  X(4, 256, 32, 1023)        \
+  X(4, 1024, 64, 4095)
+
+// Its shared-memory layout (byte offsets), a compile-time function of the code
+// so every access in the kernel is [base + immediate]; the host reads the same
+// constants (layout_c in fwbf_api.cu).  Blocks: p >= 16, so at most
+// ceil(N / 16) of them.
+template <int NN, int COVER, int WT> struct CLayout {
+  static constexpr int al(int x) { return (x + 15) & ~15; }
+  static constexpr int mx(int a, int b) { return a > b ? a : b; }
+  static constexpr int EP = (NN + 1) & ~1;     // |y| after the metric (even: float2 reads)
+  static constexpr int ZW = (NN + 31) / 32;    // words of a bit vector over N
+  static constexpr int FDW = 2 * ZW + 2;       // doubled flip bitmap words (windows read one past 2N)
+  static constexpr int NBMAX = (NN + 15) / 16;
+  static constexpr int DBLF = (2 * NN + mx(0, COVER - NN) + 2 + 31) / 32 * 32;
+  static constexpr int YST = 0;                // y row (TMA staging target), 16-byte aligned
+  static constexpr int YSTB = al(NN * 4);
+  static constexpr int E = YST + YSTB;         // float metric [EP] + |y| [N]
+  static constexpr int FA = E + al((EP + mx(NN, COVER)) * 4);
+  static constexpr int FB = FA + al(DBLF * 4);
+  static constexpr int M2 = FB + al(DBLF * 4);
+  static constexpr int A2 = M2 + al(NN * 4);
+  static constexpr int CORR = A2 + al(NN * 2);
+  static constexpr int SB = CORR + al(mx(NN, COVER) * 4);
+  static constexpr int ZB = SB + al(ZW * 4);
+  static constexpr int FD = ZB + al(ZW * 4);
+  static constexpr int BV = FD + al(2 * FDW * 4);
+  static constexpr int BI = BV + al(NBMAX * 8);
+  static constexpr int ROT = BI + al(NBMAX * 4);
+  static constexpr int MISC = ROT + al(2 * WT * 4);
+  static constexpr int BYTES = MISC + al(80 * 4);
+};
+
 struct KParams {
   // ---- code (H) ----
   int n, m;          // columns (bits), rows (checks)
@@ -97,6 +134,16 @@ struct KParams {
   int y_stage;      // 1: enabled (16-byte aligned rows; ybuf = the staging buffer)
   int off_ystage;   // staging buffer byte offset (16-byte aligned)
   int ystage_bytes; // bytes per copy: N * sizeof(YT) rounded up to 16 (<= ld * sizeof(YT))
+  // Frame lists (round 3).  The filtered circulant kernel (fwbf_circ.cu)
+  // decodes the frames that pass its path guard and appends the others to
+  // defer_list (count in *defer_count); decode_kernel then runs over that list
+  // (frame_list / *frame_count) instead of 0..batch-1.
+  int *defer_list;
+  unsigned *defer_count;
+  const int *frame_list;
+  const unsigned *frame_count;
+  int off_fd;  // fwbf_circ.cu: two doubled flip bitmaps (iteration parity)
+  int fd_words; // words per flip bitmap
 };
 
 // One-frame-per-warp FWBF kernel for small explicit codes (fwbf_explicit.cu).
