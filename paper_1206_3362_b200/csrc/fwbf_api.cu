@@ -28,7 +28,7 @@ template <typename YT>
 __global__ void noise_kernel(unsigned long long seed, long long first, long long count, double sigma,
                              const uint32_t *codeword, YT *y, long long ld, int n, int pm);
 template <int DV> __global__ void xdecode_kernel(const __grid_constant__ XParams P);
-template <int KC, int TB, int WT, int NN> __global__ void cdecode_kernel(const __grid_constant__ KParams P);
+template <int KC, int TB, int WT, int NN, int PB> __global__ void cdecode_kernel(const __grid_constant__ KParams P);
 template <int TPC> __global__ void qdecode_kernel(const __grid_constant__ QParams P);
 template <typename T> __global__ void stage_hard_decision(const T *, long long, uint8_t *);
 __global__ void stage_syndrome(const int *, const int *, int, int, const uint8_t *, long long, uint8_t *);
@@ -1054,10 +1054,11 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   void (*clayout)(KParams &) = nullptr;
   if (mode2 && sizeof(YT) == 4 && kwt > 0 && c->m == c->n && p->weight_mode == FWBF_WEIGHTS_IMWBF &&
       p->block_len_p >= 16 && !P.force_ordered && !getenv("FWBF_NO_CDEC")) {
-#define FWBF_PICK_C(KC_, TB_, WT_, NN_)                                        \
-    if (kc == KC_ && T == TB_ && kwt == WT_ && c->n == NN_) {                  \
-      ckern = (const void *)fwbf::cdecode_kernel<KC_, TB_, WT_, NN_>;          \
-      clayout = layout_c<KC_, TB_, WT_, NN_>;                                  \
+#define FWBF_PICK_C(KC_, TB_, WT_, NN_, PB_)                                          \
+    if (kc == KC_ && T == TB_ && kwt == WT_ && c->n == NN_ && (PB_ == 0 || PB_ == p->block_len_p) && \
+        !(PB_ == 0 && ckern)) {                                                         \
+      ckern = (const void *)fwbf::cdecode_kernel<KC_, TB_, WT_, NN_, PB_>;              \
+      clayout = layout_c<KC_, TB_, WT_, NN_>;                                           \
     }
     FWBF_CIRC_CONFIGS(FWBF_PICK_C)
 #undef FWBF_PICK_C
@@ -1174,6 +1175,8 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     for (int j = 0; j < c->w; ++j) {
       const int d = c->n - c->off[j];
       Q.uoff[j] = ((d & 1) ? Q.off_fb + 4 : Q.off_fa) + 4 * d;
+      const int cj = c->off[j]; // check scan: keys of columns (m + c_j, m + 1 + c_j), m even
+      Q.soff[j] = (cj & 1) ? Q.off_fb + 4 * (cj + 1) : Q.off_fa + 4 * cj;
     }
     int cper = 0;
     if (Q.smem_bytes <= c->smem_optin) {
@@ -1205,6 +1208,18 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
       void *cargs[] = {&Q};
       CUDA_TRY(cudaLaunchKernel(ckern, dim3((unsigned)cgrid), dim3(T), cargs, Q.smem_bytes, stream));
       CUDA_TRY(cudaGetLastError());
+      if (phases) {
+        long long h[8];
+        CUDA_TRY(cudaMemcpyAsync(h, phase_buf, sizeof h, cudaMemcpyDeviceToHost, stream));
+        CUDA_TRY(cudaStreamSynchronize(stream));
+        long long tot = 0;
+        for (int i = 0; i < 5; ++i) tot += h[i];
+        static const char *names[5] = {"outputs+fetch", "init", "gather", "select", "toggles+refresh"};
+        fprintf(stderr, "[fwbf phases] cdecode grid=%lld T=%d smem=%d:", cgrid, T, Q.smem_bytes);
+        for (int i = 0; i < 5; ++i) fprintf(stderr, " %s %.1f%%", names[i], tot ? 100.0 * h[i] / tot : 0.0);
+        fprintf(stderr, "\n");
+        P.phase_cycles = nullptr;
+      }
       P.frame_list = dlist;
       P.frame_count = dcount;
       P.work_counter = lwork;

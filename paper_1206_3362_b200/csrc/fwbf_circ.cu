@@ -85,7 +85,61 @@ template <int KK, int KC, int TB, int NN> struct CRefresh<KK, KC, TB, NN, false>
                                              uint32_t, float) {}
 };
 
-template <int KC, int TB, int WT, int NN>
+// One FWBF block decision, warp-wide (decoders.py:156-167, :181-183): lanes
+// scan the block's columns (SHORT: one column per lane, p <= 32), REDUX gives
+// the maximum key and the first index holding it, and the filter band decides
+// whether the approximate argmax is the exact one; lane jj receives (v, i).
+template <int WT, bool SHORT>
+__device__ __forceinline__ void select_block(const KParams &P, uint32_t sE, const float *Efl, const float *sFA,
+                                             const uint16_t *sA2, const float *sM2, const float *yabs, const int *eqp,
+                                             int base, int lim, int lane, int jj, float fd2, float fdp, double &rv,
+                                             int &ri) {
+  float fv, fv2 = -INFINITY;
+  int fi;
+  if (SHORT) {
+    fi = base + lane;
+    float e; // (lanes past the block read inside the metric region; masked)
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e) : "r"(sE + 4u * (uint32_t)fi));
+    fv = lane < lim ? e : -INFINITY;
+  } else {
+    fv = -INFINITY;
+    fi = 0x7fffffff;
+    for (int o = lane; o < lim; o += 32) { // ascending per lane, strict >
+      const float e = Efl[base + o];
+      fv2 = fmaxf(fv2, fminf(fv, e));
+      if (e > fv) { fv = e; fi = base + o; }
+    }
+  }
+  const uint32_t ka = fkey(fv);
+  const uint32_t kmx = __reduce_max_sync(FULL_MASK, ka);
+  const int imin = (int)__reduce_min_sync(FULL_MASK, ka == kmx ? (uint32_t)fi : 0xffffffffu);
+  const float fmx = fkey_val(kmx);
+  const float thr = fmx - fd2;
+  // the block's runner-up: the winning lane's second value, every other
+  // lane's first.  Settled when it is more than 2 fdelta below the maximum
+  // (then the approximate argmax is the exact first maximum) and the maximum
+  // is farther than fdelta from 0 (then its sign is exact); otherwise the
+  // columns in the band are re-decided on exact sums.
+  const float r = fi == imin ? fv2 : fv;
+  if (__any_sync(FULL_MASK, r >= thr) || (fmx > -fdp && fmx <= fdp)) {
+    const int eq = *eqp;
+    const double qexp = pow2d(eq), qinv = pow2d(-eq);
+    double ve = -dinf();
+    int ie = 0x7fffffff;
+    for (int o = lane; o < lim; o += 32) {
+      const int n = base + o;
+      if (Efl[n] >= thr) amax_combine(ve, ie, exact_split_metric(P, sFA, sA2, sM2, yabs, n, WT, qexp, qinv), n);
+    }
+    warp_amax_redux(ve, ie);
+    if (lane == jj) { rv = ve; ri = ie; }
+    if (lane == 0 && P.filter_stats) atomicAdd((unsigned long long *)P.filter_stats, 1ull);
+  } else if (lane == jj) {
+    rv = (double)fmx;
+    ri = imin;
+  }
+}
+
+template <int KC, int TB, int WT, int NN, int PB>
 __global__ void __launch_bounds__(TB, TB == 256 ? FWBF_CMINB_256 : 1024 / TB)
 cdecode_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -130,6 +184,15 @@ cdecode_kernel(const __grid_constant__ KParams P) {
   // per-CTA counters (FWBF_CNT_* order), flushed once at the end
   __shared__ unsigned long long ctr[FWBF_CNT_EDGE_VISITS + 1];
   if (tid <= FWBF_CNT_EDGE_VISITS) ctr[tid] = 0ull;
+  // optional per-phase cycle accounting (FWBF_PHASES; thread 0, at barriers)
+  __shared__ long long ph_acc[8]; // [7] = last timestamp
+  if (tid < 8) ph_acc[tid] = 0;
+#define CPH(i)                                                  \
+  if (P.phase_cycles && tid == 0) {                             \
+    const long long t_ = clock64();                             \
+    if (ph_acc[7]) ph_acc[i] += t_ - ph_acc[7];                 \
+    ph_acc[7] = t_;                                             \
+  }
 
   __shared__ __align__(8) uint64_t ystage_bar;
   unsigned ystage_phase = 0;
@@ -147,6 +210,7 @@ cdecode_kernel(const __grid_constant__ KParams P) {
     __syncthreads();
     if (!ystage && tid == 0) misc[S_FRAME] = (int)atomicAdd(P.work_counter, 1u);
     __syncthreads();
+    CPH(0)
     const unsigned fu = (unsigned)misc[S_FRAME];
     if ((long long)fu >= P.batch) break;
     const int f = (int)fu; // batch <= 2^31 - 1
@@ -156,6 +220,14 @@ cdecode_kernel(const __grid_constant__ KParams P) {
     }
 
     // ---------------- init 1: y, hard decisions, guard statistics ----------------
+    // |y_n| goes to yabs and, as a sort key, twice into the doubled key array
+    // K0 (the min1 region, free until the records are written) and its
+    // one-element-shifted copy K1: key = bits(|y|) << 1 | (first copy), so
+    // among equal values a wrapped column (second copy: actual index
+    // u - N, smaller than any unwrapped one) sorts first -- the ascending
+    // column order of decoders.py:94-103 for every check.
+    uint32_t *K0 = reinterpret_cast<uint32_t *>(sFA);
+    uint32_t *K1 = reinterpret_cast<uint32_t *>(sFB);
     float lmin = INFINITY, lmax = 0.f;
     bool nonfin = false;
 #pragma unroll
@@ -164,7 +236,6 @@ cdecode_kernel(const __grid_constant__ KParams P) {
       const bool ok = n < N;
       float v = 0.f;
       if (ok) v = ystage ? ybuf[n] : __ldg(reinterpret_cast<const float *>(P.y) + (long long)f * P.ld + n);
-      if (ok) ybuf[n] = v + 0.f; // -0.0 -> +0.0: the sign bit is the hard decision (y < 0)
       const uint32_t b = __ballot_sync(FULL_MASK, ok && v < 0.f);
       if (lane == 0 && k * TB + warp * 32 < N) zbits[(k * TB + warp * 32) >> 5] = b;
       if (ok) {
@@ -173,6 +244,12 @@ cdecode_kernel(const __grid_constant__ KParams P) {
         if (a > 0.f) lmin = fminf(lmin, a);
         lmax = fmaxf(lmax, a);
         sCorr[n] = 0;
+        yabs[n] = a;
+        const uint32_t key = __float_as_uint(a) << 1;
+        K0[n] = key | 1u;
+        K0[n + N] = key;
+        K1[n + 1] = key | 1u;
+        K1[n + N + 1] = key;
       }
     }
     if (tid < 2 * L::FDW) fdb[tid] = 0u;
@@ -227,6 +304,14 @@ cdecode_kernel(const __grid_constant__ KParams P) {
       continue;
     }
 
+    if (ystage && tid == 0) { // ybuf is dead for this frame: claim the next one and start its copy
+      const unsigned t1 = atomicAdd(P.work_counter, 1u);
+      misc[S_FRAME] = (int)t1;
+      if ((long long)t1 < P.batch)
+        bulk_row_to_smem(ybuf, reinterpret_cast<const float *>(P.y) + (long long)t1 * P.ld, (unsigned)L::YSTB,
+                         &ystage_bar);
+    }
+
     // ---------------- init 2: check minima, syndrome, signed weights -------------
     const int eq = misc[S_EQ]; // quantum q = 2^eq
     const float ymaxf = __int_as_float(misc[S_YMAX]);
@@ -235,55 +320,100 @@ cdecode_kernel(const __grid_constant__ KParams P) {
     const int gsh = gbits > 24 ? gbits - 24 : 0;
     const float Gf = ldexpf(1.f, gsh + eq);
     const float invGf = ldexpf(1.f, -(gsh + eq));
+    const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
     {
+      // the doubled hard-decision bitmap zd (bit i = z_(i mod N)) into the
+      // second flip bitmap, for the syndrome windows below
+      uint32_t *zd = fdb + L::FDW;
+      if (warp == 0)
+        for (int wi = lane; wi < L::FDW; wi += 32) {
+          auto bits = [&](int st) -> uint32_t { // bits st.. of z, zero outside [0, N)
+            if (st <= -32 || st >= N) return 0u;
+            if (st < 0) return zbits[0] << (-st);
+            const int w0 = st >> 5, sh = st & 31;
+            const uint32_t lo = zbits[w0], hi = w0 + 1 < ZW ? zbits[w0 + 1] : 0u;
+            return __funnelshift_r(lo, hi, sh);
+          };
+          zd[wi] = bits(32 * wi) | bits(32 * wi - N);
+        }
+      // per check pair (m, m + 1), m = 2 tid + 2 TB qp: min1 / min2 keys and
+      // the argmin's unwrapped column, one 8-byte key load per offset
+      constexpr int NC = 2 * NP;
+      uint32_t k1[NC], k2[NC];
+      int ua[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) { k1[c] = 0xffffffffu; k2[c] = 0xffffffffu; ua[c] = 0; }
+      const uint32_t baseT = s0 + 8u * (uint32_t)tid;
+#pragma unroll
+      for (int j = 0; j < WT; ++j) {
+        const uint32_t so = (uint32_t)P.soff[j];
+        const int cj = P.off[j];
+#pragma unroll
+        for (int qp = 0; qp < NP; ++qp) {
+          uint32_t x, y2;
+          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(x), "=r"(y2) : "r"(baseT + so + (uint32_t)(qp * TB * 8)));
+          const int u = 2 * tid + 2 * TB * qp + cj;
+          {
+            const bool lt = x < k1[2 * qp];
+            k2[2 * qp] = min(k2[2 * qp], max(k1[2 * qp], x));
+            k1[2 * qp] = min(k1[2 * qp], x);
+            ua[2 * qp] = lt ? u : ua[2 * qp];
+          }
+          {
+            const bool lt = y2 < k1[2 * qp + 1];
+            k2[2 * qp + 1] = min(k2[2 * qp + 1], max(k1[2 * qp + 1], y2));
+            k1[2 * qp + 1] = min(k1[2 * qp + 1], y2);
+            ua[2 * qp + 1] = lt ? u : ua[2 * qp + 1]; // (column u + 1)
+          }
+        }
+      }
+      // min1 (float) parks in the metric region until the signs are known
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int m = 2 * tid + 2 * TB * (c >> 1) + (c & 1);
+        if (m < N) {
+          int col = ua[c] + (c & 1);
+          if (col >= N) col -= N;
+          Efl[m] = __uint_as_float(k1[c] >> 1);
+          sM2[m] = __uint_as_float(k2[c] >> 1);
+          sA2[m] = (uint16_t)col;
+        }
+      }
+    }
+    __syncthreads();
+    {
+      // syndrome word wd = XOR_j window(zd, 32 wd + c_j) (lane j: offset c_j);
+      // then check m = tid + kk TB = 32 wd + lane writes its signed min1 and
+      // its argmin column's coarse correction
+      const uint32_t *zw0 = fdb + L::FDW + warp + (c0 >> 5);
+      const uint32_t *zw1 = fdb + L::FDW + warp + (c1 >> 5);
       float wmax = 0.f;
       int swt = 0;
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
-        const int m = tid + kk * TB;
-        const bool ok = m < N;
-        float min1 = INFINITY, min2 = INFINITY;
-        int ac = 0x7fffffff;
-        uint32_t sgn = 0;
-        if (ok) {
-          // columns in ascending order, so strict < keeps the lowest column
-          // on ties (decoders.py:94-103); min2 = second smallest of the
-          // multiset; parity = XOR of the sign bits
-          const int *orr = rot + __ldg(P.jwtab + m);
-#pragma unroll 8
-          for (int t = 0; t < WT; ++t) {
-            const int c = m + orr[t];
-            const float yv = ybuf[c];
-            sgn ^= __float_as_uint(yv);
-            const float a = fabsf(yv);
-            const bool lt = a < min1;
-            min2 = fminf(min2, fmaxf(min1, a));
-            min1 = fminf(min1, a);
-            ac = lt ? c : ac;
+        const int wd = kk * NW + warp;
+        if ((kk + 1) * NW <= ZW || wd < ZW) {
+          uint32_t win = lane < WT ? __funnelshift_r(zw0[kk * NW], zw0[kk * NW + 1], c0 & 31) : 0u;
+          if (WT > 32) win ^= __funnelshift_r(zw1[kk * NW], zw1[kk * NW + 1], c1 & 31);
+          uint32_t sw = __reduce_xor_sync(FULL_MASK, win);
+          if (wd == ZW - 1) sw &= LASTW;
+          if (lane == 0) sbits[wd] = sw;
+          swt += __popc(sw);
+          const int m = wd * 32 + lane;
+          if (m < N) {
+            const bool par = (sw >> lane) & 1u;
+            const float min1 = Efl[m];
+            wmax = fmaxf(wmax, min1);
+            const float s1v = par ? min1 : -min1;
+            sFA[m] = s1v;
+            sFA[m + N] = s1v;
+            sFB[m + 1] = s1v;
+            sFB[m + N + 1] = s1v;
+            const int Dc = coarse_dc(sM2[m], min1, invGf);
+            atomicAdd(&sCorr[sA2[m]], par ? Dc : -Dc);
           }
         }
-        const bool par = ok && (sgn >> 31);
-        const uint32_t b = __ballot_sync(FULL_MASK, par);
-        if (lane == 0 && kk * TB + warp * 32 < N) {
-          sbits[(kk * TB + warp * 32) >> 5] = b;
-          swt += __popc(b);
-        }
-        if (ok) {
-          wmax = fmaxf(wmax, min1);
-          const float s1v = par ? min1 : -min1;
-          sFA[m] = s1v;
-          sFA[m + N] = s1v;
-          sFB[m + 1] = s1v;
-          sFB[m + N + 1] = s1v;
-          sA2[m] = (uint16_t)ac;
-          sM2[m] = min2;
-          const int Dc = coarse_dc(min2, min1, invGf);
-          atomicAdd(&sCorr[ac], par ? Dc : -Dc);
-        }
       }
-#pragma unroll
-      for (int k = 0; k < KC; ++k)
-        if (tid + k * TB < N) yabs[tid + k * TB] = fabsf(ybuf[tid + k * TB]);
 #pragma unroll
       for (int off = 16; off; off >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(FULL_MASK, wmax, off));
       if (lane == 0) {
@@ -292,13 +422,7 @@ cdecode_kernel(const __grid_constant__ KParams P) {
       }
     }
     __syncthreads();
-    if (ystage && tid == 0) { // ybuf is dead for this frame: claim the next one and start its copy
-      const unsigned t1 = atomicAdd(P.work_counter, 1u);
-      misc[S_FRAME] = (int)t1;
-      if ((long long)t1 < P.batch)
-        bulk_row_to_smem(ybuf, reinterpret_cast<const float *>(P.y) + (long long)t1 * P.ld, (unsigned)L::YSTB,
-                         &ystage_bar);
-    }
+    CPH(1)
     // filter bound (decode_kernel MODE 2): W sequential
     // fp32 adds of partial sums <= k vmax, the float finalize, the coarse
     // correction grid; fd2 = the band width 2 fdelta plus the rounding of
@@ -318,7 +442,6 @@ cdecode_kernel(const __grid_constant__ KParams P) {
     int k = 0, conv = 0, stalled = 0;
     int nflips = 0; // flips so far = this frame's flip-log position
     const float alf = (float)P.alpha;
-    const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
     for (;;) {
       if (misc[S_SWT0 + (k & 1)] == 0) { conv = 1; break; }
       if (k >= P.kmax) break;
@@ -349,6 +472,7 @@ cdecode_kernel(const __grid_constant__ KParams P) {
         }
       }
       __syncthreads(); // B1: metric complete
+      CPH(2)
       if (tid == 0) misc[S_SWT0 + ((k + 1) & 1)] = 0; // read at the top of iteration k - 1
 
       // ---- selection: warp per p-block (decoders.py:156-167, :181-183) ----
@@ -356,55 +480,31 @@ cdecode_kernel(const __grid_constant__ KParams P) {
       // the warp applies all its flips with one pass of its lanes
       uint32_t *fdc = fdb + (k & 1) * L::FDW;
       {
-        const int p = P.p;
         const uint32_t sE = s0 + L::E;
         double rv = 0.0;
         int ri = 0;
         int jj = 0;
-        for (int base = warp * p; base < N; base += NW * p, ++jj) {
-          const int lim = min(p, N - base);
-          float fv, fv2 = -INFINITY;
-          int fi;
-          if (lim <= 32) {
-            fi = base + lane;
-            float e; // (lanes past the block read inside the metric region; masked)
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e) : "r"(sE + 4u * (uint32_t)fi));
-            fv = lane < lim ? e : -INFINITY;
-          } else {
-            fv = -INFINITY;
-            fi = 0x7fffffff;
-            for (int o = lane; o < lim; o += 32) { // ascending per lane, strict >
-              const float e = Efl[base + o];
-              fv2 = fmaxf(fv2, fminf(fv, e));
-              if (e > fv) { fv = e; fi = base + o; }
-            }
+        if constexpr (PB > 0) { // block length compiled in: every block index and bound is an immediate
+          constexpr int NBK = (N + PB - 1) / PB;
+          constexpr int JM = (NBK + NW - 1) / NW;
+#pragma unroll
+          for (int j2 = 0; j2 < JM; ++j2) {
+            const int b = warp + j2 * NW;
+            if ((j2 + 1) * NW > NBK && b >= NBK) break; // warp-uniform
+            const int base = b * PB;
+            const int lim = (N % PB == 0) ? PB : min(PB, N - base);
+            select_block<WT, (PB <= 32)>(P, sE, Efl, sFA, sA2, sM2, yabs, misc + S_EQ, base, lim, lane, j2, fd2, fdp,
+                                         rv, ri);
+            jj = j2 + 1;
           }
-          const uint32_t ka = fkey(fv);
-          const uint32_t kmx = __reduce_max_sync(FULL_MASK, ka);
-          const int imin = (int)__reduce_min_sync(FULL_MASK, ka == kmx ? (uint32_t)fi : 0xffffffffu);
-          const float fmx = fkey_val(kmx);
-          const float thr = fmx - fd2;
-          // the block's runner-up: the winning lane's second value, every
-          // other lane's first.  Settled when it is more than 2 fdelta below
-          // the maximum (then the approximate argmax is the exact first
-          // maximum) and the maximum is farther than fdelta from 0 (then its
-          // sign is exact); otherwise the columns in the band are re-decided
-          // on exact sums.
-          const float r = fi == imin ? fv2 : fv;
-          if (__any_sync(FULL_MASK, r >= thr) || (fmx > -fdp && fmx <= fdp)) {
-            const double qexp = pow2d(misc[S_EQ]), qinv = pow2d(-misc[S_EQ]);
-            double ve = -dinf();
-            int ie = 0x7fffffff;
-            for (int o = lane; o < lim; o += 32) {
-              const int n = base + o;
-              if (Efl[n] >= thr) amax_combine(ve, ie, exact_split_metric(P, sFA, sA2, sM2, yabs, n, WT, qexp, qinv), n);
-            }
-            warp_amax_redux(ve, ie);
-            if (lane == jj) { rv = ve; ri = ie; }
-            if (lane == 0 && P.filter_stats) atomicAdd((unsigned long long *)P.filter_stats, 1ull);
-          } else if (lane == jj) {
-            rv = (double)fmx;
-            ri = imin;
+        } else {
+          const int p = P.p;
+          for (int base = warp * p; base < N; base += NW * p, ++jj) {
+            const int lim = min(p, N - base);
+            if (lim <= 32)
+              select_block<WT, true>(P, sE, Efl, sFA, sA2, sM2, yabs, misc + S_EQ, base, lim, lane, jj, fd2, fdp, rv, ri);
+            else
+              select_block<WT, false>(P, sE, Efl, sFA, sA2, sM2, yabs, misc + S_EQ, base, lim, lane, jj, fd2, fdp, rv, ri);
           }
         }
         const bool mine = lane < jj;
@@ -423,6 +523,7 @@ cdecode_kernel(const __grid_constant__ KParams P) {
         if (lane == 0 && fm) atomicAdd(&misc[S_F0 + (k & 1)], __popc(fm));
       }
       __syncthreads(); // B2: flips chosen
+      CPH(3)
       int F = misc[S_F0 + (k & 1)];
       if (F == 0) {
         // nothing selected while the syndrome is nonzero (decoders.py:214-222)
@@ -518,6 +619,7 @@ cdecode_kernel(const __grid_constant__ KParams P) {
       nflips += F;
       k += 1;
       __syncthreads(); // B3: records, corrections, syndrome weight
+      CPH(4)
     }
 
     // ---------------- outputs -----------------------------------------------------
@@ -550,11 +652,13 @@ cdecode_kernel(const __grid_constant__ KParams P) {
     }
   }
 
+  if (P.phase_cycles && tid < 7) atomicAdd((unsigned long long *)&P.phase_cycles[tid], (unsigned long long)ph_acc[tid]);
+#undef CPH
   if (P.counters && tid <= FWBF_CNT_EDGE_VISITS && tid != FWBF_CNT_ORDERED_FRAMES && ctr[FWBF_CNT_FRAMES])
     atomicAdd((unsigned long long *)P.counters + tid, ctr[tid]);
 }
 
-#define FWBF_INST_CIRC(KC, TB, WT, NN) template __global__ void cdecode_kernel<KC, TB, WT, NN>(const __grid_constant__ KParams);
+#define FWBF_INST_CIRC(KC, TB, WT, NN, PB) template __global__ void cdecode_kernel<KC, TB, WT, NN, PB>(const __grid_constant__ KParams);
 FWBF_CIRC_CONFIGS(FWBF_INST_CIRC)
 
 } // namespace fwbf

@@ -34,10 +34,12 @@ constexpr int kMaxQcBlocks = 256;  // quasi-cyclic shift table entries in the pa
 
 // Filtered FWBF kernel for cyclic EG codes (fwbf_circ.cu): (KC, TB, WT, N),
 // the code length and weight compiled in (EG(255), EG(1023), EG(4095)).
+// PB > 0: the FWBF block length compiled in as well (0: any p >= 16).
 #define FWBF_CIRC_CONFIGS(X) \
-  X(2, 128, 16, 255)         \
-  X(4, 256, 32, 1023)        \
-  X(4, 1024, 64, 4095)
+  X(2, 128, 16, 255, 0)      \
+  X(4, 256, 32, 1023, 0)     \
+  X(4, 256, 32, 1023, 31)    \
+  X(4, 1024, 64, 4095, 0)
 
 // Its shared-memory layout (byte offsets), a compile-time function of the code
 // so every access in the kernel is [base + immediate]; the host reads the same
@@ -142,6 +144,7 @@ struct KParams {
   unsigned *defer_count;
   const int *frame_list;
   const unsigned *frame_count;
+  int soff[kMaxCircWeight]; // fwbf_circ.cu check scan: byte offset of the key pair of column m + c_j (m even), minus 4m
   int off_fd;  // fwbf_circ.cu: two doubled flip bitmaps (iteration parity)
   int fd_words; // words per flip bitmap
 };
