@@ -178,8 +178,8 @@ cdecode_kernel(const __grid_constant__ KParams P) {
   }
   if (tid == 0) misc[S_NONFIN] = 0;
   // this lane's offsets for the toggle windows: j = lane (and lane + 32)
-  const int c0 = lane < WT ? P.off[lane] : 0;
-  const int c1 = (WT > 32 && lane + 32 < WT) ? P.off[lane + 32] : 0;
+  // (read from the shared rot table where used: a per-lane index into the
+  // parameter bank would serialise over the lanes)
 
   // per-CTA counters (FWBF_CNT_* order), flushed once at the end
   __shared__ unsigned long long ctr[FWBF_CNT_EDGE_VISITS + 1];
@@ -385,6 +385,8 @@ cdecode_kernel(const __grid_constant__ KParams P) {
       // syndrome word wd = XOR_j window(zd, 32 wd + c_j) (lane j: offset c_j);
       // then check m = tid + kk TB = 32 wd + lane writes its signed min1 and
       // its argmin column's coarse correction
+      const int c0 = lane < WT ? rot[WT + lane] : 0;
+      const int c1 = (WT > 32 && lane + 32 < WT) ? rot[WT + lane + 32] : 0;
       const uint32_t *zw0 = fdb + L::FDW + warp + (c0 >> 5);
       const uint32_t *zw1 = fdb + L::FDW + warp + (c1 >> 5);
       float wmax = 0.f;
@@ -487,15 +489,51 @@ cdecode_kernel(const __grid_constant__ KParams P) {
         if constexpr (PB > 0) { // block length compiled in: every block index and bound is an immediate
           constexpr int NBK = (N + PB - 1) / PB;
           constexpr int JM = (NBK + NW - 1) / NW;
+          if constexpr (PB <= 32) {
+            // all of this warp's blocks as independent straight-line chains
+            // (load, key, two REDUX, band test) the scheduler can overlap;
+            // blocks the band leaves open are re-decided afterwards
+            float rvf = 0.f;
+            uint32_t ambm = 0u;
 #pragma unroll
-          for (int j2 = 0; j2 < JM; ++j2) {
-            const int b = warp + j2 * NW;
-            if ((j2 + 1) * NW > NBK && b >= NBK) break; // warp-uniform
-            const int base = b * PB;
-            const int lim = (N % PB == 0) ? PB : min(PB, N - base);
-            select_block<WT, (PB <= 32)>(P, sE, Efl, sFA, sA2, sM2, yabs, misc + S_EQ, base, lim, lane, j2, fd2, fdp,
-                                         rv, ri);
-            jj = j2 + 1;
+            for (int j2 = 0; j2 < JM; ++j2) {
+              const int b = warp + j2 * NW;
+              if ((j2 + 1) * NW > NBK && b >= NBK) break; // warp-uniform
+              const int base = b * PB;
+              const int lim = (N % PB == 0) ? PB : min(PB, N - base);
+              const int fi = base + lane;
+              const float e = Efl[fi]; // (lanes past the block read inside the metric region; masked)
+              const float fv = lane < lim ? e : -INFINITY;
+              const uint32_t ka = fkey(fv);
+              const uint32_t kmx = __reduce_max_sync(FULL_MASK, ka);
+              const int imin = (int)__reduce_min_sync(FULL_MASK, ka == kmx ? (uint32_t)fi : 0xffffffffu);
+              const float fmx = fkey_val(kmx);
+              // runner-up = every other lane's value (one column per lane)
+              const bool amb = __any_sync(FULL_MASK, fi != imin && fv >= fmx - fd2) || (fmx > -fdp && fmx <= fdp);
+              ambm |= (amb ? 1u : 0u) << j2;
+              if (lane == j2) { rvf = fmx; ri = imin; }
+              jj = j2 + 1;
+            }
+            rv = (double)rvf;
+            while (ambm) { // rare: exact decisions
+              const int j2 = __ffs(ambm) - 1;
+              ambm &= ambm - 1u;
+              const int base = (warp + j2 * NW) * PB;
+              const int lim = (N % PB == 0) ? PB : min(PB, N - base);
+              select_block<WT, true>(P, sE, Efl, sFA, sA2, sM2, yabs, misc + S_EQ, base, lim, lane, j2, fd2, fdp, rv,
+                                     ri);
+            }
+          } else {
+#pragma unroll
+            for (int j2 = 0; j2 < JM; ++j2) {
+              const int b = warp + j2 * NW;
+              if ((j2 + 1) * NW > NBK && b >= NBK) break; // warp-uniform
+              const int base = b * PB;
+              const int lim = (N % PB == 0) ? PB : min(PB, N - base);
+              select_block<WT, false>(P, sE, Efl, sFA, sA2, sM2, yabs, misc + S_EQ, base, lim, lane, j2, fd2, fdp,
+                                      rv, ri);
+              jj = j2 + 1;
+            }
           }
         } else {
           const int p = P.p;
@@ -585,6 +623,8 @@ cdecode_kernel(const __grid_constant__ KParams P) {
         // bit b of word wd: check m = 32 wd + b toggles iff an odd number of
         // its columns m + c_j flipped = XOR over j of the doubled flip
         // bitmap's window starting at bit 32 wd + c_j (lane j: offset c_j)
+        const int c0 = lane < WT ? rot[WT + lane] : 0;
+        const int c1 = (WT > 32 && lane + 32 < WT) ? rot[WT + lane + 32] : 0;
         const uint32_t *fw0 = fdc + warp + (c0 >> 5);
         const uint32_t *fw1 = fdc + warp + (c1 >> 5);
         uint32_t tg[KC];
@@ -613,8 +653,30 @@ cdecode_kernel(const __grid_constant__ KParams P) {
         pcnt = __reduce_add_sync(FULL_MASK, pcnt);
         if (lane == 0 && pcnt) atomicAdd(&misc[S_SWT0 + ((k + 1) & 1)], pcnt);
         // toggled checks m = tid + kk TB
-        CRefresh<0, KC, TB, NN>::run(tg, lane, s0 + L::FA + 4u * tid, s0 + L::FB + 4u * (tid + 1),
-                                     s0 + L::M2 + 4u * tid, s0 + L::A2 + 2u * tid, s0 + L::CORR, invGf);
+        // (plain shared loads for every round first, so the rounds overlap;
+        // the stores and the correction atomic only where the check toggled)
+        float rv1[KC], rm2[KC];
+        int ra2[KC];
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+          const int m = tid + kk * TB;
+          rv1[kk] = sFA[m];
+          rm2[kk] = sM2[m];
+          ra2[kk] = sA2[m];
+        }
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+          if ((tg[kk] >> lane) & 1u) {
+            const int m = tid + kk * TB;
+            const float v = -rv1[kk];
+            sFA[m] = v;
+            sFA[m + N] = v;
+            sFB[m + 1] = v;
+            sFB[m + N + 1] = v;
+            const int dc = coarse_dc(rm2[kk], fabsf(v), invGf);
+            atomicAdd(&sCorr[ra2[kk]], signbit(v) ? -2 * dc : 2 * dc);
+          }
+        }
       }
       nflips += F;
       k += 1;
