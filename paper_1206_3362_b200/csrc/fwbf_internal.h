@@ -39,7 +39,11 @@ constexpr int kMaxQcBlocks = 256;  // quasi-cyclic shift table entries in the pa
   X(2, 128, 16, 255, 0)      \
   X(4, 256, 32, 1023, 0)     \
   X(4, 256, 32, 1023, 31)    \
-  X(4, 1024, 64, 4095, 0)
+  X(4, 1024, 64, 4095, 0)    \
+  X(4, 1024, 64, 4095, 64)   \
+  X(4, 1024, 64, 4095, 128)  \
+  X(4, 1024, 64, 4095, 256)  \
+  X(4, 256, 32, 1023, 93)
 
 // Its shared-memory layout (byte offsets), a compile-time function of the code
 // so every access in the kernel is [base + immediate]; the host reads the same
