@@ -157,6 +157,11 @@ int fwbf_metric_f64(fwbf_code *code, const fwbf_params *params, const double *y,
  * global argmaxes.  Synchronous; reset != 0 zeroes the counters. */
 int fwbf_filter_stats(fwbf_code *code, int64_t *out, int32_t reset);
 
+/* Diagnostic: the decode kernel(s) the calling thread's last decode launched,
+ * e.g. "cdecode+decode_kernel" (filtered circulant kernel, then the exact
+ * kernel over the frames it deferred), "decode_kernel", "xdecode", "qdecode". */
+const char *fwbf_last_kernel(void);
+
 /* Noise modes for fwbf_decode_awgn. */
 #define FWBF_NOISE_NUMPY_F64 0 /* the reference stream: numpy Philox(key=seed,
                                   counter=frame<<128) + Generator.standard_normal,

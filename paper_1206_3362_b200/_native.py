@@ -29,7 +29,7 @@ EXPORTS = ("fwbf_abi_version", "fwbf_last_error", "fwbf_device_count", "fwbf_cod
            "fwbf_decode_f64", "fwbf_decode_awgn", "fwbf_decode_host_f32", "fwbf_metric_f32",
            "fwbf_metric_f64", "fwbf_filter_stats", "fwbf_stage_hard_decision", "fwbf_stage_syndrome",
            "fwbf_stage_weights", "fwbf_stage_edge_weights", "fwbf_stage_all_metrics", "fwbf_stage_block_argmax",
-           "fwbf_stage_bit_metric", "fwbf_channel_awgn")
+           "fwbf_stage_bit_metric", "fwbf_channel_awgn", "fwbf_last_kernel")
 
 
 class CodeDesc(C.Structure):
@@ -77,6 +77,7 @@ def lib() -> C.CDLL:
             vp = C.c_void_p
             L.fwbf_abi_version.restype = C.c_int
             L.fwbf_last_error.restype = C.c_char_p
+            L.fwbf_last_kernel.restype = C.c_char_p
             L.fwbf_device_count.restype = C.c_int
             L.fwbf_code_create.argtypes = [C.POINTER(CodeDesc), C.c_int, C.POINTER(vp)]
             L.fwbf_code_destroy.argtypes = [vp]
@@ -105,12 +106,17 @@ def lib() -> C.CDLL:
             L.fwbf_channel_awgn.argtypes = [vp, C.c_uint64, i64, i64, dbl, vp, i32, vp, i64, vp]
             for f in EXPORTS:
                 if f not in ("fwbf_abi_version", "fwbf_last_error", "fwbf_device_count",
-                             "fwbf_max_flips_per_iter"):
+                             "fwbf_max_flips_per_iter", "fwbf_last_kernel"):
                     getattr(L, f).restype = C.c_int
             if L.fwbf_abi_version() != 1:
                 raise ImportError("libfwbf_b200.so ABI version mismatch")
             _lib = L
     return _lib
+
+
+def last_kernel() -> str:
+    """Kernel(s) this thread's last decode launched (diagnostic, fwbf_last_kernel)."""
+    return lib().fwbf_last_kernel().decode()
 
 
 def check(rc: int, what: str = "") -> None:

@@ -138,6 +138,9 @@ static constexpr int kWorkRing = 1024;
 extern "C" int fwbf_abi_version(void) { return FWBF_ABI_VERSION; }
 extern "C" const char *fwbf_last_error(void) { return g_err.c_str(); }
 
+static thread_local const char *g_last_kernel = "";
+extern "C" const char *fwbf_last_kernel(void) { return g_last_kernel; }
+
 extern "C" int fwbf_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) { cudaGetLastError(); return 0; }
@@ -885,12 +888,16 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
       !getenv("FWBF_NO_QC") && !getenv("FWBF_NO_QCK")) {
     bool used = false;
     rc = launch_qc(c, p, (const float *)y, batch, ld, o, stream, &used);
+    if (used) g_last_kernel = "qdecode";
     if (rc || used) return rc;
   }
   if (!c->circ && sizeof(YT) == 4 && p->algorithm == FWBF_ALG_FWBF && !metric_out && !getenv("FWBF_NO_WARP")) {
     const XPlan *xp = get_xplan(c, p->block_len_p, &rc);
     if (rc) return rc;
-    if (xp) return launch_explicit(c, p, *xp, (const float *)y, batch, ld, o, stream);
+    if (xp) {
+      g_last_kernel = "xdecode";
+      return launch_explicit(c, p, *xp, (const float *)y, batch, ld, o, stream);
+    }
   }
   KParams P;
   memset(&P, 0, sizeof P);
@@ -1227,12 +1234,14 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
       CUDA_TRY(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(T), args, P.smem_bytes, stream));
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaFreeAsync(dlist, stream));
+      g_last_kernel = "cdecode+decode_kernel";
       return FWBF_OK;
     }
   }
   void *args[] = {&P};
   CUDA_TRY(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(T), args, P.smem_bytes, stream));
   CUDA_TRY(cudaGetLastError());
+  g_last_kernel = "decode_kernel";
   if (phases) {
     long long h[8];
     CUDA_TRY(cudaMemcpyAsync(h, phase_buf, sizeof h, cudaMemcpyDeviceToHost, stream));

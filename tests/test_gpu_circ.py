@@ -1,0 +1,144 @@
+"""The filtered FWBF kernel for cyclic EG codes (csrc/fwbf_circ.cu, round 3).
+
+It decodes every frame its guard admits (finite y, some |y| > 0, the fp64
+guard of DESIGN.md section 2) and defers the rest to decode_kernel through a
+frame list.  Its results must equal decode_kernel's MODE 2 (FWBF_NO_CDEC=1)
+and the oracle bit for bit: hard decisions, iterations, flags, flip counts
+and the flip sequence, for compiled-in and runtime block lengths, both stall
+policies, and batches that mix deferred frames in.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import wbf_oracle as O
+from oracle.c_oracle import COracle
+from paper_1206_3362_b200 import DecoderConfig, decode_batch
+from paper_1206_3362_b200 import _native as nat
+from tests.golden.codebook import build_code, code_rate
+
+pytestmark = pytest.mark.gpu
+
+
+def _frames(code, ebn0, frames, seed, quant=None):
+    h = build_code(code)
+    sigma = O.ebn0_to_sigma(ebn0, code_rate(code))
+    rng = np.random.default_rng(seed)
+    y = 1.0 + sigma * rng.standard_normal((frames, h.n_cols))
+    if quant:
+        y = np.round(y * quant) / quant
+    return h, y.astype(np.float32)
+
+
+def _decode(h, y, cfg, cdec=True):
+    """decode_batch with or without the circulant kernel (FWBF_NO_CDEC is read per launch)."""
+    if cdec:
+        os.environ.pop("FWBF_NO_CDEC", None)
+    else:
+        os.environ["FWBF_NO_CDEC"] = "1"
+    try:
+        r = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+        kern = nat.last_kernel()
+    finally:
+        os.environ.pop("FWBF_NO_CDEC", None)
+    return r, kern
+
+
+def _same(a, b, tag):
+    for name in ("iterations", "flips_total", "flags"):
+        u, v = getattr(a, name).cpu().numpy(), getattr(b, name).cpu().numpy()
+        assert np.array_equal(u, v), f"{tag}: {name} differs at {np.nonzero(u != v)[0][:8]}"
+    assert np.array_equal(a.z_bits.cpu().numpy(), b.z_bits.cpu().numpy()), f"{tag}: z differs"
+    assert a.flip_logs() == b.flip_logs(), f"{tag}: flip logs differ"
+
+
+def _vs_oracle(res, h, y, cfg, tag, rows=None):
+    rows = np.arange(y.shape[0]) if rows is None else rows
+    z, its, fl, ft = COracle(h).decode_batch(y[rows], algorithm="fwbf", alpha=cfg.alpha, k_max=cfg.k_max,
+                                             lam=cfg.lam, p=cfg.block_len_p, weight_mode=cfg.weight_mode,
+                                             stall=cfg.stall_policy, mlp_threshold=cfg.mlp_threshold)
+    bad = np.nonzero((res.iterations.cpu().numpy()[rows] != its) | ((res.flags.cpu().numpy()[rows] & 3) != fl) |
+                     (res.flips_total.cpu().numpy()[rows] != ft) | np.any(res.z()[rows] != z, axis=1))[0]
+    assert bad.size == 0, f"{tag}: {bad.size} frames differ from the oracle, first {rows[bad[:8]]}"
+
+
+@pytest.mark.parametrize("code,p,ebn0,frames", [
+    ("eg5", 31, 4.0, 2048),     # the headline shape (block length compiled in)
+    ("eg5", 31, 3.0, 512),
+    ("eg5", 93, 4.0, 1024),     # compiled in, p > 32
+    ("eg5", 16, 4.0, 512),      # runtime p, the smallest the kernel takes
+    ("eg5", 32, 4.5, 512),
+    ("eg5", 100, 3.5, 512),     # runtime p > 32, ragged last block
+    ("eg5", 1023, 4.0, 256),    # one block
+    ("eg4", 17, 3.5, 1024),     # EG(255), W = 16
+    ("eg4", 51, 4.0, 1024),
+    ("eg6", 64, 4.0, 128),      # EG(4095), W = 64, compiled in
+    ("eg6", 256, 3.5, 96),
+    ("eg6", 100, 4.5, 96),      # EG(4095), runtime p
+])
+def test_circ_kernel_equals_mode2_and_oracle(cuda_device, code, p, ebn0, frames):
+    h, y = _frames(code, ebn0, frames, seed=p * 131 + frames)
+    cfg = DecoderConfig(block_len_p=p, k_max=60, alpha=0.2)
+    a, ka = _decode(h, y, cfg, True)
+    b, kb = _decode(h, y, cfg, False)
+    assert ka == "cdecode+decode_kernel" and kb == "decode_kernel", (ka, kb)
+    _same(a, b, f"{code}/p{p}/{ebn0}dB")
+    _vs_oracle(a, h, y, cfg, f"{code}/p{p}/{ebn0}dB", rows=np.arange(min(frames, 256)))
+
+
+@pytest.mark.parametrize("stall,alpha,quant", [
+    ("flip-global-max", 1.5, 16),   # maxima near / below 0: stalls and exact fallbacks
+    ("terminate", 1.5, 8),
+    ("flip-global-max", 0.2, 4),    # coarse quantisation: many exact ties
+])
+def test_circ_kernel_stalls_and_ties(cuda_device, stall, alpha, quant):
+    h, y = _frames("eg5", 3.5, 256, seed=7 + quant, quant=quant)
+    cfg = DecoderConfig(block_len_p=31, k_max=40, alpha=alpha, stall_policy=stall)
+    a, ka = _decode(h, y, cfg, True)
+    b, _ = _decode(h, y, cfg, False)
+    assert ka == "cdecode+decode_kernel"
+    _same(a, b, f"{stall}/a{alpha}/q{quant}")
+    _vs_oracle(a, h, y, cfg, f"{stall}/a{alpha}/q{quant}")
+
+
+def test_circ_kernel_defers_unguarded_frames(cuda_device):
+    """Frames the filtered guard rejects go to decode_kernel through the defer
+    list, interleaved with ordinary frames; every frame's result is the one
+    decode_kernel alone produces (and the oracle's for the finite ones)."""
+    h, y = _frames("eg5", 4.0, 640, seed=99)
+    special = {}
+    special[3] = np.zeros(h.n_cols, np.float32)                    # all |y| == 0
+    v = y[10].copy(); v[5] = np.inf; special[10] = v                 # non-finite
+    v = y[11].copy(); v[700] = np.nan; special[11] = v
+    v = y[200].copy(); v[17] = 3e37; v[18] = 1e-38; special[200] = v  # beyond the fp64 guard
+    v = y[201].copy(); v[::7] = -0.0; special[201] = v               # signed zeros (guard passes)
+    v = y[333].copy(); v[::3] = 1e-30; special[333] = v              # huge range
+    for i, v in special.items():
+        y[i] = v
+    cfg = DecoderConfig(block_len_p=31, k_max=50, alpha=0.2)
+    a, ka = _decode(h, y, cfg, True)
+    b, _ = _decode(h, y, cfg, False)
+    assert ka == "cdecode+decode_kernel"
+    _same(a, b, "mixed batch")
+    finite = np.array([i for i in range(y.shape[0]) if np.all(np.isfinite(y[i]))])
+    _vs_oracle(a, h, y, cfg, "mixed batch", rows=finite[finite < 400])
+
+
+def test_circ_kernel_staged_rows(cuda_device):
+    """TMA-staged input rows (16-byte row stride, forced for a small batch)
+    give the same results as element loads."""
+    import torch
+    h, y = _frames("eg5", 4.0, 300, seed=5)
+    cfg = DecoderConfig(block_len_p=31, k_max=60)
+    ypad = torch.zeros((y.shape[0], 1024), dtype=torch.float32, device="cuda:0")
+    ypad[:, :h.n_cols] = torch.from_numpy(y).cuda()
+    os.environ["FWBF_FORCE_YSTAGE"] = "1"
+    try:
+        a = decode_batch(h, ypad[:, :h.n_cols], cfg, "fwbf", flip_log=True)
+        assert nat.last_kernel() == "cdecode+decode_kernel"
+    finally:
+        os.environ.pop("FWBF_FORCE_YSTAGE", None)
+    b, _ = _decode(h, y, cfg, False)
+    _same(a, b, "staged rows")
