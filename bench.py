@@ -335,6 +335,7 @@ def main():
 
     for _ in range(a.warmup):
         step()
+    launch_kernels = nat.last_kernel()
     torch.cuda.synchronize()
     dc.filter_stats(reset=True)
     if world > 1:
@@ -392,7 +393,7 @@ def main():
         e2e = {"value": world * B * a.steps * kinfo / te / 1e9, "unit": "Gbit/s",
                "h2d_bytes_per_step": B * ld * 4,
                "d2h_bytes_per_step": B * (zw * 4 + 4 + 1) + nat.NCOUNTERS * 8,
-               "path": "fwbf_decode_host_f32 (pinned host y; chunked H2D/decode/D2H on 2 streams)",
+               "path": "fwbf_decode_host_f32 (pinned host y; chunked H2D / decode / D2H on 3 streams ordered by events)",
                "chunk_frames": a.e2e_chunk}
 
     if rank == 0:
@@ -472,7 +473,10 @@ def main():
                                  "traffic": traffic,
                                  "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}},
             "e2e": e2e,
-            "gpu_launches": a.steps * 1,
+            # per step: the filtered circulant kernel + decode_kernel over the
+            # frames it deferred (2 launches when the circulant kernel applies)
+            "gpu_launches": a.steps * (2 if launch_kernels.startswith("cdecode+") else 1),
+            "decode_kernels": launch_kernels,
             "clocks": csum,
         }
         if not a.no_cpu_baseline and world == 1:

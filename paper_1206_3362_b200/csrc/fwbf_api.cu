@@ -117,7 +117,8 @@ struct fwbf_code {
   int smem_optin = 0;
   // host pipeline scratch
   std::mutex pipe_mu;
-  cudaStream_t pipe_s[2] = {nullptr, nullptr};
+  cudaStream_t pipe_s[3] = {nullptr, nullptr, nullptr}; // H2D copies, decodes, D2H copies
+  cudaEvent_t pipe_ev[3][2] = {};                         // [h2d done, decode done, d2h done][buffer]
   void *pipe_buf[2] = {nullptr, nullptr};
   size_t pipe_bytes = 0;
   int64_t *pipe_counters = nullptr;
@@ -321,10 +322,13 @@ extern "C" int fwbf_code_destroy(fwbf_code *c) {
   cudaFree(c->d_offpos);
   cudaFree(c->d_work);
   cudaFree(c->d_fstats);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 3; ++i) {
     if (c->pipe_s[i]) cudaStreamDestroy(c->pipe_s[i]);
-    if (c->pipe_buf[i]) cudaFree(c->pipe_buf[i]);
+    for (int b = 0; b < 2; ++b)
+      if (c->pipe_ev[i][b]) cudaEventDestroy(c->pipe_ev[i][b]);
   }
+  for (int i = 0; i < 2; ++i)
+    if (c->pipe_buf[i]) cudaFree(c->pipe_buf[i]);
   cudaFree(c->pipe_counters);
   cudaFree(c->noise_buf);
   if (c->noise_evt) cudaEventDestroy(c->noise_evt);
@@ -1425,32 +1429,47 @@ extern "C" int fwbf_decode_host_f32(fwbf_code *c, const fwbf_params *p, const fl
     for (int i = 0; i < 2; ++i) CUDA_TRY(cudaMalloc(&c->pipe_buf[i], need));
     c->pipe_bytes = need;
   }
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 3; ++i) {
     if (!c->pipe_s[i]) CUDA_TRY(cudaStreamCreateWithFlags(&c->pipe_s[i], cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b)
+      if (!c->pipe_ev[i][b]) CUDA_TRY(cudaEventCreateWithFlags(&c->pipe_ev[i][b], cudaEventDisableTiming));
+  }
   if (!c->pipe_counters) CUDA_TRY(cudaMalloc((void **)&c->pipe_counters, FWBF_NCOUNTERS * sizeof(int64_t)));
-  CUDA_TRY(cudaMemsetAsync(c->pipe_counters, 0, FWBF_NCOUNTERS * sizeof(long long), c->pipe_s[0]));
-  CUDA_TRY(cudaStreamSynchronize(c->pipe_s[0]));
+  CUDA_TRY(cudaMemsetAsync(c->pipe_counters, 0, FWBF_NCOUNTERS * sizeof(long long), c->pipe_s[1]));
+  CUDA_TRY(cudaStreamSynchronize(c->pipe_s[1]));
+  // Three streams: H2D copies, decodes, D2H copies, ordered by events per
+  // buffer.  Decodes run one after another on their own stream, so a chunk's
+  // launches (the filtered kernel, then decode_kernel over its deferred
+  // frames) never queue behind the next chunk's persistent grid, while both
+  // copy directions overlap them.
+  cudaStream_t sin = c->pipe_s[0], sdec = c->pipe_s[1], sout = c->pipe_s[2];
   // chunk sizes ramp up geometrically (chunk/16, chunk/8, ... chunk) so the
   // first decode starts after a short copy instead of a full chunk's
   long long f0 = 0, cur = std::max<long long>(std::min<long long>(chunk, 4096), chunk / 16);
   for (long long ci = 0; f0 < batch; ++ci) {
     const int s = (int)(ci & 1);
-    cudaStream_t st = c->pipe_s[s];
+    cudaStream_t st = sout;
     char *base = (char *)c->pipe_buf[s];
     float *dy = (float *)base;
     uint32_t *dz = (uint32_t *)(base + yb);
     int32_t *dit = (int32_t *)(base + yb + zb);
     uint8_t *dfl = (uint8_t *)(base + yb + zb + ib);
     const long long nb = std::min<long long>(cur, batch - f0);
-    CUDA_TRY(cudaMemcpyAsync(dy, y_host + f0 * ld, (size_t)nb * ld * sizeof(float), cudaMemcpyHostToDevice, st));
+    if (ci >= 2) CUDA_TRY(cudaStreamWaitEvent(sin, c->pipe_ev[1][s], 0)); // chunk ci-2 decoded: y buffer free
+    CUDA_TRY(cudaMemcpyAsync(dy, y_host + f0 * ld, (size_t)nb * ld * sizeof(float), cudaMemcpyHostToDevice, sin));
+    CUDA_TRY(cudaEventRecord(c->pipe_ev[0][s], sin));
+    CUDA_TRY(cudaStreamWaitEvent(sdec, c->pipe_ev[0][s], 0));
+    if (ci >= 2) CUDA_TRY(cudaStreamWaitEvent(sdec, c->pipe_ev[2][s], 0)); // chunk ci-2's outputs copied out
     fwbf_outputs o{};
     o.z_bits = z_host ? dz : nullptr;
     o.z_ld = zw;
     o.iterations = it_host ? dit : nullptr;
     o.flags = fl_host ? dfl : nullptr;
     o.counters = c->pipe_counters;
-    rc = launch_decode<float>(c, p, dy, nb, ld, &o, st);
+    rc = launch_decode<float>(c, p, dy, nb, ld, &o, sdec);
     if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(c->pipe_ev[1][s], sdec));
+    CUDA_TRY(cudaStreamWaitEvent(sout, c->pipe_ev[1][s], 0));
     if (z_host) {
       if (z_ld == zw) {
         CUDA_TRY(cudaMemcpyAsync(z_host + f0 * z_ld, dz, (size_t)nb * zw * 4, cudaMemcpyDeviceToHost, st));
@@ -1461,11 +1480,11 @@ extern "C" int fwbf_decode_host_f32(fwbf_code *c, const fwbf_params *p, const fl
     }
     if (it_host) CUDA_TRY(cudaMemcpyAsync(it_host + f0, dit, (size_t)nb * 4, cudaMemcpyDeviceToHost, st));
     if (fl_host) CUDA_TRY(cudaMemcpyAsync(fl_host + f0, dfl, (size_t)nb, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(c->pipe_ev[2][s], sout));
     f0 += nb;
     cur = std::min<long long>(chunk, 2 * cur);
   }
-  CUDA_TRY(cudaStreamSynchronize(c->pipe_s[0]));
-  CUDA_TRY(cudaStreamSynchronize(c->pipe_s[1]));
+  for (int i = 0; i < 3; ++i) CUDA_TRY(cudaStreamSynchronize(c->pipe_s[i]));
   if (cnt_host) {
     long long tmp[FWBF_NCOUNTERS];
     CUDA_TRY(cudaMemcpy(tmp, c->pipe_counters, sizeof tmp, cudaMemcpyDeviceToHost));
