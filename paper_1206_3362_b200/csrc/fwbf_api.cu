@@ -498,8 +498,8 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
 // Shared memory of the filtered circulant kernel (fwbf_circ.cu): the kernel's
 // compile-time layout (CLayout), copied into the parameter block so the gather
 // offsets (uoff) can be computed from it.  EG(1023): 40 KB, 5 CTAs/SM.
-template <int KC, int TB, int WT, int NN> static void layout_c(KParams &P) {
-  using L = fwbf::CLayout<NN, KC * TB, WT>;
+template <int KC, int TB, int WT, int NN, int PB> static void layout_c(KParams &P) {
+  using L = fwbf::CLayout<NN, KC * TB, WT, PB < 0 ? (TB / 32) * 32 * 8 : 0>;
   P.ystage_bytes = L::YSTB;
   P.off_ystage = L::YST;
   P.off_y = L::YST;
@@ -1063,13 +1063,18 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   // defers the rest to this MODE 2 kernel, which then runs over that list.
   const void *ckern = nullptr;
   void (*clayout)(KParams &) = nullptr;
-  if (mode2 && sizeof(YT) == 4 && kwt > 0 && c->m == c->n && p->weight_mode == FWBF_WEIGHTS_IMWBF &&
-      p->block_len_p >= 16 && !P.force_ordered && !getenv("FWBF_NO_CDEC")) {
-#define FWBF_PICK_C(KC_, TB_, WT_, NN_, PB_)                                          \
-    if (kc == KC_ && T == TB_ && kwt == WT_ && c->n == NN_ && (PB_ == 0 || PB_ == p->block_len_p) && \
-        !(PB_ == 0 && ckern)) {                                                         \
-      ckern = (const void *)fwbf::cdecode_kernel<KC_, TB_, WT_, NN_, PB_>;              \
-      clayout = layout_c<KC_, TB_, WT_, NN_>;                                           \
+  // MLP-WBF (lambda <= 31) on the same kernel with the filtered top-lambda
+  // selection, under the same conditions as FWBF's filtered metric
+  const bool cmlp = p->algorithm == FWBF_ALG_MLP && p->lam >= 1 && p->lam <= fwbf::kCircMaxLam && circ &&
+                    sizeof(YT) == 4 && kwt > 0 && !metric_out && !p->force_ordered &&
+                    !getenv("FWBF_NO_FILTER") && !getenv("FWBF_NO_SPLIT");
+  if ((mode2 || cmlp) && sizeof(YT) == 4 && kwt > 0 && c->m == c->n && p->weight_mode == FWBF_WEIGHTS_IMWBF &&
+      (cmlp || p->block_len_p >= 16) && !P.force_ordered && !getenv("FWBF_NO_CDEC")) {
+#define FWBF_PICK_C(KC_, TB_, WT_, NN_, PB_)                                                        \
+    if (kc == KC_ && T == TB_ && kwt == WT_ && c->n == NN_ &&                                      \
+        (cmlp ? PB_ < 0 : (PB_ == 0 || PB_ == p->block_len_p)) && !(PB_ == 0 && ckern)) {          \
+      ckern = (const void *)fwbf::cdecode_kernel<KC_, TB_, WT_, NN_, PB_>;                          \
+      clayout = layout_c<KC_, TB_, WT_, NN_, PB_>;                                                  \
     }
     FWBF_CIRC_CONFIGS(FWBF_PICK_C)
 #undef FWBF_PICK_C

@@ -1,4 +1,4 @@
-// fwbf_circ.cu -- filtered FWBF decoding of circulant (EG) codes on B200 (round 3).
+// fwbf_circ.cu -- filtered FWBF and MLP-WBF decoding of cyclic EG codes on B200.
 //
 // The headline path: FWBF (decoders.py:156-167, :181-183) on float32 y for a
 // cyclic EG code whose length and weight are compiled in.  One persistent CTA
@@ -139,11 +139,196 @@ __device__ __forceinline__ void select_block(const KParams &P, uint32_t sE, cons
   }
 }
 
+// ---- MLP-WBF top-lambda (decoders.py:174-178) ------------------------------
+// 64-bit ranking key of a column: the order-preserving float key above the
+// complemented index, so a larger key is a larger value, then a lower index
+// (np.argsort(-e, kind="stable")).
+__device__ __forceinline__ unsigned long long mkey(float v, int n) {
+  return ((unsigned long long)fkey(v) << 32) | (uint32_t)~n;
+}
+__device__ __forceinline__ float mkey_val(unsigned long long k) { return fkey_val((uint32_t)(k >> 32)); }
+__device__ __forceinline__ int mkey_idx(unsigned long long k) { return (int)~(uint32_t)k; }
+
+// Warp argmax of 64-bit keys by two REDUX reductions (keys are unique).
+__device__ __forceinline__ unsigned long long warp_kmax(unsigned long long k) {
+  const uint32_t hi = (uint32_t)(k >> 32), lo = (uint32_t)k;
+  const uint32_t mh = __reduce_max_sync(FULL_MASK, hi);
+  const uint32_t ml = __reduce_max_sync(FULL_MASK, hi == mh ? lo : 0u);
+  return ((unsigned long long)mh << 32) | ml;
+}
+
+// Per warp: the nl best keys of columns base + lane + 32 t (t < CPL), written
+// best first to lst[0 .. nl).  Each lane sorts its CPL keys once; a round's
+// winner is the warp maximum of the lane heads, and the winning lane pops.
+template <int CPL>
+__device__ __forceinline__ void mlp_warp_list(const float *Efl, int N, int base, int lane, int nl,
+                                              unsigned long long *lst) {
+  unsigned long long kk[CPL];
+#pragma unroll
+  for (int t = 0; t < CPL; ++t) {
+    const int n = base + lane + 32 * t;
+    kk[t] = mkey(n < N ? Efl[n] : -INFINITY, n);
+  }
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) // descending (CPL <= 4: a few compare-exchanges)
+#pragma unroll
+    for (int j = CPL - 1; j > i; --j)
+      if (kk[j] > kk[j - 1]) { const unsigned long long t = kk[j]; kk[j] = kk[j - 1]; kk[j - 1] = t; }
+  unsigned long long mine = 0ull;
+  for (int r = 0; r < nl; ++r) {
+    const unsigned long long w = warp_kmax(kk[0]);
+    if (kk[0] == w) {
+#pragma unroll
+      for (int t = 0; t + 1 < CPL; ++t) kk[t] = kk[t + 1];
+      kk[CPL - 1] = 0ull;
+    }
+    if (lane == r) mine = w;
+  }
+  if (lane < nl) lst[lane] = mine;
+}
+
+// Exact top-lambda of the columns whose filtered value is >= thr (the band
+// the filter leaves open, and everything above it): lambda rounds of an
+// exact-metric warp argmax over the columns still unranked.  Lane r receives
+// the r-th (value, column).  Rare path; recomputes the candidates' exact
+// sums each round.
+template <int WT>
+__device__ void mlp_exact_top(const KParams &P, const float *Efl, const float *sFA, const uint16_t *sA2,
+                              const float *sM2, const float *yabs, int N, float thr, int lam, int lane,
+                              double qexp, double qinv, double &xv, int &xi) {
+  // Each lane caches the exact values of up to 4 of its candidates (columns
+  // lane + 32 q): the exact sums run once, lanes in parallel, and the rounds
+  // only rank cached values.  More than 4 candidates in a lane (quantised
+  // inputs with many equal metrics): rounds recompute, ranking below the
+  // previous round's winner.
+  int c0 = -1, c1 = -1, c2 = -1, c3 = -1;
+  bool over = false;
+  for (int n = lane; n < N; n += 32)
+    if (Efl[n] >= thr) {
+      if (c0 < 0) c0 = n;
+      else if (c1 < 0) c1 = n;
+      else if (c2 < 0) c2 = n;
+      else if (c3 < 0) c3 = n;
+      else over = true;
+    }
+  if (!__any_sync(FULL_MASK, over)) {
+    const double x0 = c0 >= 0 ? exact_split_metric(P, sFA, sA2, sM2, yabs, c0, WT, qexp, qinv) : -dinf();
+    const double x1 = c1 >= 0 ? exact_split_metric(P, sFA, sA2, sM2, yabs, c1, WT, qexp, qinv) : -dinf();
+    const double x2 = c2 >= 0 ? exact_split_metric(P, sFA, sA2, sM2, yabs, c2, WT, qexp, qinv) : -dinf();
+    const double x3 = c3 >= 0 ? exact_split_metric(P, sFA, sA2, sM2, yabs, c3, WT, qexp, qinv) : -dinf();
+    uint32_t tk = 0u; // ranked cache slots
+    for (int r = 0; r < lam; ++r) {
+      double ve = -dinf();
+      int ie = 0x7fffffff, slot = -1;
+      if (c0 >= 0 && !(tk & 1u) && (x0 > ve || (x0 == ve && c0 < ie))) { ve = x0; ie = c0; slot = 0; }
+      if (c1 >= 0 && !(tk & 2u) && (x1 > ve || (x1 == ve && c1 < ie))) { ve = x1; ie = c1; slot = 1; }
+      if (c2 >= 0 && !(tk & 4u) && (x2 > ve || (x2 == ve && c2 < ie))) { ve = x2; ie = c2; slot = 2; }
+      if (c3 >= 0 && !(tk & 8u) && (x3 > ve || (x3 == ve && c3 < ie))) { ve = x3; ie = c3; slot = 3; }
+      const int mine = ie;
+      warp_amax_redux(ve, ie);
+      if (slot >= 0 && mine == ie) tk |= 1u << slot;
+      if (lane == r) { xv = ve; xi = ie; }
+    }
+    return;
+  }
+  double pv = dinf();
+  int pi = -1;
+  for (int r = 0; r < lam; ++r) {
+    double ve = -dinf();
+    int ie = 0x7fffffff;
+    for (int n = lane; n < N; n += 32) {
+      if (Efl[n] >= thr) {
+        const double e = exact_split_metric(P, sFA, sA2, sM2, yabs, n, WT, qexp, qinv);
+        if (e < pv || (e == pv && n > pi)) amax_combine(ve, ie, e, n);
+      }
+    }
+    warp_amax_redux(ve, ie);
+    pv = ve;
+    pi = ie;
+    if (lane == r) { xv = ve; xi = ie; }
+  }
+}
+
+// Warp 0: merge the per-warp lists, decide the flips on the filtered values
+// where the band settles them (the lambda-th and (lambda+1)-th more than
+// 2 fdelta apart; every member farther than fdelta from 0 when thresholded),
+// exactly otherwise; set the flip bits, the flip count, the stall flag and
+// the flip log (ascending columns).  The stall policy's global argmax
+// (decoders.py:214-222) is decided here too.
+template <int NW, int WT>
+__device__ void mlp_decide(const KParams &P, const float *Efl, const float *sFA, const uint16_t *sA2,
+                           const float *sM2, const float *yabs, int *misc, const unsigned long long *lst,
+                           int lam, int lane, float fd2, float fdp, uint32_t *fdc, int N, int *flog,
+                           int sF, int sStall, int sEq) {
+  int ptr = 0;
+  unsigned long long head = lane < NW ? lst[32 * lane] : 0ull;
+  unsigned long long top = 0ull; // lane r: the r-th best overall (filtered values)
+  for (int r = 0; r < lam; ++r) {
+    const unsigned long long w = warp_kmax(head);
+    if (lane < NW && head == w) head = lst[32 * lane + (++ptr)];
+    if (lane == r) top = w;
+  }
+  const unsigned long long nxt = warp_kmax(head); // the (lambda+1)-th
+  const bool member = lane < lam;
+  float v = mkey_val(top);
+  int idx = mkey_idx(top);
+  const float vT = __shfl_sync(FULL_MASK, v, lam - 1);
+  const float v1 = lam > 1 ? __shfl_sync(FULL_MASK, v, 1) : mkey_val(nxt);
+  const float vN = mkey_val(nxt);
+  const bool thr_on = P.mlp_thr != 0;
+  const bool settled = vN < vT - fd2;
+  const bool signamb = thr_on && __any_sync(FULL_MASK, member && v > -fdp && v <= fdp);
+  double xv = (double)v;
+  const int eq = misc[sEq];
+  if (!settled || signamb) { // exact decisions
+    mlp_exact_top<WT>(P, Efl, sFA, sA2, sM2, yabs, N, vT - fd2, lam, lane, pow2d(eq), pow2d(-eq), xv, idx);
+    if (lane == 0 && P.filter_stats) atomicAdd((unsigned long long *)P.filter_stats, 1ull);
+  }
+  bool sel = member && (!thr_on || xv > 0.0);
+  uint32_t sm = __ballot_sync(FULL_MASK, sel);
+  int stall = 0;
+  if (!sm) { // no candidate: terminate, or flip the global argmax
+    stall = 1;
+    if (P.stall != FWBF_STALL_TERMINATE) {
+      int gi = __shfl_sync(FULL_MASK, idx, 0);
+      // lane 0 holds the exact top-1 if the exact path ran; otherwise the
+      // filtered first is exact when it leads the second by more than 2 fdelta
+      if (settled && !signamb && !(v1 < __shfl_sync(FULL_MASK, v, 0) - fd2)) {
+        double gv;
+        mlp_exact_top<WT>(P, Efl, sFA, sA2, sM2, yabs, N, __shfl_sync(FULL_MASK, v, 0) - fd2, 1, lane, pow2d(eq),
+                          pow2d(-eq), gv, gi);
+        gi = __shfl_sync(FULL_MASK, gi, 0);
+        if (lane == 0 && P.filter_stats) atomicAdd((unsigned long long *)P.filter_stats + 1, 1ull);
+      }
+      sel = lane == 0;
+      idx = gi;
+      sm = 1u;
+    }
+  }
+  if (sel) {
+    const int i2 = idx + N;
+    atomicOr(fdc + (idx >> 5), 1u << (idx & 31));
+    atomicOr(fdc + (i2 >> 5), 1u << (i2 & 31));
+  }
+  if (flog) { // ascending columns: rank among the selected
+    int rank = 0;
+    for (int r = 0; r < 32; ++r) {
+      const int o = __shfl_sync(FULL_MASK, idx, r);
+      rank += ((sm >> r) & 1u) && o < idx;
+    }
+    if (sel) flog[rank] = idx;
+  }
+  if (lane == 0) {
+    misc[sF] = __popc(sm);
+    misc[sStall] = stall;
+  }
+}
+
 template <int KC, int TB, int WT, int NN, int PB>
 __global__ void __launch_bounds__(TB, TB == 256 ? FWBF_CMINB_256 : 1024 / TB)
 cdecode_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  using L = CLayout<NN, KC * TB, WT>;
+  using L = CLayout<NN, KC * TB, WT, PB < 0 ? (TB / 32) * 32 * 8 : 0>;
   constexpr int NW = TB / 32;
   constexpr int NP = KC / 2; // column pairs per thread in the gather
   constexpr int N = NN;      // cyclic code: N columns, N checks
@@ -170,7 +355,7 @@ cdecode_kernel(const __grid_constant__ KParams P) {
   int *rot = reinterpret_cast<int *>(smem_raw + L::ROT);      // rotated offsets (ascending row walk)
   int *misc = reinterpret_cast<int *>(smem_raw + L::MISC);
   float *redf = reinterpret_cast<float *>(misc + 16);
-  enum { S_FRAME = 0, S_SWT0, S_SWT1, S_F0, S_F1, S_PATH, S_EQ, S_VMAX, S_YMAX, S_NONFIN };
+  enum { S_FRAME = 0, S_SWT0, S_SWT1, S_F0, S_F1, S_PATH, S_EQ, S_VMAX, S_YMAX, S_NONFIN, S_MSTALL };
 
   for (int j = tid; j < WT; j += TB) {
     rot[j] = P.off[j] - N; // check m's columns in ascending order: the wrapped
@@ -477,141 +662,169 @@ cdecode_kernel(const __grid_constant__ KParams P) {
       CPH(2)
       if (tid == 0) misc[S_SWT0 + ((k + 1) & 1)] = 0; // read at the top of iteration k - 1
 
-      // ---- selection: warp per p-block (decoders.py:156-167, :181-183) ----
-      // warp w takes blocks w + NW jj; lane jj keeps block jj's result, and
-      // the warp applies all its flips with one pass of its lanes
       uint32_t *fdc = fdb + (k & 1) * L::FDW;
-      {
-        const uint32_t sE = s0 + L::E;
-        double rv = 0.0;
-        int ri = 0;
-        int jj = 0;
-        if constexpr (PB > 0) { // block length compiled in: every block index and bound is an immediate
-          constexpr int NBK = (N + PB - 1) / PB;
-          constexpr int JM = (NBK + NW - 1) / NW;
-          if constexpr (PB <= 32) {
-            // all of this warp's blocks as independent straight-line chains
-            // (load, key, two REDUX, band test) the scheduler can overlap;
-            // blocks the band leaves open are re-decided afterwards
-            float rvf = 0.f;
-            uint32_t ambm = 0u;
-#pragma unroll
-            for (int j2 = 0; j2 < JM; ++j2) {
-              const int b = warp + j2 * NW;
-              if ((j2 + 1) * NW > NBK && b >= NBK) break; // warp-uniform
-              const int base = b * PB;
-              const int lim = (N % PB == 0) ? PB : min(PB, N - base);
-              const int fi = base + lane;
-              const float e = Efl[fi]; // (lanes past the block read inside the metric region; masked)
-              const float fv = lane < lim ? e : -INFINITY;
-              const uint32_t ka = fkey(fv);
-              const uint32_t kmx = __reduce_max_sync(FULL_MASK, ka);
-              const int imin = (int)__reduce_min_sync(FULL_MASK, ka == kmx ? (uint32_t)fi : 0xffffffffu);
-              const float fmx = fkey_val(kmx);
-              // runner-up = every other lane's value (one column per lane)
-              const bool amb = __any_sync(FULL_MASK, fi != imin && fv >= fmx - fd2) || (fmx > -fdp && fmx <= fdp);
-              ambm |= (amb ? 1u : 0u) << j2;
-              if (lane == j2) { rvf = fmx; ri = imin; }
-              jj = j2 + 1;
-            }
-            rv = (double)rvf;
-            while (ambm) { // rare: exact decisions
-              const int j2 = __ffs(ambm) - 1;
-              ambm &= ambm - 1u;
-              const int base = (warp + j2 * NW) * PB;
-              const int lim = (N % PB == 0) ? PB : min(PB, N - base);
-              select_block<WT, true>(P, sE, Efl, sFA, sA2, sM2, yabs, misc + S_EQ, base, lim, lane, j2, fd2, fdp, rv,
-                                     ri);
+      int F;
+      if constexpr (PB >= 0) {
+        // ---- selection: warp per p-block (decoders.py:156-167, :181-183) ----
+        // warp w takes blocks w + NW jj; lane jj keeps block jj's result, and
+        // the warp applies all its flips with one pass of its lanes
+        {
+          const uint32_t sE = s0 + L::E;
+          double rv = 0.0;
+          int ri = 0;
+          int jj = 0;
+          if constexpr (PB > 0) { // block length compiled in: every block index and bound is an immediate
+            constexpr int NBK = (N + PB - 1) / PB;
+            constexpr int JM = (NBK + NW - 1) / NW;
+            if constexpr (PB <= 32) {
+              // all of this warp's blocks as independent straight-line chains
+              // (load, key, two REDUX, band test) the scheduler can overlap;
+              // blocks the band leaves open are re-decided afterwards
+              float rvf = 0.f;
+              uint32_t ambm = 0u;
+  #pragma unroll
+              for (int j2 = 0; j2 < JM; ++j2) {
+                const int b = warp + j2 * NW;
+                if ((j2 + 1) * NW > NBK && b >= NBK) break; // warp-uniform
+                const int base = b * PB;
+                const int lim = (N % PB == 0) ? PB : min(PB, N - base);
+                const int fi = base + lane;
+                const float e = Efl[fi]; // (lanes past the block read inside the metric region; masked)
+                const float fv = lane < lim ? e : -INFINITY;
+                const uint32_t ka = fkey(fv);
+                const uint32_t kmx = __reduce_max_sync(FULL_MASK, ka);
+                const int imin = (int)__reduce_min_sync(FULL_MASK, ka == kmx ? (uint32_t)fi : 0xffffffffu);
+                const float fmx = fkey_val(kmx);
+                // runner-up = every other lane's value (one column per lane)
+                const bool amb = __any_sync(FULL_MASK, fi != imin && fv >= fmx - fd2) || (fmx > -fdp && fmx <= fdp);
+                ambm |= (amb ? 1u : 0u) << j2;
+                if (lane == j2) { rvf = fmx; ri = imin; }
+                jj = j2 + 1;
+              }
+              rv = (double)rvf;
+              while (ambm) { // rare: exact decisions
+                const int j2 = __ffs(ambm) - 1;
+                ambm &= ambm - 1u;
+                const int base = (warp + j2 * NW) * PB;
+                const int lim = (N % PB == 0) ? PB : min(PB, N - base);
+                select_block<WT, true>(P, sE, Efl, sFA, sA2, sM2, yabs, misc + S_EQ, base, lim, lane, j2, fd2, fdp, rv,
+                                       ri);
+              }
+            } else {
+  #pragma unroll
+              for (int j2 = 0; j2 < JM; ++j2) {
+                const int b = warp + j2 * NW;
+                if ((j2 + 1) * NW > NBK && b >= NBK) break; // warp-uniform
+                const int base = b * PB;
+                const int lim = (N % PB == 0) ? PB : min(PB, N - base);
+                select_block<WT, false>(P, sE, Efl, sFA, sA2, sM2, yabs, misc + S_EQ, base, lim, lane, j2, fd2, fdp,
+                                        rv, ri);
+                jj = j2 + 1;
+              }
             }
           } else {
-#pragma unroll
-            for (int j2 = 0; j2 < JM; ++j2) {
-              const int b = warp + j2 * NW;
-              if ((j2 + 1) * NW > NBK && b >= NBK) break; // warp-uniform
-              const int base = b * PB;
-              const int lim = (N % PB == 0) ? PB : min(PB, N - base);
-              select_block<WT, false>(P, sE, Efl, sFA, sA2, sM2, yabs, misc + S_EQ, base, lim, lane, j2, fd2, fdp,
-                                      rv, ri);
-              jj = j2 + 1;
+            const int p = P.p;
+            for (int base = warp * p; base < N; base += NW * p, ++jj) {
+              const int lim = min(p, N - base);
+              if (lim <= 32)
+                select_block<WT, true>(P, sE, Efl, sFA, sA2, sM2, yabs, misc + S_EQ, base, lim, lane, jj, fd2, fdp, rv, ri);
+              else
+                select_block<WT, false>(P, sE, Efl, sFA, sA2, sM2, yabs, misc + S_EQ, base, lim, lane, jj, fd2, fdp, rv, ri);
             }
           }
-        } else {
-          const int p = P.p;
-          for (int base = warp * p; base < N; base += NW * p, ++jj) {
-            const int lim = min(p, N - base);
-            if (lim <= 32)
-              select_block<WT, true>(P, sE, Efl, sFA, sA2, sM2, yabs, misc + S_EQ, base, lim, lane, jj, fd2, fdp, rv, ri);
-            else
-              select_block<WT, false>(P, sE, Efl, sFA, sA2, sM2, yabs, misc + S_EQ, base, lim, lane, jj, fd2, fdp, rv, ri);
+          const bool mine = lane < jj;
+          const bool flip = mine && rv > 0.0;
+          if (mine) {
+            const int b = warp + lane * NW;
+            blk_v[b] = rv;
+            blk_i[b] = ri;
           }
+          if (flip) {
+            const int i2 = ri + N;
+            atomicOr(fdc + (ri >> 5), 1u << (ri & 31));
+            atomicOr(fdc + (i2 >> 5), 1u << (i2 & 31));
+          }
+          const uint32_t fm = __ballot_sync(FULL_MASK, flip);
+          if (lane == 0 && fm) atomicAdd(&misc[S_F0 + (k & 1)], __popc(fm));
         }
-        const bool mine = lane < jj;
-        const bool flip = mine && rv > 0.0;
-        if (mine) {
-          const int b = warp + lane * NW;
-          blk_v[b] = rv;
-          blk_i[b] = ri;
-        }
-        if (flip) {
-          const int i2 = ri + N;
-          atomicOr(fdc + (ri >> 5), 1u << (ri & 31));
-          atomicOr(fdc + (i2 >> 5), 1u << (i2 & 31));
-        }
-        const uint32_t fm = __ballot_sync(FULL_MASK, flip);
-        if (lane == 0 && fm) atomicAdd(&misc[S_F0 + (k & 1)], __popc(fm));
-      }
-      __syncthreads(); // B2: flips chosen
-      CPH(3)
-      int F = misc[S_F0 + (k & 1)];
-      if (F == 0) {
-        // nothing selected while the syndrome is nonzero (decoders.py:214-222)
-        stalled = 1;
-        if (P.stall == FWBF_STALL_TERMINATE) {
-          if (tid == 0 && P.fliplog_counts) P.fliplog_counts[(long long)f * P.kmax + k] = 0;
-          k += 1;
-          break;
-        }
-        if (warp == 0) {
+        __syncthreads(); // B2: flips chosen
+        CPH(3)
+        F = misc[S_F0 + (k & 1)];
+        if (F == 0) {
+          // nothing selected while the syndrome is nonzero (decoders.py:214-222)
+          stalled = 1;
+          if (P.stall == FWBF_STALL_TERMINATE) {
+            if (tid == 0 && P.fliplog_counts) P.fliplog_counts[(long long)f * P.kmax + k] = 0;
+            k += 1;
+            break;
+          }
+          if (warp == 0) {
+            const int nb = P.nblocks;
+            double gv = -dinf();
+            int gi = 0x7fffffff;
+            for (int bb = lane; bb < nb; bb += 32) amax_combine(gv, gi, blk_v[bb], blk_i[bb]);
+            warp_amax(gv, gi);
+            // the block maxima are exact argmaxes, their values within fdelta
+            const double thr = gv - (double)fd2;
+            int nc = 0;
+            for (int bb = lane; bb < nb; bb += 32) nc += blk_v[bb] >= thr;
+            nc = __reduce_add_sync(FULL_MASK, nc);
+            if (nc > 1) {
+              const double qexp = pow2d(misc[S_EQ]), qinv = pow2d(-misc[S_EQ]);
+              double ve = -dinf();
+              int ie = 0x7fffffff;
+              for (int bb = lane; bb < nb; bb += 32)
+                if (blk_v[bb] >= thr)
+                  amax_combine(ve, ie, exact_split_metric(P, sFA, sA2, sM2, yabs, blk_i[bb], WT, qexp, qinv), blk_i[bb]);
+              warp_amax(ve, ie);
+              gi = ie;
+              if (lane == 0 && P.filter_stats) atomicAdd((unsigned long long *)P.filter_stats + 1, 1ull);
+            }
+            if (lane == 0) {
+              const int g2 = gi + N;
+              fdc[gi >> 5] |= 1u << (gi & 31);
+              fdc[g2 >> 5] |= 1u << (g2 & 31);
+              if (P.fliplog) P.fliplog[(long long)f * P.fliplog_stride + nflips] = gi;
+            }
+          }
+          F = 1;
+          __syncthreads();
+        } else if (P.fliplog && warp == 0) { // ascending = block order
           const int nb = P.nblocks;
-          double gv = -dinf();
-          int gi = 0x7fffffff;
-          for (int bb = lane; bb < nb; bb += 32) amax_combine(gv, gi, blk_v[bb], blk_i[bb]);
-          warp_amax(gv, gi);
-          // the block maxima are exact argmaxes, their values within fdelta
-          const double thr = gv - (double)fd2;
-          int nc = 0;
-          for (int bb = lane; bb < nb; bb += 32) nc += blk_v[bb] >= thr;
-          nc = __reduce_add_sync(FULL_MASK, nc);
-          if (nc > 1) {
-            const double qexp = pow2d(misc[S_EQ]), qinv = pow2d(-misc[S_EQ]);
-            double ve = -dinf();
-            int ie = 0x7fffffff;
-            for (int bb = lane; bb < nb; bb += 32)
-              if (blk_v[bb] >= thr)
-                amax_combine(ve, ie, exact_split_metric(P, sFA, sA2, sM2, yabs, blk_i[bb], WT, qexp, qinv), blk_i[bb]);
-            warp_amax(ve, ie);
-            gi = ie;
-            if (lane == 0 && P.filter_stats) atomicAdd((unsigned long long *)P.filter_stats + 1, 1ull);
-          }
-          if (lane == 0) {
-            const int g2 = gi + N;
-            fdc[gi >> 5] |= 1u << (gi & 31);
-            fdc[g2 >> 5] |= 1u << (g2 & 31);
-            if (P.fliplog) P.fliplog[(long long)f * P.fliplog_stride + nflips] = gi;
+          int cnt = 0;
+          for (int base = 0; base < nb; base += 32) {
+            const int bb = base + lane;
+            const bool pos = bb < nb && blk_v[bb] > 0.0;
+            const uint32_t msk = __ballot_sync(FULL_MASK, pos);
+            if (pos)
+              P.fliplog[(long long)f * P.fliplog_stride + nflips + cnt + __popc(msk & ((1u << lane) - 1u))] = blk_i[bb];
+            cnt += __popc(msk);
           }
         }
-        F = 1;
+      } else {
+        // ---- MLP-WBF: top-lambda by (value desc, index asc), > 0 when
+        // thresholded, flipped in ascending order (decoders.py:174-178) ----
+        // per warp: its columns' lambda + 1 best as 64-bit keys (REDUX
+        // argmax rounds over lane-sorted heads); then warp 0 merges the lists
+        // and decides on the filtered values, exactly where the band is open
+        unsigned long long *lst = reinterpret_cast<unsigned long long *>(smem_raw + L::LST);
+        const int lam = P.lam;
+        mlp_warp_list<(N + TB - 1) / TB>(Efl, N, warp * 32 * ((N + TB - 1) / TB), lane, lam + 1, lst + warp * 32);
         __syncthreads();
-      } else if (P.fliplog && warp == 0) { // ascending = block order
-        const int nb = P.nblocks;
-        int cnt = 0;
-        for (int base = 0; base < nb; base += 32) {
-          const int bb = base + lane;
-          const bool pos = bb < nb && blk_v[bb] > 0.0;
-          const uint32_t msk = __ballot_sync(FULL_MASK, pos);
-          if (pos)
-            P.fliplog[(long long)f * P.fliplog_stride + nflips + cnt + __popc(msk & ((1u << lane) - 1u))] = blk_i[bb];
-          cnt += __popc(msk);
+        if (warp == 0)
+          mlp_decide<NW, WT>(P, Efl, sFA, sA2, sM2, yabs, misc, lst, lam, lane, fd2, fdp, fdc, N,
+                             P.fliplog ? P.fliplog + (long long)f * P.fliplog_stride + nflips : nullptr,
+                             S_F0 + (k & 1), S_MSTALL, S_EQ);
+        __syncthreads(); // B2: flips chosen
+        CPH(3)
+        F = misc[S_F0 + (k & 1)];
+        if (misc[S_MSTALL]) {
+          stalled = 1;
+          if (P.stall == FWBF_STALL_TERMINATE) { // nothing selected (decoders.py:214-222)
+            if (tid == 0 && P.fliplog_counts) P.fliplog_counts[(long long)f * P.kmax + k] = 0;
+            k += 1;
+            break;
+          }
         }
       }
       if (P.fliplog && tid == 0) P.fliplog_counts[(long long)f * P.kmax + k] = F;

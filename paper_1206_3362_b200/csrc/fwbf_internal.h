@@ -34,7 +34,8 @@ constexpr int kMaxQcBlocks = 256;  // quasi-cyclic shift table entries in the pa
 
 // Filtered FWBF kernel for cyclic EG codes (fwbf_circ.cu): (KC, TB, WT, N),
 // the code length and weight compiled in (EG(255), EG(1023), EG(4095)).
-// PB > 0: the FWBF block length compiled in as well (0: any p >= 16).
+// PB > 0: the FWBF block length compiled in as well (0: any p >= 16);
+// PB = -1: MLP-WBF (top-lambda selection, lambda <= 31).
 #define FWBF_CIRC_CONFIGS(X) \
   X(2, 128, 16, 255, 0)      \
   X(4, 256, 32, 1023, 0)     \
@@ -43,13 +44,17 @@ constexpr int kMaxQcBlocks = 256;  // quasi-cyclic shift table entries in the pa
   X(4, 1024, 64, 4095, 64)   \
   X(4, 1024, 64, 4095, 128)  \
   X(4, 1024, 64, 4095, 256)  \
-  X(4, 256, 32, 1023, 93)
+  X(4, 256, 32, 1023, 93)    \
+  X(2, 128, 16, 255, -1)     \
+  X(4, 256, 32, 1023, -1)    \
+  X(4, 1024, 64, 4095, -1)
+constexpr int kCircMaxLam = 31; // MLP lists: lambda + 1 <= 32 entries per warp
 
 // Its shared-memory layout (byte offsets), a compile-time function of the code
 // so every access in the kernel is [base + immediate]; the host reads the same
 // constants (layout_c in fwbf_api.cu).  Blocks: p >= 16, so at most
 // ceil(N / 16) of them.
-template <int NN, int COVER, int WT> struct CLayout {
+template <int NN, int COVER, int WT, int LSTB = 0> struct CLayout {
   static constexpr int al(int x) { return (x + 15) & ~15; }
   static constexpr int mx(int a, int b) { return a > b ? a : b; }
   static constexpr int EP = (NN + 1) & ~1;     // |y| after the metric (even: float2 reads)
@@ -72,7 +77,8 @@ template <int NN, int COVER, int WT> struct CLayout {
   static constexpr int BI = BV + al(NBMAX * 8);
   static constexpr int ROT = BI + al(NBMAX * 4);
   static constexpr int MISC = ROT + al(2 * WT * 4);
-  static constexpr int BYTES = MISC + al(80 * 4);
+  static constexpr int LST = MISC + al(80 * 4); // MLP: per-warp candidate lists (LSTB bytes)
+  static constexpr int BYTES = LST + al(LSTB);
 };
 
 struct KParams {

@@ -1,11 +1,13 @@
-"""The filtered FWBF kernel for cyclic EG codes (csrc/fwbf_circ.cu, round 3).
+"""The filtered kernel for cyclic EG codes (csrc/fwbf_circ.cu): FWBF and MLP-WBF.
 
 It decodes every frame its guard admits (finite y, some |y| > 0, the fp64
 guard of DESIGN.md section 2) and defers the rest to decode_kernel through a
 frame list.  Its results must equal decode_kernel's MODE 2 (FWBF_NO_CDEC=1)
 and the oracle bit for bit: hard decisions, iterations, flags, flip counts
 and the flip sequence, for compiled-in and runtime block lengths, both stall
-policies, and batches that mix deferred frames in.
+policies, and batches that mix deferred frames in.  MLP-WBF (lambda <= 31)
+runs on the same kernel with a filtered top-lambda selection and must equal
+decode_kernel's exact MODE 0 and the oracle.
 """
 
 import os
@@ -32,31 +34,36 @@ def _frames(code, ebn0, frames, seed, quant=None):
     return h, y.astype(np.float32)
 
 
-def _decode(h, y, cfg, cdec=True):
+def _decode(h, y, cfg, cdec=True, alg="fwbf"):
     """decode_batch with or without the circulant kernel (FWBF_NO_CDEC is read per launch)."""
     if cdec:
         os.environ.pop("FWBF_NO_CDEC", None)
     else:
         os.environ["FWBF_NO_CDEC"] = "1"
     try:
-        r = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+        r = decode_batch(h, y, cfg, alg, flip_log=True)
         kern = nat.last_kernel()
     finally:
         os.environ.pop("FWBF_NO_CDEC", None)
     return r, kern
 
 
-def _same(a, b, tag):
+def _same(a, b, tag, flag_mask=0xff):
+    """flag_mask 11 (converged, stalled, non-finite): the metric-path bits may
+    differ from decode_kernel's exact MODE 0 (it flags frames that fail the
+    split-fp32 guard as fp64-guarded; the filtered kernel's path is one)."""
     for name in ("iterations", "flips_total", "flags"):
         u, v = getattr(a, name).cpu().numpy(), getattr(b, name).cpu().numpy()
+        if name == "flags":
+            u, v = u & flag_mask, v & flag_mask
         assert np.array_equal(u, v), f"{tag}: {name} differs at {np.nonzero(u != v)[0][:8]}"
     assert np.array_equal(a.z_bits.cpu().numpy(), b.z_bits.cpu().numpy()), f"{tag}: z differs"
     assert a.flip_logs() == b.flip_logs(), f"{tag}: flip logs differ"
 
 
-def _vs_oracle(res, h, y, cfg, tag, rows=None):
+def _vs_oracle(res, h, y, cfg, tag, rows=None, alg="fwbf"):
     rows = np.arange(y.shape[0]) if rows is None else rows
-    z, its, fl, ft = COracle(h).decode_batch(y[rows], algorithm="fwbf", alpha=cfg.alpha, k_max=cfg.k_max,
+    z, its, fl, ft = COracle(h).decode_batch(y[rows], algorithm=alg, alpha=cfg.alpha, k_max=cfg.k_max,
                                              lam=cfg.lam, p=cfg.block_len_p, weight_mode=cfg.weight_mode,
                                              stall=cfg.stall_policy, mlp_threshold=cfg.mlp_threshold)
     bad = np.nonzero((res.iterations.cpu().numpy()[rows] != its) | ((res.flags.cpu().numpy()[rows] & 3) != fl) |
@@ -142,3 +149,25 @@ def test_circ_kernel_staged_rows(cuda_device):
         os.environ.pop("FWBF_FORCE_YSTAGE", None)
     b, _ = _decode(h, y, cfg, False)
     _same(a, b, "staged rows")
+
+
+@pytest.mark.parametrize("code,lam,ebn0,thr,stall,quant,frames", [
+    ("eg5", 10, 4.0, True, "flip-global-max", None, 2048),   # config E's comparison decoder
+    ("eg5", 10, 3.0, True, "flip-global-max", None, 512),
+    ("eg5", 1, 4.0, True, "flip-global-max", None, 512),
+    ("eg5", 3, 3.5, False, "flip-global-max", None, 512),    # unthresholded: lambda flips every iteration
+    ("eg5", 31, 4.0, True, "flip-global-max", None, 512),    # the largest lambda the kernel takes
+    ("eg5", 10, 3.5, True, "terminate", None, 512),
+    ("eg5", 10, 3.5, True, "flip-global-max", 8, 512),       # quantised: ties, exact decisions
+    ("eg5", 5, 3.5, True, "terminate", 4, 512),
+    ("eg4", 10, 4.0, True, "flip-global-max", None, 1024),   # EG(255)
+    ("eg6", 10, 4.0, True, "flip-global-max", None, 96),     # EG(4095)
+])
+def test_circ_kernel_mlp_equals_mode0_and_oracle(cuda_device, code, lam, ebn0, thr, stall, quant, frames):
+    h, y = _frames(code, ebn0, frames, seed=lam * 17 + frames, quant=quant)
+    cfg = DecoderConfig(lam=lam, k_max=40, alpha=1.5 if quant else 0.2, mlp_threshold=thr, stall_policy=stall)
+    a, ka = _decode(h, y, cfg, True, "mlp")
+    b, kb = _decode(h, y, cfg, False, "mlp")
+    assert ka == "cdecode+decode_kernel" and kb == "decode_kernel", (ka, kb)
+    _same(a, b, f"mlp/{code}/l{lam}/{ebn0}dB/q{quant}", flag_mask=11)
+    _vs_oracle(a, h, y, cfg, f"mlp/{code}/l{lam}", rows=np.arange(min(frames, 256)), alg="mlp")
