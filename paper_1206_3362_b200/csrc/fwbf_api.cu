@@ -779,7 +779,7 @@ static int launch_qc(fwbf_code *c, const fwbf_params *p, const float *y, long lo
                      const fwbf_outputs &o, cudaStream_t stream, bool *used) {
   *used = false;
   const int Z = c->qc_z, pp = p->block_len_p;
-  if (!Z || c->qc_jb > 4 || pp % 32 || pp > Z || Z % pp || c->n > 0xffff || c->m > 32 * 512) return FWBF_OK;
+  if (!Z || c->qc_jb > 4 || pp % 32 || pp > Z || Z % pp || c->m > 32 * 512) return FWBF_OK;
   const int tpc = pp / 32;
   const void *kern = tpc == 1 ? (const void *)fwbf::qdecode_kernel<1>
                    : tpc == 2 ? (const void *)fwbf::qdecode_kernel<2>
@@ -807,10 +807,10 @@ static int launch_qc(fwbf_code *c, const fwbf_params *p, const float *y, long lo
   int off = 0;
   auto take = [&](int bytes) { int r0 = off; off = align16(off + bytes); return r0; };
   P.off_y = take(c->n * 4);
-  P.off_rec = take(P.jb * (Z + pp) * 8);
-  P.off_amc = take(P.jb * (Z + pp) * 2);
-  P.off_zrec = take(pp * 8);
-  P.off_zamc = take(pp * 2);
+  P.off_m1 = take(P.jb * (Z + pp) * 4);
+  P.off_m2 = take(P.jb * (Z + pp) * 4);
+  P.off_cmask = take((c->n + 3) / 4 * 4);
+  P.off_zrec = take(pp * 4);
   P.off_sbits = take(((c->m + 31) / 32) * 4);
   P.off_zbits = take(((c->n + 31) / 32) * 4);
   P.off_blkv = take(P.nb * 8);

@@ -204,7 +204,7 @@ struct QParams {
   int nb;                    // blocks (p = 32 * TPC columns each)
   int kmax, stall, wmode;
   double alpha;
-  int off_y, off_rec, off_amc, off_zrec, off_zamc, off_sbits, off_zbits, off_blkv, off_blki, off_misc;
+  int off_y, off_m1, off_m2, off_cmask, off_zrec, off_sbits, off_zbits, off_blkv, off_blki, off_misc;
   const float *y;
   long long ld;
   long long batch;

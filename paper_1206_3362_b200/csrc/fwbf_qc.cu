@@ -11,12 +11,17 @@
 // takes columns base + l + 32 t (t < p / 32).  Its check in row block r is
 // i0 + 32 t with i0 = (o0 + l - s) mod Z, so with each row block's records
 // stored twice over their first p entries ("doubled head") the lane's
-// records are rec_r[i0 + 32 t]: a pointer per row block and an immediate
-// offset per t -- no index arithmetic per edge.  An absent block points at a
-// row of zero records.  Per edge: the check's argmin column (u16), its
-// (sgn min1, sgn min2) float pair, a select, float -> double, one DADD in
-// ascending check order from +0.0 (adding the +0.0 of an absent block to a
-// sum that started at +0.0 is the identity) -- the reference's fp64 sum.
+// records are m1_r[i0 + 32 t] / m2_r[i0 + 32 t]: two pointers per row block
+// and an immediate offset per t -- no index arithmetic per edge.  An absent
+// block points at a row of zeros.  Each column carries a 4-bit argmin mask
+// (bit r: the column is the argmin of its check in row block r, set at frame
+// init), so per edge the mask bit picks the sgn*min1 or the sgn*min2 array
+// and one 4-byte load, float -> double and one DADD follow, in ascending
+// check order from the first term (starting from +0.0 differs at most in the
+// sign of a zero sum, which no comparison sees) -- the reference's fp64 sum.
+// (Round 2, third session: the records were (min1, min2) pairs plus a u16
+// argmin column per check, 3 shared wavefronts per warp and edge instead of
+// 1 + 1/4.)
 //
 // Flips toggle z and syndrome words (atomic XOR); after a CTA barrier every
 // thread negates the records of its own checks whose syndrome bit changed
@@ -43,10 +48,10 @@ __global__ void __launch_bounds__(512, 2) qdecode_kernel(const __grid_constant__
   const int T = blockDim.x;
   const int N = P.n, M = P.m, Z = P.z, lgz = P.lgz, H = P.head, RS = P.z + P.head;
   float *ys = reinterpret_cast<float *>(sm + P.off_y);           // signed y, -0 -> +0
-  float2 *rec = reinterpret_cast<float2 *>(sm + P.off_rec);      // [jb][Z + H] (sgn min1, sgn min2)
-  uint16_t *amc = reinterpret_cast<uint16_t *>(sm + P.off_amc);  // [jb][Z + H] argmin column
-  const float2 *rzero = reinterpret_cast<const float2 *>(sm + P.off_zrec); // [H] (0, 0)
-  const uint16_t *azero = reinterpret_cast<const uint16_t *>(sm + P.off_zamc); // [H] 0xffff
+  float *m1 = reinterpret_cast<float *>(sm + P.off_m1);          // [jb][Z + H] sgn min1
+  float *m2 = reinterpret_cast<float *>(sm + P.off_m2);          // [jb][Z + H] sgn min2 (MWBF: min1)
+  uint8_t *cmask = reinterpret_cast<uint8_t *>(sm + P.off_cmask); // [N] argmin bit per row block
+  const float *rzero = reinterpret_cast<const float *>(sm + P.off_zrec); // [H] zeros
   uint32_t *sbits = reinterpret_cast<uint32_t *>(sm + P.off_sbits);
   uint32_t *zbits = reinterpret_cast<uint32_t *>(sm + P.off_zbits);
   double *blk_v = reinterpret_cast<double *>(sm + P.off_blkv);
@@ -57,10 +62,7 @@ __global__ void __launch_bounds__(512, 2) qdecode_kernel(const __grid_constant__
   const double alpha = P.alpha;
   const int zw = (N + 31) >> 5, nKm = (M + T - 1) / T;
 
-  for (int i = tid; i < H; i += T) {
-    const_cast<float2 *>(rzero)[i] = make_float2(0.f, 0.f);
-    const_cast<uint16_t *>(azero)[i] = 0xffffu;
-  }
+  for (int i = tid; i < H; i += T) const_cast<float *>(rzero)[i] = 0.f;
   long long c_frames = 0, c_biterr = 0, c_worderr = 0, c_iters = 0, c_flips = 0, c_stalls = 0, c_conv = 0,
             c_edges = 0;
 
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(512, 2) qdecode_kernel(const __grid_constant__
         nonfin |= !isfinite(v);
       }
     }
+    for (int w = tid; w < (N + 3) >> 2; w += T) reinterpret_cast<uint32_t *>(cmask)[w] = 0u;
     if (tid == 0) { misc[Q_SWT] = 0; misc[Q_F] = 0; misc[Q_FLIP] = 0; }
     nonfin = __syncthreads_or(nonfin);
     for (int w0 = warp * 32; w0 < N; w0 += T) {
@@ -122,14 +125,14 @@ __global__ void __launch_bounds__(512, 2) qdecode_kernel(const __grid_constant__
         }
         par >>= 31;
         const float sg = par ? 1.0f : -1.0f;
-        const float2 rv = make_float2(sg * min1, sg * (imw ? min2 : min1));
-        const uint16_t av = imw ? (uint16_t)ac : (uint16_t)0xffffu; // MWBF: every edge reads min1
-        rec[r * RS + i] = rv;
-        amc[r * RS + i] = av;
+        const float v1 = sg * min1, v2 = sg * (imw ? min2 : min1); // MWBF: every edge reads min1
+        m1[r * RS + i] = v1;
+        m2[r * RS + i] = v2;
         if (i < H) {
-          rec[r * RS + Z + i] = rv;
-          amc[r * RS + Z + i] = av;
+          m1[r * RS + Z + i] = v1;
+          m2[r * RS + Z + i] = v2;
         }
+        if (imw) atomicOr(reinterpret_cast<uint32_t *>(cmask) + (ac >> 2), 1u << (r + 8 * (ac & 3)));
         sprev |= par << k;
       }
       const uint32_t b = __ballot_sync(QFULL, par != 0);
@@ -152,29 +155,27 @@ __global__ void __launch_bounds__(512, 2) qdecode_kernel(const __grid_constant__
       // fused metric + block argmax + flips: warp w owns blocks w, w + nwarps, ...
       for (int b = warp; b < P.nb; b += nwarps) {
         const int base = b * TPC * 32, cb = base >> lgz, o0 = (base & (Z - 1)) + lane;
-        const float2 *pr[4];
-        const uint16_t *pa[4];
+        const float *p1[4], *p2[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int s = r < P.jb ? P.shift[r * P.kb + cb] : -1;
           const int i0 = (o0 - s) & (Z - 1);
-          pr[r] = s >= 0 ? rec + r * RS + i0 : rzero + lane;
-          pa[r] = s >= 0 ? amc + r * RS + i0 : azero + lane;
+          p1[r] = s >= 0 ? m1 + r * RS + i0 : rzero + lane;
+          p2[r] = s >= 0 ? m2 + r * RS + i0 : rzero + lane;
         }
         double v = -qdinf();
         int vi = 0x7fffffff;
 #pragma unroll
         for (int t = 0; t < TPC; ++t) {
           const int n = base + lane + 32 * t;
+          const uint32_t mk = cmask[n]; // bit r: n is the argmin of its check in row block r
           // the reference's sum starts at +0.0; starting at the first term
           // instead differs at most in the sign of a zero sum, which no
           // comparison (> 0, argmax) can see
           double acc = 0.0;
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
-            const float2 w = pr[r][32 * t];
-            const bool am = (uint32_t)pa[r][32 * t] == (uint32_t)n; // zero-extended u16 vs n < 2^16
-            const double x = (double)(am ? w.y : w.x);
+            const double x = (double)(((mk >> r) & 1u) ? p2[r] : p1[r])[32 * t];
             acc = r == 0 ? x : __dadd_rn(acc, x);
           }
           const double e = __dsub_rn(acc, __dmul_rn(alpha, (double)fabsf(ys[n])));
@@ -272,11 +273,11 @@ __global__ void __launch_bounds__(512, 2) qdecode_kernel(const __grid_constant__
           const uint32_t s = (word >> lane) & 1u;
           if (m < M && s != ((sprev >> kk) & 1u)) {
             const int r = m >> lgz, i = m & (Z - 1);
-            float2 *p0 = rec + r * RS + i;
-            const float2 w = *p0;
-            const float2 nw = make_float2(-w.x, -w.y);
-            *p0 = nw;
-            if (i < H) p0[Z] = nw;
+            float *q1 = m1 + r * RS + i, *q2 = m2 + r * RS + i;
+            const float a = -*q1, b = -*q2;
+            *q1 = a;
+            *q2 = b;
+            if (i < H) { q1[Z] = a; q2[Z] = b; }
             sprev ^= 1u << kk;
           }
           pc += __popc(word);
