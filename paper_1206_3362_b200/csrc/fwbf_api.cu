@@ -1172,7 +1172,6 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
   if (rc) return rc;
   if (per_sm < 1) return fail(FWBF_EUNSUPPORTED, "kernel does not fit on an SM");
   const long long grid = std::min<long long>(batch, (long long)per_sm * c->sm_count);
-  CUDA_TRY(cudaMemsetAsync(P.work_counter, 0, sizeof(unsigned), stream));
   static long long *phase_buf = nullptr;
   const bool phases = getenv("FWBF_PHASES") != nullptr;
   if (phases) {
@@ -1200,12 +1199,15 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
       if (rc) return rc;
     }
     if (cper >= 1) {
-      // frames outside the filtered guard: appended to a list (count in a
-      // second queue slot), decoded by decode_kernel afterwards (third slot)
-      unsigned *dcount = c->d_work + (c->work_slot.fetch_add(1) % kWorkRing);
-      unsigned *lwork = c->d_work + (c->work_slot.fetch_add(1) % kWorkRing);
-      CUDA_TRY(cudaMemsetAsync(dcount, 0, sizeof(unsigned), stream));
-      CUDA_TRY(cudaMemsetAsync(lwork, 0, sizeof(unsigned), stream));
+      // frames outside the filtered guard are appended to a list and
+      // decoded by decode_kernel afterwards; three adjacent queue slots, one
+      // memset: this kernel's frame queue, the defer count, decode_kernel's
+      // queue over the list
+      unsigned *trio = c->d_work + (c->work_slot.fetch_add(3) % (kWorkRing - 2));
+      CUDA_TRY(cudaMemsetAsync(trio, 0, 3 * sizeof(unsigned), stream));
+      Q.work_counter = trio;
+      unsigned *dcount = trio + 1;
+      unsigned *lwork = trio + 2;
       int *dlist = nullptr;
       static std::once_flag pool_once[64];
       std::call_once(pool_once[c->device & 63], [&] {
@@ -1247,6 +1249,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
       return FWBF_OK;
     }
   }
+  CUDA_TRY(cudaMemsetAsync(P.work_counter, 0, sizeof(unsigned), stream));
   void *args[] = {&P};
   CUDA_TRY(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(T), args, P.smem_bytes, stream));
   CUDA_TRY(cudaGetLastError());

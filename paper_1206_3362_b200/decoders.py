@@ -288,6 +288,28 @@ def _result_tensors(res: "BatchResult"):
             getattr(res, "y", None)]
 
 
+def _new_result(torch, n, B, zw, k_max, kw, batches=0):
+    """Output tensors of one decode.  Per-frame outputs are written for every
+    frame by the kernels, so they start uninitialised; the accumulated ones
+    (counters, iteration histogram, per-batch word errors) are views of one
+    zeroed allocation -- one memset instead of eight per call (small batches
+    are launch-bound)."""
+    nacc = nat.NCOUNTERS + k_max + 1 + (batches + 1) // 2
+    acc = torch.zeros(nacc, dtype=torch.int64, **kw)
+    res = BatchResult(
+        n=n,
+        z_bits=torch.empty((B, zw), dtype=torch.int32, **kw),
+        iterations=torch.empty(B, dtype=torch.int32, **kw),
+        flags=torch.empty(B, dtype=torch.uint8, **kw),
+        flips_total=torch.empty(B, dtype=torch.int32, **kw),
+        bit_errors=torch.empty(B, dtype=torch.int32, **kw),
+        counters=acc[:nat.NCOUNTERS],
+        iter_hist=acc[nat.NCOUNTERS:nat.NCOUNTERS + k_max + 1])
+    if batches:
+        res.batch_word_err = acc[nat.NCOUNTERS + k_max + 1:].view(torch.int32)[:batches]
+    return res
+
+
 def decode_batch(h, y, cfg: DecoderConfig, algorithm: str = "fwbf", *, flip_log: bool = False,
                  codeword=None, device=None, force_ordered: bool = False, stream=None) -> BatchResult:
     """Decode a batch of frames Y[B, ld>=N] (float32 or float64; torch or numpy).
@@ -326,15 +348,7 @@ def decode_batch(h, y, cfg: DecoderConfig, algorithm: str = "fwbf", *, flip_log:
     L = nat.lib()
     zw = (dc.n + 31) // 32
     kw = dict(device=dev)
-    res = BatchResult(
-        n=dc.n,
-        z_bits=torch.zeros((B, zw), dtype=torch.int32, **kw),
-        iterations=torch.zeros(B, dtype=torch.int32, **kw),
-        flags=torch.zeros(B, dtype=torch.uint8, **kw),
-        flips_total=torch.zeros(B, dtype=torch.int32, **kw),
-        bit_errors=torch.zeros(B, dtype=torch.int32, **kw),
-        counters=torch.zeros(nat.NCOUNTERS, dtype=torch.int64, **kw),
-        iter_hist=torch.zeros(cfg.k_max + 1, dtype=torch.int64, **kw))
+    res = _new_result(torch, dc.n, B, zw, cfg.k_max, kw)
     stride = 0
     if flip_log:
         maxf = int(L.fwbf_max_flips_per_iter(dc.handle, C.byref(p)))
@@ -419,15 +433,7 @@ def decode_awgn(h, cfg: DecoderConfig, algorithm: str, seed: int, first_frame: i
     B = int(count)
     zw = (dc.n + 31) // 32
     kw = dict(device=dev)
-    res = BatchResult(
-        n=dc.n,
-        z_bits=torch.zeros((B, zw), dtype=torch.int32, **kw),
-        iterations=torch.zeros(B, dtype=torch.int32, **kw),
-        flags=torch.zeros(B, dtype=torch.uint8, **kw),
-        flips_total=torch.zeros(B, dtype=torch.int32, **kw),
-        bit_errors=torch.zeros(B, dtype=torch.int32, **kw),
-        counters=torch.zeros(nat.NCOUNTERS, dtype=torch.int64, **kw),
-        iter_hist=torch.zeros(cfg.k_max + 1, dtype=torch.int64, **kw))
+    res = _new_result(torch, dc.n, B, zw, cfg.k_max, kw, batches=max(1, -(-B // batch_frames)))
     stride = 0
     if flip_log:
         maxf = int(L.fwbf_max_flips_per_iter(dc.handle, C.byref(p)))
@@ -437,7 +443,6 @@ def decode_awgn(h, cfg: DecoderConfig, algorithm: str, seed: int, first_frame: i
     cw_t = None
     if codeword is not None:
         cw_t = torch.from_numpy(pack_bits(codeword, dc.n).view(np.int32)).to(dev)
-    res.batch_word_err = torch.zeros(max(1, -(-B // batch_frames)), dtype=torch.int32, **kw)
     out = _outputs(res, stride, cw_t)
     out.batch_word_err = res.batch_word_err.data_ptr()
     out.batch_frames = int(batch_frames)
