@@ -499,7 +499,7 @@ static void layout(const fwbf_code *c, const fwbf_params *p, int ysize, bool cir
 // compile-time layout (CLayout), copied into the parameter block so the gather
 // offsets (uoff) can be computed from it.  EG(1023): 40 KB, 5 CTAs/SM.
 template <int KC, int TB, int WT, int NN, int PB> static void layout_c(KParams &P) {
-  using L = fwbf::CLayout<NN, KC * TB, WT, PB < 0 ? (TB / 32) * 32 * 8 : 0>;
+  using L = fwbf::CLayout<NN, KC * TB, WT, PB < 0 ? (TB / 32) * 32 * 8 : 0, fwbf::CircShape<TB, PB>::kStage>;
   P.ystage_bytes = L::YSTB;
   P.off_ystage = L::YST;
   P.off_y = L::YST;
@@ -1183,7 +1183,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     KParams Q = P; // the filtered circulant kernel's own layout, TMA-staged rows when they qualify
     clayout(Q);
     const long long row_bytes = ld * (long long)sizeof(YT);
-    Q.y_stage = !getenv("FWBF_NO_YSTAGE") && ((uintptr_t)y % 16) == 0 && row_bytes % 16 == 0 &&
+    Q.y_stage = Q.ystage_bytes > 0 && !getenv("FWBF_NO_YSTAGE") && ((uintptr_t)y % 16) == 0 && row_bytes % 16 == 0 &&
                 (long long)Q.ystage_bytes <= row_bytes &&
                 (batch >= 128LL * c->sm_count || getenv("FWBF_FORCE_YSTAGE"));
     Q.alias_y = 0;

@@ -40,10 +40,6 @@
 #include "fwbf_internal.h"
 #include "fwbf_device.cuh"
 
-#ifndef FWBF_CMINB_256
-#define FWBF_CMINB_256 5
-#endif
-
 namespace fwbf {
 
 // order-preserving 32-bit key of a float (-0.0 and +0.0 tie; no NaN here)
@@ -325,10 +321,10 @@ __device__ void mlp_decide(const KParams &P, const float *Efl, const float *sFA,
 }
 
 template <int KC, int TB, int WT, int NN, int PB>
-__global__ void __launch_bounds__(TB, TB == 256 ? FWBF_CMINB_256 : 1024 / TB)
+__global__ void __launch_bounds__(TB, CircShape<TB, PB>::kMinBlocks)
 cdecode_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  using L = CLayout<NN, KC * TB, WT, PB < 0 ? (TB / 32) * 32 * 8 : 0>;
+  using L = CLayout<NN, KC * TB, WT, PB < 0 ? (TB / 32) * 32 * 8 : 0, CircShape<TB, PB>::kStage>;
   constexpr int NW = TB / 32;
   constexpr int NP = KC / 2; // column pairs per thread in the gather
   constexpr int N = NN;      // cyclic code: N columns, N checks

@@ -50,11 +50,20 @@ constexpr int kMaxQcBlocks = 256;  // quasi-cyclic shift table entries in the pa
   X(4, 1024, 64, 4095, -1)
 constexpr int kCircMaxLam = 31; // MLP lists: lambda + 1 <= 32 entries per warp
 
+// FWBF on EG(1023) (256 threads) runs 6 CTAs per SM at 40 registers without
+// the staging buffer (4 KB less shared memory: 36.3 KB): +3 % over 5 CTAs
+// with staged rows.  Other shapes keep the staging buffer.
+template <int TB, int PB> struct CircShape {
+  static constexpr bool kSix = TB == 256 && PB >= 0;
+  static constexpr bool kStage = !kSix;
+  static constexpr int kMinBlocks = TB == 256 ? (kSix ? 6 : 5) : 1024 / TB;
+};
+
 // Its shared-memory layout (byte offsets), a compile-time function of the code
 // so every access in the kernel is [base + immediate]; the host reads the same
 // constants (layout_c in fwbf_api.cu).  Blocks: p >= 16, so at most
 // ceil(N / 16) of them.
-template <int NN, int COVER, int WT, int LSTB = 0> struct CLayout {
+template <int NN, int COVER, int WT, int LSTB = 0, bool STAGE = true> struct CLayout {
   static constexpr int al(int x) { return (x + 15) & ~15; }
   static constexpr int mx(int a, int b) { return a > b ? a : b; }
   static constexpr int EP = (NN + 1) & ~1;     // |y| after the metric (even: float2 reads)
@@ -63,7 +72,7 @@ template <int NN, int COVER, int WT, int LSTB = 0> struct CLayout {
   static constexpr int NBMAX = (NN + 15) / 16;
   static constexpr int DBLF = (2 * NN + mx(0, COVER - NN) + 2 + 31) / 32 * 32;
   static constexpr int YST = 0;                // y row (TMA staging target), 16-byte aligned
-  static constexpr int YSTB = al(NN * 4);
+  static constexpr int YSTB = STAGE ? al(NN * 4) : 0; // (none: the row is read from HBM)
   static constexpr int E = YST + YSTB;         // float metric [EP] + |y| [N]
   static constexpr int FA = E + al((EP + mx(NN, COVER)) * 4);
   static constexpr int FB = FA + al(DBLF * 4);
