@@ -389,7 +389,10 @@ cdecode_kernel(const __grid_constant__ KParams P) {
 
   for (;;) {
     __syncthreads();
-    if (!ystage && tid == 0) misc[S_FRAME] = (int)atomicAdd(P.work_counter, 1u);
+    if (tid == 0) {
+      if (!ystage) misc[S_FRAME] = (int)atomicAdd(P.work_counter, 1u);
+      misc[S_NONFIN] = 0; // (every read of the previous frame's flag is behind the barrier above)
+    }
     __syncthreads();
     CPH(0)
     const unsigned fu = (unsigned)misc[S_FRAME];
@@ -452,50 +455,50 @@ cdecode_kernel(const __grid_constant__ KParams P) {
       misc[S_F1] = 0;
     }
     __syncthreads();
-    if (tid == 0) {
-      float mn = INFINITY, mx = 0.f;
-      for (int w2 = 0; w2 < NW; ++w2) { mn = fminf(mn, redf[w2]); mx = fmaxf(mx, redf[32 + w2]); }
-      // decode_kernel MODE 2's filtered-path condition: finite y, some |y| > 0,
-      // every sum of 2 W weights exact in fp64 (2 W max|y| < 2^53 q with
-      // q = 2^(e_min - 23)), and the quantum within the float range the
-      // filter's grid needs.  Everything else goes to the exact kernel.
-      int keep = 0, eq = 0;
-      if (!misc[S_NONFIN] && mn < INFINITY) {
-        int e = ((__float_as_int(mn) >> 23) & 0xff) - 127;
-        if (e < -126) e = -126;
-        eq = e - 23;
-        keep = (2.0 * (double)WT * (double)mx < ldexp(1.0, 30 + e)) && eq >= -123 && eq <= 77;
-      }
-      misc[S_NONFIN] = 0;
-      misc[S_PATH] = keep;
-      misc[S_EQ] = eq;
-      misc[S_YMAX] = __float_as_int(mx);
-      misc[S_VMAX] = 0;
-      if (!keep) P.defer_list[atomicAdd(P.defer_count, 1u)] = f;
+    // every thread takes the path decision itself (no serial section, no
+    // second barrier) -- decode_kernel MODE 2's filtered-path condition:
+    // finite y, some |y| > 0, every sum of 2 W weights exact in fp64
+    // (2 W max|y| < 2^53 q with q = 2^(e_min - 23)), and the quantum within
+    // the float range the filter's grid needs.  Everything else goes to the
+    // exact kernel.
+    float mn = INFINITY, ymaxf = 0.f;
+#pragma unroll
+    for (int w2 = 0; w2 < NW; ++w2) { mn = fminf(mn, redf[w2]); ymaxf = fmaxf(ymaxf, redf[32 + w2]); }
+    int eq = 0;
+    bool keep = false;
+    if (!misc[S_NONFIN] && mn < INFINITY) {
+      int e = ((__float_as_int(mn) >> 23) & 0xff) - 127;
+      if (e < -126) e = -126;
+      eq = e - 23;
+      keep = (2.0 * (double)WT * (double)ymaxf < ldexp(1.0, 30 + e)) && eq >= -123 && eq <= 77;
     }
-    __syncthreads();
-    if (!misc[S_PATH]) {
-      if (ystage && tid == 0) { // every read of ybuf for this frame is done
+    if (!keep) {
+      if (tid == 0) {
+        P.defer_list[atomicAdd(P.defer_count, 1u)] = f;
+        if (ystage) { // every read of ybuf for this frame is done
+          const unsigned t1 = atomicAdd(P.work_counter, 1u);
+          misc[S_FRAME] = (int)t1;
+          if ((long long)t1 < P.batch)
+            bulk_row_to_smem(ybuf, reinterpret_cast<const float *>(P.y) + (long long)t1 * P.ld, (unsigned)L::YSTB,
+                             &ystage_bar);
+        }
+      }
+      continue;
+    }
+    if (tid == 0) {
+      misc[S_EQ] = eq;
+      misc[S_VMAX] = 0;
+      if (ystage) { // ybuf is dead for this frame: claim the next one and start its copy
         const unsigned t1 = atomicAdd(P.work_counter, 1u);
         misc[S_FRAME] = (int)t1;
         if ((long long)t1 < P.batch)
           bulk_row_to_smem(ybuf, reinterpret_cast<const float *>(P.y) + (long long)t1 * P.ld, (unsigned)L::YSTB,
                            &ystage_bar);
       }
-      continue;
-    }
-
-    if (ystage && tid == 0) { // ybuf is dead for this frame: claim the next one and start its copy
-      const unsigned t1 = atomicAdd(P.work_counter, 1u);
-      misc[S_FRAME] = (int)t1;
-      if ((long long)t1 < P.batch)
-        bulk_row_to_smem(ybuf, reinterpret_cast<const float *>(P.y) + (long long)t1 * P.ld, (unsigned)L::YSTB,
-                         &ystage_bar);
     }
 
     // ---------------- init 2: check minima, syndrome, signed weights -------------
-    const int eq = misc[S_EQ]; // quantum q = 2^eq
-    const float ymaxf = __int_as_float(misc[S_YMAX]);
+    // quantum q = 2^eq, largest |y| ymaxf (both from the decision above)
     // coarse grid G = 2^gsh q for the argmin corrections: |Dc| <= 2^24
     const int gbits = ilogbf(ymaxf) + 1 - eq;
     const int gsh = gbits > 24 ? gbits - 24 : 0;
