@@ -125,6 +125,8 @@ struct fwbf_code {
   void *noise_buf = nullptr;
   size_t noise_bytes = 0;
   cudaEvent_t noise_evt = nullptr; // last use of noise_buf (device-side ordering across streams)
+  cudaStream_t noise_side = nullptr; // decode_awgn: odd chunks (noise + decode) on a second stream
+  cudaEvent_t noise_fork = nullptr, noise_join = nullptr;
   // explicit-code warp-per-frame plans, one per block length p
   std::mutex xplan_mu;
   std::list<XPlan> xplans; // stable addresses: launches hold a plan pointer outside the lock
@@ -332,6 +334,9 @@ extern "C" int fwbf_code_destroy(fwbf_code *c) {
   cudaFree(c->pipe_counters);
   cudaFree(c->noise_buf);
   if (c->noise_evt) cudaEventDestroy(c->noise_evt);
+  if (c->noise_side) cudaStreamDestroy(c->noise_side);
+  if (c->noise_fork) cudaEventDestroy(c->noise_fork);
+  if (c->noise_join) cudaEventDestroy(c->noise_join);
   for (XPlan &x : c->xplans) {
     cudaFree(x.d_tab);
     cudaFree(x.d_rtab);
@@ -1326,9 +1331,14 @@ static int decode_awgn_t(fwbf_code *c, const fwbf_params *p, uint64_t seed, int6
   const int n = c->n;
   const long long ld = o.y_out ? o.y_out_ld : ((n + 3) / 4 * 4);
   if (o.y_out && ld < n) return fail(FWBF_EINVAL, "y_out_ld too small");
-  long long chunk = std::min<long long>(count, 1 << 18);
+  // Scratch y: chunks alternate between two buffers and two streams (the
+  // caller's and a library side stream), so a chunk's noise generation and
+  // decode overlap the previous chunk's tail -- the frames that run to
+  // K_max keep a few SMs busy while the rest would idle.
+  long long chunk = std::min<long long>(count, o.y_out ? (1 << 18) : (1 << 17));
   const int bf = o.batch_word_err ? std::max(1, o.batch_frames) : 1;
   chunk = std::max<long long>(bf, chunk / bf * bf);
+  const bool two = !o.y_out && count > chunk;
   DeviceGuard dg;
   CUDA_TRY(cudaSetDevice(c->device));
   YT *scratch = nullptr;
@@ -1340,7 +1350,7 @@ static int decode_awgn_t(fwbf_code *c, const fwbf_params *p, uint64_t seed, int6
     lock.lock();
     if (!c->noise_evt) CUDA_TRY(cudaEventCreateWithFlags(&c->noise_evt, cudaEventDisableTiming));
     else CUDA_TRY(cudaStreamWaitEvent(stream, c->noise_evt, 0));
-    const size_t need = (size_t)chunk * ld * sizeof(YT);
+    const size_t need = (size_t)chunk * ld * sizeof(YT) * (two ? 2 : 1);
     if (need > c->noise_bytes) {
       if (c->noise_buf) cudaFree(c->noise_buf);
       c->noise_buf = nullptr;
@@ -1357,9 +1367,19 @@ static int decode_awgn_t(fwbf_code *c, const fwbf_params *p, uint64_t seed, int6
   CUDA_TRY(cudaFuncSetAttribute((const void *)nk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const long long kmax = p->k_max;
   const long long maxf = fwbf_max_flips_per_iter(c, p);
-  for (long long s = 0; s < count; s += chunk) {
+  if (two) {
+    if (!c->noise_side) CUDA_TRY(cudaStreamCreateWithFlags(&c->noise_side, cudaStreamNonBlocking));
+    if (!c->noise_fork) CUDA_TRY(cudaEventCreateWithFlags(&c->noise_fork, cudaEventDisableTiming));
+    if (!c->noise_join) CUDA_TRY(cudaEventCreateWithFlags(&c->noise_join, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(c->noise_fork, stream)); // the side stream starts after the caller's prior work
+    CUDA_TRY(cudaStreamWaitEvent(c->noise_side, c->noise_fork, 0));
+  }
+  const cudaStream_t caller = stream;
+  long long ci = 0;
+  for (long long s = 0; s < count; s += chunk, ++ci) {
     const long long nb = std::min(chunk, count - s);
-    YT *yb = o.y_out ? (YT *)o.y_out + s * ld : scratch;
+    stream = (two && (ci & 1)) ? c->noise_side : caller; // (chunk ci - 2 used this buffer on this stream)
+    YT *yb = o.y_out ? (YT *)o.y_out + s * ld : scratch + (two ? (ci & 1) * chunk * ld : 0);
     static const bool cta_gen = getenv("FWBF_NOISE_CTA") != nullptr; // the CTA-per-frame generator
     if (cta_gen) {
       const int grid = (int)std::min<long long>(nb, (long long)c->sm_count * 32);
@@ -1385,6 +1405,11 @@ static int decode_awgn_t(fwbf_code *c, const fwbf_params *p, uint64_t seed, int6
     (void)maxf;
     rc = launch_decode<YT>(c, p, yb, nb, ld, &oc, stream);
     if (rc) return rc;
+  }
+  stream = caller;
+  if (two) { // join: the caller's stream waits for the side stream's chunks
+    CUDA_TRY(cudaEventRecord(c->noise_join, c->noise_side));
+    CUDA_TRY(cudaStreamWaitEvent(stream, c->noise_join, 0));
   }
   if (!o.y_out) CUDA_TRY(cudaEventRecord(c->noise_evt, stream));
   return FWBF_OK;
