@@ -2,8 +2,8 @@
 //
 // The headline path: FWBF (decoders.py:156-167, :181-183) on float32 y for a
 // cyclic EG code whose length and weight are compiled in.  One persistent CTA
-// decodes one frame at a time (frames from an atomic queue, the next frame's y
-// row staged by a TMA bulk copy).  Same arithmetic contract as decode_kernel's
+// decodes one frame at a time (frames from an atomic queue; except on the
+// 6-CTA EG(1023) shape the next frame's y row is staged by a TMA bulk copy).  Same arithmetic contract as decode_kernel's
 // MODE 2: the metric is summed in fp32 (within a
 // per-frame bound fdelta of the exact one) and every block decision the bound
 // leaves open is re-decided on exact column sums, so flips, iterations and
@@ -28,9 +28,10 @@
 //     syndrome, no compare against remembered syndrome bits).
 // The shared-memory layout is a compile-time function of the code (CLayout,
 // fwbf_internal.h), so every shared access is [base + immediate].  Three CTA
-// barriers per iteration (metric ready, flips chosen, state refreshed); the
-// flip bitmap, flip count and syndrome weight alternate between two slots by
-// iteration parity so no extra barrier clears them.
+// barriers per iteration (metric ready, flips chosen, state refreshed; MLP
+// adds one between its per-warp lists and the merge); the flip bitmap, flip
+// count and syndrome weight alternate between two slots by iteration parity
+// so no extra barrier clears them.
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -52,34 +53,6 @@ __device__ __forceinline__ double pow2d(int e) { return __longlong_as_double((lo
 __device__ __forceinline__ float fkey_val(uint32_t k) {
   return __uint_as_float((k >> 31) ? (k & 0x7fffffffu) : ~k);
 }
-
-// Refresh of toggled check m = tid + KK TB (compile-time KK): negate its signed
-// min1 in both doubled copies and move its argmin column's coarse correction
-// by +-2 Dc (the new sign); shared addresses in registers, KK TB as immediates.
-template <int KK, int KC, int TB, int NN, bool GO = (KK < KC)> struct CRefresh {
-  static __device__ __forceinline__ void run(const uint32_t (&tg)[KC], int lane, uint32_t aFA, uint32_t aFB,
-                                             uint32_t aM2, uint32_t aA2, uint32_t aC, float invG) {
-    if ((tg[KK] >> lane) & 1u) {
-      float v, mn2;
-      unsigned short a2;
-      asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(aFA), "n"(4 * KK * TB));
-      v = -v;
-      asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(aFA), "n"(4 * KK * TB), "f"(v));
-      asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(aFA), "n"(4 * (KK * TB + NN)), "f"(v));
-      asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(aFB), "n"(4 * KK * TB), "f"(v));
-      asm volatile("st.shared.f32 [%0+%1], %2;" ::"r"(aFB), "n"(4 * (KK * TB + NN)), "f"(v));
-      asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(mn2) : "r"(aM2), "n"(4 * KK * TB));
-      asm volatile("ld.shared.u16 %0, [%1+%2];" : "=h"(a2) : "r"(aA2), "n"(2 * KK * TB));
-      const int dc = coarse_dc(mn2, fabsf(v), invG);
-      asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(aC + 4u * (uint32_t)a2), "r"(signbit(v) ? -2 * dc : 2 * dc));
-    }
-    CRefresh<KK + 1, KC, TB, NN>::run(tg, lane, aFA, aFB, aM2, aA2, aC, invG);
-  }
-};
-template <int KK, int KC, int TB, int NN> struct CRefresh<KK, KC, TB, NN, false> {
-  static __device__ __forceinline__ void run(const uint32_t (&)[KC], int, uint32_t, uint32_t, uint32_t, uint32_t,
-                                             uint32_t, float) {}
-};
 
 // One FWBF block decision, warp-wide (decoders.py:156-167, :181-183): lanes
 // scan the block's columns (SHORT: one column per lane, p <= 32), REDUX gives
@@ -351,7 +324,7 @@ cdecode_kernel(const __grid_constant__ KParams P) {
   int *rot = reinterpret_cast<int *>(smem_raw + L::ROT);      // rotated offsets (ascending row walk)
   int *misc = reinterpret_cast<int *>(smem_raw + L::MISC);
   float *redf = reinterpret_cast<float *>(misc + 16);
-  enum { S_FRAME = 0, S_SWT0, S_SWT1, S_F0, S_F1, S_PATH, S_EQ, S_VMAX, S_YMAX, S_NONFIN, S_MSTALL };
+  enum { S_FRAME = 0, S_SWT0, S_SWT1, S_F0, S_F1, S_EQ, S_VMAX, S_NONFIN, S_MSTALL };
 
   for (int j = tid; j < WT; j += TB) {
     rot[j] = P.off[j] - N; // check m's columns in ascending order: the wrapped
