@@ -30,6 +30,7 @@ __global__ void noise_kernel(unsigned long long seed, long long first, long long
 template <int DV> __global__ void xdecode_kernel(const __grid_constant__ XParams P);
 template <int KC, int TB, int WT, int NN, int PB> __global__ void cdecode_kernel(const __grid_constant__ KParams P);
 template <int TPC> __global__ void qdecode_kernel(const __grid_constant__ QParams P);
+template <int TPC> __global__ void qinc_kernel(const __grid_constant__ QParams P);
 template <typename T> __global__ void stage_hard_decision(const T *, long long, uint8_t *);
 __global__ void stage_syndrome(const int *, const int *, int, int, const uint8_t *, long long, uint8_t *);
 __global__ void stage_weights(const int *, const int *, int, long long, const double *, long long, long long,
@@ -786,11 +787,19 @@ static int launch_qc(fwbf_code *c, const fwbf_params *p, const float *y, long lo
   const int Z = c->qc_z, pp = p->block_len_p;
   if (!Z || c->qc_jb > 4 || pp % 32 || pp > Z || Z % pp || c->m > 32 * 512) return FWBF_OK;
   const int tpc = pp / 32;
-  const void *kern = tpc == 1 ? (const void *)fwbf::qdecode_kernel<1>
-                   : tpc == 2 ? (const void *)fwbf::qdecode_kernel<2>
-                   : tpc == 4 ? (const void *)fwbf::qdecode_kernel<4>
-                   : tpc == 8 ? (const void *)fwbf::qdecode_kernel<8>
-                   : tpc == 16 ? (const void *)fwbf::qdecode_kernel<16> : nullptr;
+  // the incremental kernel (stored metric keys, only the columns of toggled
+  // checks recomputed) unless switched off; the full-pass kernel otherwise
+  const bool inc = !getenv("FWBF_NO_QCINC") && c->n < 65535;
+  const void *kern = inc ? (tpc == 1 ? (const void *)fwbf::qinc_kernel<1>
+                            : tpc == 2 ? (const void *)fwbf::qinc_kernel<2>
+                            : tpc == 4 ? (const void *)fwbf::qinc_kernel<4>
+                            : tpc == 8 ? (const void *)fwbf::qinc_kernel<8>
+                            : tpc == 16 ? (const void *)fwbf::qinc_kernel<16> : nullptr)
+                         : (tpc == 1 ? (const void *)fwbf::qdecode_kernel<1>
+                            : tpc == 2 ? (const void *)fwbf::qdecode_kernel<2>
+                            : tpc == 4 ? (const void *)fwbf::qdecode_kernel<4>
+                            : tpc == 8 ? (const void *)fwbf::qdecode_kernel<8>
+                            : tpc == 16 ? (const void *)fwbf::qdecode_kernel<16> : nullptr);
   if (!kern) return FWBF_OK;
   fwbf::QParams P;
   memset(&P, 0, sizeof P);
@@ -811,16 +820,33 @@ static int launch_qc(fwbf_code *c, const fwbf_params *p, const float *y, long lo
   P.alpha = p->alpha;
   int off = 0;
   auto take = [&](int bytes) { int r0 = off; off = align16(off + bytes); return r0; };
-  P.off_y = take(c->n * 4);
-  P.off_m1 = take(P.jb * (Z + pp) * 4);
-  P.off_m2 = take(P.jb * (Z + pp) * 4);
-  P.off_cmask = take((c->n + 3) / 4 * 4);
-  P.off_zrec = take(pp * 4);
-  P.off_sbits = take(((c->m + 31) / 32) * 4);
-  P.off_zbits = take(((c->n + 31) / 32) * 4);
-  P.off_blkv = take(P.nb * 8);
-  P.off_blki = take(P.nb * 4);
-  P.off_misc = take(16 * 4);
+  if (inc) {
+    P.off_y = take(c->n * 4);                 // metric keys (y during the check scan)
+    P.off_m1 = take(c->m * 4);
+    P.off_m2 = take(c->m * 4);
+    P.off_cmask = take(c->m * 2);             // argmin column per check (u16)
+    P.off_zrec = take(P.jb * P.kb * 4);       // shift table
+    P.off_sbits = take(((c->m + 31) / 32) * 4);
+    P.off_sold = take(((c->m + 31) / 32) * 4);
+    P.off_zbits = take(((c->n + 31) / 32) * 4);
+    P.off_blkv = take(P.nb * 8);
+    P.off_blki = take(P.nb * 4);
+    P.off_blkk = take(P.nb * 4);
+    P.off_blkf = take(P.nb * 4);
+    P.off_list = take(std::min(c->m, P.jb * (P.nb + 1)) * 4);
+    P.off_misc = take(16 * 4);
+  } else {
+    P.off_y = take(c->n * 4);
+    P.off_m1 = take(P.jb * (Z + pp) * 4);
+    P.off_m2 = take(P.jb * (Z + pp) * 4);
+    P.off_cmask = take((c->n + 3) / 4 * 4);
+    P.off_zrec = take(pp * 4);
+    P.off_sbits = take(((c->m + 31) / 32) * 4);
+    P.off_zbits = take(((c->n + 31) / 32) * 4);
+    P.off_blkv = take(P.nb * 8);
+    P.off_blki = take(P.nb * 4);
+    P.off_misc = take(16 * 4);
+  }
   const int smem = off;
   if (smem > c->smem_optin) return FWBF_OK;
   const int T = 512;
@@ -897,7 +923,7 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
       !getenv("FWBF_NO_QC") && !getenv("FWBF_NO_QCK")) {
     bool used = false;
     rc = launch_qc(c, p, (const float *)y, batch, ld, o, stream, &used);
-    if (used) g_last_kernel = "qdecode";
+    if (used) g_last_kernel = getenv("FWBF_NO_QCINC") || c->n >= 65535 ? "qdecode" : "qinc";
     if (rc || used) return rc;
   }
   if (!c->circ && sizeof(YT) == 4 && p->algorithm == FWBF_ALG_FWBF && !metric_out && !getenv("FWBF_NO_WARP")) {
