@@ -30,7 +30,7 @@ __global__ void noise_kernel(unsigned long long seed, long long first, long long
 template <int DV> __global__ void xdecode_kernel(const __grid_constant__ XParams P);
 template <int KC, int TB, int WT, int NN, int PB> __global__ void cdecode_kernel(const __grid_constant__ KParams P);
 template <int TPC> __global__ void qdecode_kernel(const __grid_constant__ QParams P);
-template <int TPC> __global__ void qinc_kernel(const __grid_constant__ QParams P);
+template <int TPC, bool ALLP> __global__ void qinc_kernel(const __grid_constant__ QParams P);
 template <typename T> __global__ void stage_hard_decision(const T *, long long, uint8_t *);
 __global__ void stage_syndrome(const int *, const int *, int, int, const uint8_t *, long long, uint8_t *);
 __global__ void stage_weights(const int *, const int *, int, long long, const double *, long long, long long,
@@ -790,11 +790,14 @@ static int launch_qc(fwbf_code *c, const fwbf_params *p, const float *y, long lo
   // the incremental kernel (stored metric keys, only the columns of toggled
   // checks recomputed) unless switched off; the full-pass kernel otherwise
   const bool inc = !getenv("FWBF_NO_QCINC") && c->n < 65535;
-  const void *kern = inc ? (tpc == 1 ? (const void *)fwbf::qinc_kernel<1>
-                            : tpc == 2 ? (const void *)fwbf::qinc_kernel<2>
-                            : tpc == 4 ? (const void *)fwbf::qinc_kernel<4>
-                            : tpc == 8 ? (const void *)fwbf::qinc_kernel<8>
-                            : tpc == 16 ? (const void *)fwbf::qinc_kernel<16> : nullptr)
+  bool allp = true; // every circulant block present: the kernel skips the absent-block tests
+  for (int i = 0; i < c->qc_jb * c->qc_kb; ++i) allp = allp && c->qc_shift[i] >= 0;
+#define QINC_PICK(A)                                                                                         \
+  (tpc == 1 ? (const void *)fwbf::qinc_kernel<1, A> : tpc == 2 ? (const void *)fwbf::qinc_kernel<2, A>       \
+   : tpc == 4 ? (const void *)fwbf::qinc_kernel<4, A> : tpc == 8 ? (const void *)fwbf::qinc_kernel<8, A>     \
+   : tpc == 16 ? (const void *)fwbf::qinc_kernel<16, A> : nullptr)
+  const void *kern = inc ? (allp ? QINC_PICK(true) : QINC_PICK(false))
+#undef QINC_PICK
                          : (tpc == 1 ? (const void *)fwbf::qdecode_kernel<1>
                             : tpc == 2 ? (const void *)fwbf::qdecode_kernel<2>
                             : tpc == 4 ? (const void *)fwbf::qdecode_kernel<4>
@@ -822,9 +825,9 @@ static int launch_qc(fwbf_code *c, const fwbf_params *p, const float *y, long lo
   auto take = [&](int bytes) { int r0 = off; off = align16(off + bytes); return r0; };
   if (inc) {
     P.off_y = take(c->n * 4);                 // metric keys (y during the check scan)
-    P.off_m1 = take(c->m * 4);
-    P.off_m2 = take(c->m * 4);
-    P.off_cmask = take(c->m * 2);             // argmin column per check (u16)
+    P.off_m1 = take(2 * c->m * 4);            // sgn min1 [M], then sgn min2 [M]
+    P.off_m2 = P.off_m1 + c->m * 4;
+    P.off_cmask = take((c->n + 3) / 4 * 4);   // argmin bit per row block, per column
     P.off_zrec = take(P.jb * P.kb * 4);       // shift table
     P.off_sbits = take(((c->m + 31) / 32) * 4);
     P.off_sold = take(((c->m + 31) / 32) * 4);

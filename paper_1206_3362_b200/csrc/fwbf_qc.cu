@@ -373,25 +373,27 @@ __device__ __forceinline__ uint32_t qfkey(float v) { // order-preserving; caller
 #define QKEY_ZERO 0x80000000u
 
 struct QView {
-  const float *m1, *m2;
-  const uint16_t *amin;
-  const int *sh;
-  int lgz, zm, jb, kb;
+  const float *rec;       // [2][M]: sgn*min1, then sgn*min2
+  const uint8_t *cmask;   // [N] bit r: the column is the argmin of its check in row block r
+  const int *sh;          // [jb][kb] shifts, -1 = absent block
+  int lgz, zm, jb, kb, m;
   double alpha;
 };
 
-// the reference's Eq.(1) value of column c (ascending checks, fp64, first term first)
-__device__ __forceinline__ double qexact(const QView &V, int c, float y) {
+// the reference's Eq.(1) value of column c (ascending checks, fp64, first term first);
+// ALLP: every circulant block is present
+template <bool ALLP> __device__ __forceinline__ double qexact(const QView &V, int c, float y) {
   const int cb = c >> V.lgz, o = c & V.zm;
+  const uint32_t mk = V.cmask[c];
   double acc = 0.0;
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     double x = 0.0;
     if (r < V.jb) {
       const int s = V.sh[r * V.kb + cb];
-      if (s >= 0) {
+      if (ALLP || s >= 0) {
         const int m = (r << V.lgz) + ((o - s) & V.zm);
-        x = (double)((int)V.amin[m] == c ? V.m2[m] : V.m1[m]);
+        x = (double)V.rec[m + (((mk >> r) & 1u) ? V.m : 0)];
       }
     }
     acc = r == 0 ? x : __dadd_rn(acc, x);
@@ -434,7 +436,32 @@ template <int TPC> __device__ __forceinline__ int qcol(int base0, int lane, int 
   else return base0 + TPC * lane + u;
 }
 
-template <int TPC> // columns per lane per block (p / 32)
+// largest (hi) and second largest (lo) of a lane's keys: sorted pairs merged by a tree
+template <int TPC> __device__ __forceinline__ void qtop2(const uint32_t (&kk)[TPC], uint32_t &hi, uint32_t &lo) {
+  if constexpr (TPC == 1) {
+    hi = kk[0];
+    lo = 0;
+  } else {
+    uint32_t H[TPC / 2], L[TPC / 2];
+#pragma unroll
+    for (int i = 0; i < TPC / 2; ++i) {
+      H[i] = max(kk[2 * i], kk[2 * i + 1]);
+      L[i] = min(kk[2 * i], kk[2 * i + 1]);
+    }
+#pragma unroll
+    for (int n = TPC / 2; n > 1; n >>= 1)
+#pragma unroll
+      for (int i = 0; i < n / 2; ++i) {
+        const uint32_t h1 = H[2 * i], h2 = H[2 * i + 1];
+        L[i] = __vimax3_u32(min(h1, h2), L[2 * i], L[2 * i + 1]);
+        H[i] = max(h1, h2);
+      }
+    hi = H[0];
+    lo = L[0];
+  }
+}
+
+template <int TPC, bool ALLP> // columns per lane per block (p / 32); every circulant block present
 __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QParams P) {
   extern __shared__ __align__(16) unsigned char sm[];
   constexpr int T = 512, nwarps = 16; // launch_qc launches 512 threads
@@ -442,9 +469,9 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
   const int N = P.n, M = P.m, Z = P.z, lgz = P.lgz;
   uint32_t *keys = reinterpret_cast<uint32_t *>(sm + P.off_y);   // [N] metric keys; y during the check scan
   float *ys = reinterpret_cast<float *>(sm + P.off_y);
-  float *m1 = reinterpret_cast<float *>(sm + P.off_m1);          // [M] sgn min1
-  float *m2 = reinterpret_cast<float *>(sm + P.off_m2);          // [M] sgn min2 (MWBF: min1)
-  uint16_t *amin = reinterpret_cast<uint16_t *>(sm + P.off_cmask); // [M] argmin column
+  float *m1 = reinterpret_cast<float *>(sm + P.off_m1);          // [M] sgn min1, then [M] sgn min2 (MWBF: min1)
+  float *m2 = m1 + P.m;
+  uint8_t *cmask = reinterpret_cast<uint8_t *>(sm + P.off_cmask); // [N] argmin bit per row block
   int *sh = reinterpret_cast<int *>(sm + P.off_zrec);            // [jb][kb] shifts
   uint32_t *sbits = reinterpret_cast<uint32_t *>(sm + P.off_sbits);
   uint32_t *sold = reinterpret_cast<uint32_t *>(sm + P.off_sold); // syndrome words the records agree with
@@ -460,8 +487,8 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
   const bool imw = P.wmode == FWBF_WEIGHTS_IMWBF;
   const int zw = (N + 31) >> 5, mw = (M + 31) >> 5, nKm = (M + T - 1) / T;
   QView V;
-  V.m1 = m1; V.m2 = m2; V.amin = amin; V.sh = sh;
-  V.lgz = lgz; V.zm = Z - 1; V.jb = P.jb; V.kb = P.kb; V.alpha = P.alpha;
+  V.rec = m1; V.cmask = cmask; V.sh = sh;
+  V.lgz = lgz; V.zm = Z - 1; V.jb = P.jb; V.kb = P.kb; V.m = M; V.alpha = P.alpha;
 
   for (int i = tid; i < P.jb * P.kb; i += T) sh[i] = P.shift[i];
   long long c_frames = 0, c_biterr = 0, c_worderr = 0, c_iters = 0, c_flips = 0, c_stalls = 0, c_conv = 0,
@@ -495,6 +522,7 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
         nonfin |= !isfinite(v);
       }
     }
+    for (int w = tid; w < (N + 3) >> 2; w += T) reinterpret_cast<uint32_t *>(cmask)[w] = 0u;
     if (tid >= 1 && tid < 8) misc[tid] = 0; // not Q_FRAME: other warps may still be reading it
     nonfin = __syncthreads_or(nonfin);
     for (int w0 = warp * 32; w0 < N; w0 += T) {
@@ -526,7 +554,7 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
         const float sg = par ? 1.0f : -1.0f;
         m1[m] = sg * min1;
         m2[m] = sg * (imw ? min2 : min1); // MWBF: every edge reads min1
-        amin[m] = (uint16_t)(imw ? ac : 0xffff);
+        if (imw) atomicOr(reinterpret_cast<uint32_t *>(cmask) + (ac >> 2), 1u << (r + 8 * (ac & 3)));
       }
       const uint32_t b = __ballot_sync(QFULL, par != 0);
       if (lane == 0 && k * T + warp * 32 < M) {
@@ -538,7 +566,7 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
     }
     __syncthreads();
     // ---- init 3: every column's metric; the key replaces y in the column's own slot ----
-    for (int n = tid; n < N; n += T) keys[n] = qfkey((float)qexact(V, n, ys[n]) + 0.0f);
+    for (int n = tid; n < N; n += T) keys[n] = qfkey((float)qexact<ALLP>(V, n, ys[n]) + 0.0f);
     __syncthreads();
 
     // ---- iterations ----
@@ -556,12 +584,8 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
         const int base0 = b * TPC * 32;
         uint32_t kk[TPC];
         qload_keys<TPC>(keys, base0, lane, kk);
-        uint32_t hi = 0, lo = 0; // the lane's largest and second largest key
-#pragma unroll
-        for (int u = 0; u < TPC; ++u) {
-          lo = max(lo, min(hi, kk[u]));
-          hi = max(hi, kk[u]);
-        }
+        uint32_t hi, lo; // the lane's largest and second largest key
+        qtop2<TPC>(kk, hi, lo);
         const uint32_t Mk = __reduce_max_sync(QFULL, hi);
         const uint32_t holders = __ballot_sync(QFULL, hi == Mk);
         const bool amb = nonfin || Mk == QKEY_ZERO || (holders & (holders - 1u)) != 0u ||
@@ -584,7 +608,7 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
           for (int u = 0; u < TPC; ++u)
             if (nonfin || kk[u] == Mk) {
               const int n = qcol<TPC>(base0, lane, u);
-              const double e = qexact(V, n, __ldg(yr + n) + 0.0f);
+              const double e = qexact<ALLP>(V, n, __ldg(yr + n) + 0.0f);
               if (e > v) { v = e; vi = n; }
             }
           qwarp_amax(v, vi);
@@ -620,57 +644,98 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
           k += 1;
           break;
         }
-        // The global first maximum.  Among the blocks decided on keys alone
-        // only those holding the largest such key can hold it (monotone
-        // rounding); their exact maxima are computed now.
+        // The global first maximum.  Gk = the largest key among the blocks
+        // decided on keys alone; if no block was decided exactly and one
+        // block holds Gk, its (unique) holder is the maximum -- monotone
+        // rounding again.
         uint32_t Gk = 0;
-        for (int bb = lane; bb < P.nb; bb += 32) Gk = max(Gk, blk_k[bb] == 0xffffffffu ? 0u : blk_k[bb]);
+        bool anyx = false;
+        for (int bb = lane; bb < P.nb; bb += 32) {
+          const uint32_t bk = blk_k[bb];
+          anyx |= bk == 0xffffffffu;
+          Gk = max(Gk, bk == 0xffffffffu ? 0u : bk);
+        }
         Gk = __reduce_max_sync(QFULL, Gk);
-        for (int b = warp; b < P.nb; b += nwarps) {
-          const uint32_t bk = blk_k[b];
-          if (bk == 0xffffffffu) continue;           // exact value and winner already stored
-          double v = -qdinf();
-          int vi = 0x7fffffff;
-          if (bk == Gk) {
-            const int base0 = b * TPC * 32;
+        anyx = __any_sync(QFULL, anyx);
+        int cntg = 0, bg = -1;
+        for (int b0 = 0; b0 < P.nb; b0 += 32) {
+          const uint32_t msk = __ballot_sync(QFULL, b0 + lane < P.nb && blk_k[b0 + lane] == Gk);
+          if (msk) {
+            cntg += __popc(msk);
+            if (bg < 0) bg = b0 + __ffs(msk) - 1;
+          }
+        }
+        if (!anyx && cntg == 1) {
+          if (warp == (bg & (nwarps - 1))) {
+            const int base0 = bg * TPC * 32;
             uint32_t kk[TPC];
             qload_keys<TPC>(keys, base0, lane, kk);
+            int idx = -1;
 #pragma unroll
-            for (int u = 0; u < TPC; ++u)
-              if (kk[u] == bk) {
-                const int n = qcol<TPC>(base0, lane, u);
-                const double e = qexact(V, n, __ldg(yr + n) + 0.0f);
-                if (e > v) { v = e; vi = n; }
+            for (int u = TPC - 1; u >= 0; --u)
+              if (kk[u] == Gk) idx = qcol<TPC>(base0, lane, u);
+            const int gi = __shfl_sync(QFULL, idx, __ffs(__ballot_sync(QFULL, idx >= 0)) - 1);
+            if (lane == 0) {
+              atomicXor(&zbits[gi >> 5], 1u << (gi & 31));
+              blk_f[bg] = 1; // logged below as the single flip
+              blk_i[bg] = gi;
+            }
+            if (lane < P.jb) {
+              const int cbv = gi >> lgz, o = gi & (Z - 1), s = sh[lane * P.kb + cbv];
+              if (s >= 0) {
+                const int m = (lane << lgz) + ((o - s) & (Z - 1));
+                atomicXor(&sbits[m >> 5], 1u << (m & 31));
               }
-            qwarp_amax(v, vi);
+            }
           }
-          if (lane == 0) { blk_v[b] = v; blk_i[b] = vi; }
-        }
-        __syncthreads();
-        if (warp == 0) { // the largest exact block maximum, lowest index
-          double gv = -qdinf();
-          int gi = 0x7fffffff;
-          for (int bb = lane; bb < P.nb; bb += 32) {
-            const double v2 = blk_v[bb];
-            const int i2 = blk_i[bb];
-            if (v2 > gv || (v2 == gv && i2 < gi)) { gv = v2; gi = i2; }
-          }
+        } else {
+          // exact maxima of the key-decided blocks that hold Gk (the others cannot hold the maximum)
+          for (int b = warp; b < P.nb; b += nwarps) {
+            const uint32_t bk = blk_k[b];
+            if (bk == 0xffffffffu) continue;           // exact value and winner already stored
+            double v = -qdinf();
+            int vi = 0x7fffffff;
+            if (bk == Gk) {
+              const int base0 = b * TPC * 32;
+              uint32_t kk[TPC];
+              qload_keys<TPC>(keys, base0, lane, kk);
 #pragma unroll
-          for (int off = 16; off; off >>= 1) {
-            const double v2 = __shfl_xor_sync(QFULL, gv, off);
-            const int i2 = __shfl_xor_sync(QFULL, gi, off);
-            if (v2 > gv || (v2 == gv && i2 < gi)) { gv = v2; gi = i2; }
+              for (int u = 0; u < TPC; ++u)
+                if (kk[u] == bk) {
+                  const int n = qcol<TPC>(base0, lane, u);
+                  const double e = qexact<ALLP>(V, n, __ldg(yr + n) + 0.0f);
+                  if (e > v) { v = e; vi = n; }
+                }
+              qwarp_amax(v, vi);
+            }
+            if (lane == 0) { blk_v[b] = v; blk_i[b] = vi; }
           }
-          if (lane == 0) {
-            atomicXor(&zbits[gi >> 5], 1u << (gi & 31));
-            blk_f[gi / (TPC * 32)] = 1; // logged below as the single flip
-            blk_i[gi / (TPC * 32)] = gi;
-          }
-          if (lane < P.jb) {
-            const int cbv = gi >> lgz, o = gi & (Z - 1), s = sh[lane * P.kb + cbv];
-            if (s >= 0) {
-              const int m = (lane << lgz) + ((o - s) & (Z - 1));
-              atomicXor(&sbits[m >> 5], 1u << (m & 31));
+          __syncthreads();
+          if (warp == 0) { // the largest exact block maximum, lowest index
+            double gv = -qdinf();
+            int gi = 0x7fffffff;
+            for (int bb = lane; bb < P.nb; bb += 32) {
+              const double v2 = blk_v[bb];
+              const int i2 = blk_i[bb];
+              if (v2 > gv || (v2 == gv && i2 < gi)) { gv = v2; gi = i2; }
+            }
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+              const double v2 = __shfl_xor_sync(QFULL, gv, off);
+              const int i2 = __shfl_xor_sync(QFULL, gi, off);
+              if (v2 > gv || (v2 == gv && i2 < gi)) { gv = v2; gi = i2; }
+            }
+            if (lane == 0) {
+              atomicXor(&zbits[gi >> 5], 1u << (gi & 31));
+              blk_f[gi / (TPC * 32)] = 1; // logged below as the single flip
+              blk_i[gi / (TPC * 32)] = gi;
+            }
+            if (lane < P.jb) {
+              const int cbv = gi >> lgz, o = gi & (Z - 1), s = sh[lane * P.kb + cbv];
+              if (s >= 0) {
+                const int m = (lane << lgz) + ((o - s) & (Z - 1));
+                atomicXor(&sbits[m >> 5], 1u << (m & 31));
+              }
             }
           }
         }
@@ -729,7 +794,7 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
             if (e < L && lane < P.kb) {
               const int m = tlist[e], r = m >> lgz, i = m & (Z - 1);
               const int s = sh[r * P.kb + lane];
-              if (s >= 0) {
+              if (ALLP || s >= 0) {
                 cc[u] = lane * Z + ((i + s) & (Z - 1));
                 yy[u] = __ldg(yr + cc[u]);
               }
@@ -737,7 +802,7 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            if (cc[u] >= 0) keys[cc[u]] = qfkey((float)qexact(V, cc[u], yy[u] + 0.0f) + 0.0f);
+            if (cc[u] >= 0) keys[cc[u]] = qfkey((float)qexact<ALLP>(V, cc[u], yy[u] + 0.0f) + 0.0f);
         }
         for (int cb = 32 + lane; cb < P.kb; cb += 32) // block columns past the first 32 (wide codes)
           for (int e = warp; e < L; e += nwarps) {
@@ -745,7 +810,7 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
             const int s = sh[r * P.kb + cb];
             if (s >= 0) {
               const int c = cb * Z + ((i + s) & (Z - 1));
-              keys[c] = qfkey((float)qexact(V, c, __ldg(yr + c) + 0.0f) + 0.0f);
+              keys[c] = qfkey((float)qexact<ALLP>(V, c, __ldg(yr + c) + 0.0f) + 0.0f);
             }
           }
       }
@@ -799,10 +864,15 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
   }
 }
 
-template __global__ void qinc_kernel<1>(const __grid_constant__ QParams);
-template __global__ void qinc_kernel<2>(const __grid_constant__ QParams);
-template __global__ void qinc_kernel<4>(const __grid_constant__ QParams);
-template __global__ void qinc_kernel<8>(const __grid_constant__ QParams);
-template __global__ void qinc_kernel<16>(const __grid_constant__ QParams);
+template __global__ void qinc_kernel<1, false>(const __grid_constant__ QParams);
+template __global__ void qinc_kernel<1, true>(const __grid_constant__ QParams);
+template __global__ void qinc_kernel<2, false>(const __grid_constant__ QParams);
+template __global__ void qinc_kernel<2, true>(const __grid_constant__ QParams);
+template __global__ void qinc_kernel<4, false>(const __grid_constant__ QParams);
+template __global__ void qinc_kernel<4, true>(const __grid_constant__ QParams);
+template __global__ void qinc_kernel<8, false>(const __grid_constant__ QParams);
+template __global__ void qinc_kernel<8, true>(const __grid_constant__ QParams);
+template __global__ void qinc_kernel<16, false>(const __grid_constant__ QParams);
+template __global__ void qinc_kernel<16, true>(const __grid_constant__ QParams);
 
 } // namespace fwbf

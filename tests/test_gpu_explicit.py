@@ -146,3 +146,45 @@ def test_qc_kernel_quantised_ties(cuda_device, monkeypatch, quant, p, alpha):
     z, its, fl, ft = COracle(h).decode_batch(y.cpu().numpy()[:96], algorithm="fwbf", alpha=alpha, k_max=25, p=p)
     assert np.array_equal(a.iterations.cpu().numpy()[:96], its)
     assert np.array_equal(a.z()[:96], z)
+
+
+# ---- incremental quasi-cyclic kernel (qinc_kernel): stored metric keys, only
+# the columns of toggled checks recomputed ----
+
+@pytest.mark.parametrize("code,p,stall", [
+    ("qc4x32", 256, "flip-global-max"), ("r2x40z32", 32, "flip-global-max"),
+    ("r3x36z64a", 64, "terminate"), ("r4x12z32a", 32, "flip-global-max")])
+def test_qc_incremental_kernel_equals_full_pass(cuda_device, monkeypatch, code, p, stall):
+    """The incremental kernel against the full-pass QC kernel (FWBF_NO_QCINC)
+    and the oracle, on batches that also hold frames it must decide exactly
+    everywhere (non-finite y), all-zero frames and quantised frames (equal
+    keys); codes wider than 32 block columns take the second update loop."""
+    import torch
+    from paper_1206_3362_b200 import _native as nat
+    if code == "qc4x32":
+        h = build_code(code)
+    else:
+        jb, rest = code[1:].split("x")
+        kb, zz = rest.split("z")
+        h = _qc_code(len(code) + p, int(jb), int(kb), int(zz.rstrip("a")), zz.endswith("a"))
+    big = h.n_cols > 4000
+    frames = 192 if big else 1500
+    y = _y(h, frames, 5.0 if big else 3.5, 0.8 if big else 0.6, 3 * p + 1, pad=True)
+    y[5, 7] = float("nan")
+    y[6, 11] = float("inf")
+    y[7, 3] = float("-inf")
+    y[8, :] = 0.0
+    y[9:40] = torch.round(y[9:40] * 2) / 2                 # many equal metrics
+    cfg = DecoderConfig(block_len_p=p, k_max=30, stall_policy=stall, alpha=0.3)
+    a = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+    assert nat.last_kernel() == "qinc"
+    monkeypatch.setenv("FWBF_NO_QCINC", "1")
+    b = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+    assert nat.last_kernel() == "qdecode"
+    _same(a, b)
+    assert a.flip_logs() == b.flip_logs()
+    sel = [i for i in range(64) if i not in (5, 6, 7)]    # finite frames against the oracle
+    z, its, fl, ft = COracle(h).decode_batch(y.cpu().numpy()[sel], algorithm="fwbf", alpha=0.3, k_max=30, p=p,
+                                             stall=stall)
+    assert np.array_equal(a.iterations.cpu().numpy()[sel], its)
+    assert np.array_equal(a.z()[sel], z)
