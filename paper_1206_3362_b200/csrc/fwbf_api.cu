@@ -837,6 +837,7 @@ static int launch_qc(fwbf_code *c, const fwbf_params *p, const float *y, long lo
     P.off_blkk = take(P.nb * 4);
     P.off_blkf = take(P.nb * 4);
     P.off_list = take(std::min(c->m, P.jb * (P.nb + 1)) * 4);
+    P.off_dirty = take(3 * P.nb * 4);          // dirty flags [nb], two dirty lists [nb]
     P.off_misc = take(16 * 4);
   } else {
     P.off_y = take(c->n * 4);

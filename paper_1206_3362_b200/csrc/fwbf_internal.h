@@ -214,7 +214,7 @@ struct QParams {
   int kmax, stall, wmode;
   double alpha;
   int off_y, off_m1, off_m2, off_cmask, off_zrec, off_sbits, off_zbits, off_blkv, off_blki, off_misc;
-  int off_blkk, off_blkf, off_list, off_sold; // qinc_kernel only: block keys, flip flags, toggled checks, previous syndrome
+  int off_blkk, off_blkf, off_list, off_sold, off_dirty; // qinc_kernel only: block keys, flip flags, toggled checks, previous syndrome
   const float *y;
   long long ld;
   long long batch;

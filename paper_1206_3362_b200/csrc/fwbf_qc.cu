@@ -481,9 +481,11 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
   uint32_t *blk_k = reinterpret_cast<uint32_t *>(sm + P.off_blkk); // block maximum key (~0: decided exactly)
   int *blk_f = reinterpret_cast<int *>(sm + P.off_blkf);         // 1 = the block flipped (flip log only)
   int *tlist = reinterpret_cast<int *>(sm + P.off_list);         // toggled checks of this iteration
+  int *dirty = reinterpret_cast<int *>(sm + P.off_dirty);        // [nb] 1 = the block is rescanned next selection
+  int *dlist = dirty + P.nb;                                     // [2][nb] the dirty blocks, by iteration parity
   int *misc = reinterpret_cast<int *>(sm + P.off_misc);
   // counters used in alternate iterations come in pairs (slot = iteration parity)
-  enum { Q_FRAME = 0, Q_BE, Q_SWT = 2, Q_F = 4, Q_L = 6 };
+  enum { Q_FRAME = 0, Q_BE, Q_SWT = 2, Q_F = 4, Q_L = 6, Q_D = 8 };
   const bool imw = P.wmode == FWBF_WEIGHTS_IMWBF;
   const int zw = (N + 31) >> 5, mw = (M + 31) >> 5, nKm = (M + T - 1) / T;
   QView V;
@@ -523,7 +525,7 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
       }
     }
     for (int w = tid; w < (N + 3) >> 2; w += T) reinterpret_cast<uint32_t *>(cmask)[w] = 0u;
-    if (tid >= 1 && tid < 8) misc[tid] = 0; // not Q_FRAME: other warps may still be reading it
+    if (tid >= 1 && tid < 10) misc[tid] = 0; // not Q_FRAME: other warps may still be reading it
     nonfin = __syncthreads_or(nonfin);
     for (int w0 = warp * 32; w0 < N; w0 += T) {
       const int n = w0 + lane;
@@ -567,6 +569,8 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
     __syncthreads();
     // ---- init 3: every column's metric; the key replaces y in the column's own slot ----
     for (int n = tid; n < N; n += T) keys[n] = qfkey((float)qexact<ALLP>(V, n, ys[n]) + 0.0f);
+    for (int b = tid; b < P.nb; b += T) { dirty[b] = 1; dlist[b] = b; } // every block is scanned first
+    if (tid == 0) misc[Q_D] = P.nb;
     __syncthreads();
 
     // ---- iterations ----
@@ -579,8 +583,15 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
       if (k >= P.kmax) break;
       // the slots of the next iteration are cleared now (last read before the barrier behind us)
       if (tid == 0) { misc[Q_SWT + 1 - par] = 0; misc[Q_F + 1 - par] = 0; misc[Q_L + 1 - par] = 0; }
-      // selection: warp w owns blocks w, w + nwarps, ...
-      for (int b = warp; b < P.nb; b += nwarps) {
+      // Selection over the dirty blocks only.  A clean block's largest key is
+      // cached in blk_k and is below the key of 0 (a block that flips or was
+      // decided exactly stays dirty), so it selects nothing; it turns dirty
+      // when an update raises a column to its maximum or changes the holder.
+      const int nd = misc[Q_D + par];
+      const int *dl = dlist + par * P.nb;
+      int *dn = dlist + (1 - par) * P.nb;
+      for (int e = warp; e < nd; e += nwarps) {
+        const int b = dl[e];
         const int base0 = b * TPC * 32;
         uint32_t kk[TPC];
         qload_keys<TPC>(keys, base0, lane, kk);
@@ -618,6 +629,8 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
         if (lane == 0) {
           blk_k[b] = amb ? 0xffffffffu : Mk;
           if (P.fliplog) blk_f[b] = pos ? 1 : 0;
+          if (amb || pos) dn[atomicAdd(&misc[Q_D + 1 - par], 1)] = b; // stays dirty
+          else dirty[b] = 0;
         }
         if (pos) { // decoders.py:181-183: the warp applies its block's flip
           if (lane == 0) {
@@ -679,6 +692,7 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
               atomicXor(&zbits[gi >> 5], 1u << (gi & 31));
               blk_f[bg] = 1; // logged below as the single flip
               blk_i[bg] = gi;
+              if (atomicExch(&dirty[bg], 1) == 0) dn[atomicAdd(&misc[Q_D + 1 - par], 1)] = bg; // rescan: resets blk_f
             }
             if (lane < P.jb) {
               const int cbv = gi >> lgz, o = gi & (Z - 1), s = sh[lane * P.kb + cbv];
@@ -726,9 +740,11 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
               if (v2 > gv || (v2 == gv && i2 < gi)) { gv = v2; gi = i2; }
             }
             if (lane == 0) {
+              const int bg2 = gi / (TPC * 32);
               atomicXor(&zbits[gi >> 5], 1u << (gi & 31));
-              blk_f[gi / (TPC * 32)] = 1; // logged below as the single flip
-              blk_i[gi / (TPC * 32)] = gi;
+              blk_f[bg2] = 1; // logged below as the single flip
+              blk_i[bg2] = gi;
+              if (atomicExch(&dirty[bg2], 1) == 0) dn[atomicAdd(&misc[Q_D + 1 - par], 1)] = bg2; // rescan: resets blk_f
             }
             if (lane < P.jb) {
               const int cbv = gi >> lgz, o = gi & (Z - 1), s = sh[lane * P.kb + cbv];
@@ -758,6 +774,7 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
       // refresh, one syndrome word per thread: negate the records of the
       // checks whose bit changed since the records were last brought in line,
       // list them, add up the syndrome weight
+      if (tid == T - 1) misc[Q_D + par] = 0; // consumed by this iteration's selection; refilled from the next one on
       if (tid < ((mw + 31) & ~31)) {
         uint32_t word = 0, tog = 0;
         if (tid < mw) {
@@ -783,6 +800,18 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
       // update: the columns of every toggled check, from scratch
       {
         const int L = misc[Q_L + par];
+        // store a recomputed key; a clean block turns dirty when the column
+        // reaches the cached maximum or was its holder (old key = maximum)
+        auto qput = [&](int c, uint32_t nk) {
+          const uint32_t ok = keys[c];
+          if (nk == ok) return;
+          keys[c] = nk;
+          const int b = c / (TPC * 32);
+          if (dirty[b] == 0) {
+            const uint32_t bk = blk_k[b];
+            if ((nk >= bk || ok == bk) && atomicExch(&dirty[b], 1) == 0) dn[atomicAdd(&misc[Q_D + 1 - par], 1)] = b;
+          }
+        };
         for (int e0 = warp; e0 < L; e0 += 4 * nwarps) {
           int cc[4];
           float yy[4];
@@ -802,7 +831,7 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            if (cc[u] >= 0) keys[cc[u]] = qfkey((float)qexact<ALLP>(V, cc[u], yy[u] + 0.0f) + 0.0f);
+            if (cc[u] >= 0) qput(cc[u], qfkey((float)qexact<ALLP>(V, cc[u], yy[u] + 0.0f) + 0.0f));
         }
         for (int cb = 32 + lane; cb < P.kb; cb += 32) // block columns past the first 32 (wide codes)
           for (int e = warp; e < L; e += nwarps) {
@@ -810,7 +839,7 @@ __global__ void __launch_bounds__(512, 2) qinc_kernel(const __grid_constant__ QP
             const int s = sh[r * P.kb + cb];
             if (s >= 0) {
               const int c = cb * Z + ((i + s) & (Z - 1));
-              keys[c] = qfkey((float)qexact<ALLP>(V, c, __ldg(yr + c) + 0.0f) + 0.0f);
+              qput(c, qfkey((float)qexact<ALLP>(V, c, __ldg(yr + c) + 0.0f) + 0.0f));
             }
           }
       }
