@@ -390,7 +390,17 @@ def main():
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         te = float(tt.item())
+        # what the PCIe link alone allows: the same pinned buffer copied to the device, nothing else running
+        torch.cuda.synchronize()
+        pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        pe0.record()
+        y.copy_(yh, non_blocking=True)
+        pe1.record()
+        torch.cuda.synchronize()
+        h2d_gbs = B * ld * 4 / (pe0.elapsed_time(pe1) / 1e3) / 1e9
         e2e = {"value": world * B * a.steps * kinfo / te / 1e9, "unit": "Gbit/s",
+               "h2d_link_GBps": h2d_gbs,
+               "h2d_link_bound": world * h2d_gbs * 1e9 / (ld * 4) * kinfo / 1e9,
                "h2d_bytes_per_step": B * ld * 4,
                "d2h_bytes_per_step": B * (zw * 4 + 4 + 1) + nat.NCOUNTERS * 8,
                "path": "fwbf_decode_host_f32 (pinned host y; chunked H2D / decode / D2H on 3 streams ordered by events)",
