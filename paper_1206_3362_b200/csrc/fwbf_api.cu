@@ -28,7 +28,7 @@ template <typename YT>
 __global__ void noise_kernel(unsigned long long seed, long long first, long long count, double sigma,
                              const uint32_t *codeword, YT *y, long long ld, int n, int pm);
 template <int DV> __global__ void xdecode_kernel(const __grid_constant__ XParams P);
-template <int KC, int TB, int WT, int NN, int PB> __global__ void cdecode_kernel(const __grid_constant__ KParams P);
+template <int KC, int TB, int WT, int NN, int PB, bool Q16> __global__ void cdecode_kernel(const __grid_constant__ KParams P);
 template <int TPC> __global__ void qdecode_kernel(const __grid_constant__ QParams P);
 template <int TPC, bool ALLP> __global__ void qinc_kernel(const __grid_constant__ QParams P);
 template <typename T> __global__ void stage_hard_decision(const T *, long long, uint8_t *);
@@ -143,6 +143,11 @@ extern "C" int fwbf_abi_version(void) { return FWBF_ABI_VERSION; }
 extern "C" const char *fwbf_last_error(void) { return g_err.c_str(); }
 
 static thread_local const char *g_last_kernel = "";
+// the 16-bit quantised gather of the filtered circulant kernel: FWBF_Q16=1/0 (experiment switch)
+static bool q16_enabled() {
+  const char *e = getenv("FWBF_Q16");
+  return e ? atoi(e) != 0 : false;
+}
 extern "C" const char *fwbf_last_kernel(void) { return g_last_kernel; }
 
 extern "C" int fwbf_device_count(void) {
@@ -1108,11 +1113,19 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
 #define FWBF_PICK_C(KC_, TB_, WT_, NN_, PB_)                                                        \
     if (kc == KC_ && T == TB_ && kwt == WT_ && c->n == NN_ &&                                      \
         (cmlp ? PB_ < 0 : (PB_ == 0 || PB_ == p->block_len_p)) && !(PB_ == 0 && ckern)) {          \
-      ckern = (const void *)fwbf::cdecode_kernel<KC_, TB_, WT_, NN_, PB_>;                          \
+      ckern = (const void *)fwbf::cdecode_kernel<KC_, TB_, WT_, NN_, PB_, false>;                   \
       clayout = layout_c<KC_, TB_, WT_, NN_, PB_>;                                                  \
     }
     FWBF_CIRC_CONFIGS(FWBF_PICK_C)
 #undef FWBF_PICK_C
+    // the 16-bit quantised gather (Q16) where it is compiled (same layout)
+    if (ckern && !cmlp && q16_enabled()) {
+#define FWBF_PICK_C16(KC_, TB_, WT_, NN_, PB_)                                                      \
+      if (kc == KC_ && T == TB_ && kwt == WT_ && c->n == NN_ && PB_ == p->block_len_p)              \
+        ckern = (const void *)fwbf::cdecode_kernel<KC_, TB_, WT_, NN_, PB_, true>;
+      FWBF_CIRC16_CONFIGS(FWBF_PICK_C16)
+#undef FWBF_PICK_C16
+    }
   }
   const bool compact = circ && sizeof(YT) == 4 && c->w <= 32 && !getenv("FWBF_NO_COMPACT");
   // staged input rows (TMA bulk copy one frame ahead): compile-time-shape
@@ -1225,6 +1238,8 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     for (int j = 0; j < c->w; ++j) {
       const int d = c->n - c->off[j];
       Q.uoff[j] = ((d & 1) ? Q.off_fb + 4 : Q.off_fa) + 4 * d;
+      // Q16: int16 arrays QA (doubled) and QB (shifted one element) share the FB region
+      Q.uoff16[j] = (d & 1) ? Q.off_fb + (Q.off_m2s - Q.off_fb) / 2 + 2 * (d + 1) : Q.off_fb + 2 * d;
       const int cj = c->off[j]; // check scan: keys of columns (m + c_j, m + 1 + c_j), m even
       Q.soff[j] = (cj & 1) ? Q.off_fb + 4 * (cj + 1) : Q.off_fa + 4 * cj;
     }

@@ -54,6 +54,12 @@ __device__ __forceinline__ float fkey_val(uint32_t k) {
   return __uint_as_float((k >> 31) ? (k & 0x7fffffffu) : ~k);
 }
 
+// Q16: the frame's 16-bit grid step for signed minima up to vmax: every
+// |v| / G16 rounds to at most 32766 (vmax = 0: any step, every value is 0)
+__device__ __forceinline__ float q16_grid(float vmax) {
+  return vmax > 0.f ? __fmul_ru(vmax, 3.0520e-5f) : 1.0f; // 1 / 32766 = 3.05194e-5, rounded up
+}
+
 // One FWBF block decision, warp-wide (decoders.py:156-167, :181-183): lanes
 // scan the block's columns (SHORT: one column per lane, p <= 32), REDUX gives
 // the maximum key and the first index holding it, and the filter band decides
@@ -293,7 +299,7 @@ __device__ void mlp_decide(const KParams &P, const float *Efl, const float *sFA,
   }
 }
 
-template <int KC, int TB, int WT, int NN, int PB>
+template <int KC, int TB, int WT, int NN, int PB, bool Q16>
 __global__ void __launch_bounds__(TB, CircShape<TB, PB>::kMinBlocks)
 cdecode_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -313,6 +319,10 @@ cdecode_kernel(const __grid_constant__ KParams P) {
   float *yabs = Efl + L::EP;                                  // |y_n| (exact, float)
   float *sFA = reinterpret_cast<float *>(smem_raw + L::FA);   // signed min1, doubled
   float *sFB = reinterpret_cast<float *>(smem_raw + L::FB);   // the same, shifted one element
+  // Q16: after frame init the FB region holds the minima quantised to signed
+  // 16 bits instead -- QA doubled over [0, 2N), QB the same shifted one element
+  int16_t *sQA = reinterpret_cast<int16_t *>(smem_raw + L::FB);
+  int16_t *sQB = sQA + L::DBLF;
   float *sM2 = reinterpret_cast<float *>(smem_raw + L::M2);   // min2 per check
   uint16_t *sA2 = reinterpret_cast<uint16_t *>(smem_raw + L::A2); // argmin column per check
   int *sCorr = reinterpret_cast<int *>(smem_raw + L::CORR);   // coarse argmin correction per column
@@ -565,9 +575,11 @@ cdecode_kernel(const __grid_constant__ KParams P) {
             wmax = fmaxf(wmax, min1);
             const float s1v = par ? min1 : -min1;
             sFA[m] = s1v;
-            sFA[m + N] = s1v;
-            sFB[m + 1] = s1v;
-            sFB[m + N + 1] = s1v;
+            if constexpr (!Q16) {
+              sFA[m + N] = s1v;
+              sFB[m + 1] = s1v;
+              sFB[m + N + 1] = s1v;
+            }
             const int Dc = coarse_dc(sM2[m], min1, invGf);
             atomicAdd(&sCorr[sA2[m]], par ? Dc : -Dc);
           }
@@ -593,8 +605,31 @@ cdecode_kernel(const __grid_constant__ KParams P) {
       const double fdelta = ldexp(vmax * (0.5 * (double)WT * (double)(WT + 1)) * 1.001, -24) +
                             ldexp(((double)WT + P.alpha + 1.0) * ymax, -22) + 0.5 * (double)WT * (double)Gf +
                             ldexp((double)WT * ymax, -23);
-      fdp = __double2float_ru(fdelta);
-      fd2 = __double2float_ru(2.0 * fdelta + ldexp(((double)WT + P.alpha + 1.0) * ymax, -22));
+      double fd = fdelta;
+      if constexpr (Q16) // the quantisation: W values, each within 0.504 G16 of its grid point (rounding of v / G16 included)
+        fd += (double)WT * 0.505 * (double)q16_grid(__int_as_float(misc[S_VMAX]));
+      fdp = __double2float_ru(fd);
+      fd2 = __double2float_ru(2.0 * fd + ldexp(((double)WT + P.alpha + 1.0) * ymax, -22));
+    }
+    float G16 = 0.f, invG16 = 0.f;
+    if constexpr (Q16) {
+      // the signed minima on the frame's 16-bit grid (|q| <= 32766), into the
+      // dead shifted-copy region; a toggle later stores the negated value's
+      // grid point, which is the negated grid point
+      G16 = q16_grid(__int_as_float(misc[S_VMAX]));
+      invG16 = __frcp_rn(G16);
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        const int m = tid + kk * TB;
+        if (m < N) {
+          const int16_t q = (int16_t)__float2int_rn(__fmul_rn(sFA[m], invG16));
+          sQA[m] = q;
+          sQA[m + N] = q;
+          sQB[m + 1] = q;
+          sQB[m + N + 1] = q;
+        }
+      }
+      __syncthreads();
     }
 
     // ---------------- iterations (decoders.py:204-229) -------------------------
@@ -610,11 +645,23 @@ cdecode_kernel(const __grid_constant__ KParams P) {
       // min1, one FADD2 sums them
       {
         unsigned long long hs[NP];
+        if constexpr (Q16) {
+          int qlo[NP], qhi[NP];
 #pragma unroll
-        for (int qp = 0; qp < NP; ++qp) hs[qp] = 0ull;
-        const uint32_t baseT = s0 + 8u * (uint32_t)tid;
+          for (int qp = 0; qp < NP; ++qp) { qlo[qp] = 0; qhi[qp] = 0; }
+          const uint32_t baseQ = s0 + 4u * (uint32_t)tid;
 #pragma unroll
-        for (int j = 0; j < WT; ++j) GatherF2<0, NP, TB>::run(hs, baseT + (uint32_t)P.uoff[j]);
+          for (int j = 0; j < WT; ++j) GatherQ16<0, NP, TB>::run(qlo, qhi, baseQ + (uint32_t)P.uoff16[j]);
+#pragma unroll
+          for (int qp = 0; qp < NP; ++qp)
+            hs[qp] = f2pack(__fmul_rn((float)qlo[qp], G16), __fmul_rn((float)qhi[qp], G16));
+        } else {
+#pragma unroll
+          for (int qp = 0; qp < NP; ++qp) hs[qp] = 0ull;
+          const uint32_t baseT = s0 + 8u * (uint32_t)tid;
+#pragma unroll
+          for (int j = 0; j < WT; ++j) GatherF2<0, NP, TB>::run(hs, baseT + (uint32_t)P.uoff[j]);
+        }
 #pragma unroll
         for (int qp = 0; qp < NP; ++qp) {
           const float2 h = f2unpack(hs[qp]);
@@ -855,9 +902,17 @@ cdecode_kernel(const __grid_constant__ KParams P) {
             const int m = tid + kk * TB;
             const float v = -rv1[kk];
             sFA[m] = v;
-            sFA[m + N] = v;
-            sFB[m + 1] = v;
-            sFB[m + N + 1] = v;
+            if constexpr (Q16) {
+              const int16_t q = (int16_t)__float2int_rn(__fmul_rn(v, invG16));
+              sQA[m] = q;
+              sQA[m + N] = q;
+              sQB[m + 1] = q;
+              sQB[m + N + 1] = q;
+            } else {
+              sFA[m + N] = v;
+              sFB[m + 1] = v;
+              sFB[m + N + 1] = v;
+            }
             const int dc = coarse_dc(rm2[kk], fabsf(v), invGf);
             atomicAdd(&sCorr[ra2[kk]], signbit(v) ? -2 * dc : 2 * dc);
           }
@@ -905,7 +960,9 @@ cdecode_kernel(const __grid_constant__ KParams P) {
     atomicAdd((unsigned long long *)P.counters + tid, ctr[tid]);
 }
 
-#define FWBF_INST_CIRC(KC, TB, WT, NN, PB) template __global__ void cdecode_kernel<KC, TB, WT, NN, PB>(const __grid_constant__ KParams);
+#define FWBF_INST_CIRC(KC, TB, WT, NN, PB) template __global__ void cdecode_kernel<KC, TB, WT, NN, PB, false>(const __grid_constant__ KParams);
 FWBF_CIRC_CONFIGS(FWBF_INST_CIRC)
+#define FWBF_INST_CIRC16(KC, TB, WT, NN, PB) template __global__ void cdecode_kernel<KC, TB, WT, NN, PB, true>(const __grid_constant__ KParams);
+FWBF_CIRC16_CONFIGS(FWBF_INST_CIRC16)
 
 } // namespace fwbf

@@ -89,6 +89,22 @@ template <int QP, int NP, int TB> struct GatherF2<QP, NP, TB, false> {
   static __device__ __forceinline__ void run(unsigned long long (&)[NP], uint32_t) {}
 };
 
+// 16-bit gather step (fwbf_circ.cu, Q16): one 4-byte load brings the signed
+// 16-bit quantised minima of a column pair; two IDP.2A add the halves to the
+// pair's 32-bit sums (exact integer arithmetic, no carries between halves).
+template <int QP, int NP, int TB, bool GO = (QP < NP)> struct GatherQ16 {
+  static __device__ __forceinline__ void run(int (&lo)[NP], int (&hi)[NP], uint32_t a) {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(QP * TB * 4));
+    lo[QP] = __dp2a_lo(v, 0x00000001, lo[QP]);
+    hi[QP] = __dp2a_lo(v, 0x00000100, hi[QP]);
+    GatherQ16<QP + 1, NP, TB>::run(lo, hi, a);
+  }
+};
+template <int QP, int NP, int TB> struct GatherQ16<QP, NP, TB, false> {
+  static __device__ __forceinline__ void run(int (&)[NP], int (&)[NP], uint32_t) {}
+};
+
 // MODE 2 coarse argmin correction of a check, in units of the frame's grid G:
 // a deterministic function of the check's float32 minima (init and every
 // refresh compute the same value), within G/2 + 2^-23 max|y| of min2 - min1.
@@ -146,10 +162,10 @@ __device__ __forceinline__ double exact_split_metric(const KParams &P, const flo
   long long corr = 0;
   const bool imw = P.wmode == FWBF_WEIGHTS_IMWBF;
   for (int j = 0; j < W; ++j) {
-    const int d = n + N - P.off[j]; // doubled copy: check (n - c_j) mod N
-    const float v = sFA[d];
-    acc = __dadd_rn(acc, (double)v);
+    const int d = n + N - P.off[j]; // check (n - c_j) mod N, read from the first copy
     const int m = d >= N ? d - N : d;
+    const float v = sFA[m];
+    acc = __dadd_rn(acc, (double)v);
     if (imw && sA2[m] == n) {
       const long long D = (long long)__dmul_rn(__dsub_rn((double)sMin2[m], (double)fabsf(v)), qinv); // exact
       corr += signbit(v) ? -D : D;

@@ -48,6 +48,9 @@ constexpr int kMaxQcBlocks = 256;  // quasi-cyclic shift table entries in the pa
   X(2, 128, 16, 255, -1)     \
   X(4, 256, 32, 1023, -1)    \
   X(4, 1024, 64, 4095, -1)
+// the same kernel with the 16-bit quantised gather (Q16)
+#define FWBF_CIRC16_CONFIGS(X) \
+  X(4, 256, 32, 1023, 31)
 constexpr int kCircMaxLam = 31; // MLP lists: lambda + 1 <= 32 entries per warp
 
 // FWBF on EG(1023) (256 threads) runs 6 CTAs per SM at 40 registers without
@@ -163,6 +166,7 @@ struct KParams {
   unsigned *defer_count;
   const int *frame_list;
   const unsigned *frame_count;
+  int uoff16[kMaxCircWeight]; // fwbf_circ.cu Q16 gather: byte offset of the int16 pair of check (n - c_j), n even, minus 2n
   int soff[kMaxCircWeight]; // fwbf_circ.cu check scan: byte offset of the key pair of column m + c_j (m even), minus 4m
   int off_fd;  // fwbf_circ.cu: two doubled flip bitmaps (iteration parity)
   int fd_words; // words per flip bitmap
