@@ -438,10 +438,14 @@ def main():
         ev_rate = edge_visits / (launch_ms / 1e3)
         dadd_peak = sms * 64 * max_mhz * 1e6
         smem_peak = sms * 128 * max_mhz * 1e6
-        # filtered gather (FWBF on split-path frames): one 8-byte LDS brings the
-        # float32 signed weights of two columns, one FADD2 adds them -- 4 B of
-        # shared memory per edge visit, so 128 B/clk/SM caps it at 32 visits/clk/SM
-        gather_bound = sms * 32.0 * max_mhz * 1e6
+        # filtered gather (FWBF on split-path frames).  Q16 (the default): one
+        # 4-byte LDS brings the int16 quantised signed minima of two columns, two
+        # IDP.2A add them -- 2 B of shared memory per edge visit, so 128 B/clk/SM
+        # caps the gather at 64 visits/clk/SM.  FWBF_Q16=0: the float32 gather
+        # (8-byte LDS + FADD2), 4 B per edge visit, 32 visits/clk/SM.
+        q16 = os.environ.get("FWBF_Q16", "1") != "0"
+        gather_bytes = 2 if q16 else 4
+        gather_bound = sms * (128.0 / gather_bytes) * max_mhz * 1e6
         block_decisions = B * a.steps * ((n + a.p - 1) // a.p) * mean_iters
         line = {
             "metric": "FWBF decoded info Gbit/s", "value": value, "unit": "Gbit/s",
@@ -470,10 +474,14 @@ def main():
                          "ncu_source": trf.get("ncu_source"),
                          "clock_mhz_for_peaks": max_mhz,
                          "gather_bound": {
-                             "resource": "shared memory: filtered metric gather (one 8-byte LDS + one FADD2 "
-                                         "per two edge visits; 4 B/edge at 128 B/clk/SM = 32 edge visits/clk/SM)",
+                             "resource": ("shared memory: filtered metric gather, int16 quantised minima (one 4-byte "
+                                          "LDS + two IDP.2A per two edge visits; 2 B/edge at 128 B/clk/SM = 64 edge "
+                                          "visits/clk/SM)") if q16 else
+                                         ("shared memory: filtered metric gather (one 8-byte LDS + one FADD2 "
+                                          "per two edge visits; 4 B/edge at 128 B/clk/SM = 32 edge visits/clk/SM)"),
                              "peak": gather_bound, "frac": ev_rate / gather_bound,
-                             "smem_bytes_per_s_at_4B_per_edge": 4 * ev_rate,
+                             "smem_gather_bytes_per_edge": gather_bytes,
+                             "smem_gather_bytes_per_s": gather_bytes * ev_rate,
                              "smem_peak_GBps": smem_peak / 1e9},
                          "filter": {"exact_block_decisions": fstats[0],
                                     "exact_fraction": fstats[0] / max(1.0, block_decisions),

@@ -143,10 +143,11 @@ extern "C" int fwbf_abi_version(void) { return FWBF_ABI_VERSION; }
 extern "C" const char *fwbf_last_error(void) { return g_err.c_str(); }
 
 static thread_local const char *g_last_kernel = "";
-// the 16-bit quantised gather of the filtered circulant kernel: FWBF_Q16=1/0 (experiment switch)
+// the filtered circulant kernel gathers 16-bit quantised minima (Q16) unless
+// FWBF_Q16=0 asks for the float32 gather (A/B timing, parity tests of both)
 static bool q16_enabled() {
   const char *e = getenv("FWBF_Q16");
-  return e ? atoi(e) != 0 : false;
+  return e ? atoi(e) != 0 : true;
 }
 extern "C" const char *fwbf_last_kernel(void) { return g_last_kernel; }
 
@@ -1110,22 +1111,18 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
                     !getenv("FWBF_NO_FILTER") && !getenv("FWBF_NO_SPLIT");
   if ((mode2 || cmlp) && sizeof(YT) == 4 && kwt > 0 && c->m == c->n && p->weight_mode == FWBF_WEIGHTS_IMWBF &&
       (cmlp || p->block_len_p >= 16) && !P.force_ordered && !getenv("FWBF_NO_CDEC")) {
+    // 16-bit quantised gather (default for FWBF) or the float32 gather; MLP keeps the float32 one: its
+    // exact top-lambda over a wider band costs small batches more than the gather saves
+    const bool q16 = q16_enabled() && !cmlp;
 #define FWBF_PICK_C(KC_, TB_, WT_, NN_, PB_)                                                        \
     if (kc == KC_ && T == TB_ && kwt == WT_ && c->n == NN_ &&                                      \
         (cmlp ? PB_ < 0 : (PB_ == 0 || PB_ == p->block_len_p)) && !(PB_ == 0 && ckern)) {          \
-      ckern = (const void *)fwbf::cdecode_kernel<KC_, TB_, WT_, NN_, PB_, false>;                   \
+      ckern = q16 ? (const void *)fwbf::cdecode_kernel<KC_, TB_, WT_, NN_, PB_, true>                 \
+                  : (const void *)fwbf::cdecode_kernel<KC_, TB_, WT_, NN_, PB_, false>;               \
       clayout = layout_c<KC_, TB_, WT_, NN_, PB_>;                                                  \
     }
     FWBF_CIRC_CONFIGS(FWBF_PICK_C)
 #undef FWBF_PICK_C
-    // the 16-bit quantised gather (Q16) where it is compiled (same layout)
-    if (ckern && !cmlp && q16_enabled()) {
-#define FWBF_PICK_C16(KC_, TB_, WT_, NN_, PB_)                                                      \
-      if (kc == KC_ && T == TB_ && kwt == WT_ && c->n == NN_ && PB_ == p->block_len_p)              \
-        ckern = (const void *)fwbf::cdecode_kernel<KC_, TB_, WT_, NN_, PB_, true>;
-      FWBF_CIRC16_CONFIGS(FWBF_PICK_C16)
-#undef FWBF_PICK_C16
-    }
   }
   const bool compact = circ && sizeof(YT) == 4 && c->w <= 32 && !getenv("FWBF_NO_COMPACT");
   // staged input rows (TMA bulk copy one frame ahead): compile-time-shape

@@ -963,6 +963,6 @@ cdecode_kernel(const __grid_constant__ KParams P) {
 #define FWBF_INST_CIRC(KC, TB, WT, NN, PB) template __global__ void cdecode_kernel<KC, TB, WT, NN, PB, false>(const __grid_constant__ KParams);
 FWBF_CIRC_CONFIGS(FWBF_INST_CIRC)
 #define FWBF_INST_CIRC16(KC, TB, WT, NN, PB) template __global__ void cdecode_kernel<KC, TB, WT, NN, PB, true>(const __grid_constant__ KParams);
-FWBF_CIRC16_CONFIGS(FWBF_INST_CIRC16)
+FWBF_CIRC_CONFIGS(FWBF_INST_CIRC16)
 
 } // namespace fwbf

@@ -48,9 +48,6 @@ constexpr int kMaxQcBlocks = 256;  // quasi-cyclic shift table entries in the pa
   X(2, 128, 16, 255, -1)     \
   X(4, 256, 32, 1023, -1)    \
   X(4, 1024, 64, 4095, -1)
-// the same kernel with the 16-bit quantised gather (Q16)
-#define FWBF_CIRC16_CONFIGS(X) \
-  X(4, 256, 32, 1023, 31)
 constexpr int kCircMaxLam = 31; // MLP lists: lambda + 1 <= 32 entries per warp
 
 // FWBF on EG(1023) (256 threads) runs 6 CTAs per SM at 40 registers without

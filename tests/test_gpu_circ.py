@@ -7,7 +7,9 @@ and the oracle bit for bit: hard decisions, iterations, flags, flip counts
 and the flip sequence, for compiled-in and runtime block lengths, both stall
 policies, and batches that mix deferred frames in.  MLP-WBF (lambda <= 31)
 runs on the same kernel with a filtered top-lambda selection and must equal
-decode_kernel's exact MODE 0 and the oracle.
+decode_kernel's exact MODE 0 and the oracle.  Round 2, fourth session: the
+gather reads the minima quantised to 16 bits on a per-frame grid (Q16); the
+float32 gather remains as FWBF_Q16=0, and every case here runs on both.
 """
 
 import os
@@ -22,6 +24,16 @@ from paper_1206_3362_b200 import _native as nat
 from tests.golden.codebook import build_code, code_rate
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True, params=["q16", "f32"])
+def gather_variant(request, monkeypatch):
+    """Every case runs on both gathers of the kernel: the 16-bit quantised one
+    (the default) and the float32 one (FWBF_Q16=0); both must give the
+    reference's results bit for bit -- only the width of the filter band, and
+    so the number of exact re-decisions, differs."""
+    monkeypatch.setenv("FWBF_Q16", "1" if request.param == "q16" else "0")
+    return request.param
 
 
 def _frames(code, ebn0, frames, seed, quant=None):
@@ -131,6 +143,34 @@ def test_circ_kernel_defers_unguarded_frames(cuda_device):
     _same(a, b, "mixed batch")
     finite = np.array([i for i in range(y.shape[0]) if np.all(np.isfinite(y[i]))])
     _vs_oracle(a, h, y, cfg, "mixed batch", rows=finite[finite < 400])
+
+
+def test_circ_kernel_coarse_quantisation_grid(cuda_device):
+    """Frames whose largest check minimum is far above the others (every
+    column of one check, or of many, scaled up): the 16-bit grid is then
+    coarse for all the other minima, most block decisions fall inside the
+    widened band and are re-decided exactly -- results must not change."""
+    from paper_1206_3362_b200 import device_code
+    h, y = _frames("eg5", 4.0, 384, seed=41)
+    rows = h.row_adj
+    for i in range(0, 128):                       # one check's 32 columns x 2^10
+        y[i, list(rows[(7 * i) % h.n_rows])] *= np.float32(1024.0)
+    for i in range(128, 256):                     # a third of the columns x 2^6 (many large minima)
+        y[i, ::3] *= np.float32(64.0)
+    for i in range(256, 320):                     # tiny values next to ordinary ones
+        y[i, 1::2] *= np.float32(2.0 ** -12)
+    for mlp in (False, True):
+        cfg = DecoderConfig(lam=7, k_max=40) if mlp else DecoderConfig(block_len_p=31, k_max=60, alpha=0.2)
+        alg = "mlp" if mlp else "fwbf"
+        dc = device_code(h)
+        dc.filter_stats(reset=True)
+        a, ka = _decode(h, y, cfg, True, alg=alg)
+        st = dc.filter_stats(reset=True)
+        b, _ = _decode(h, y, cfg, False, alg=alg)
+        assert ka == "cdecode+decode_kernel"
+        _same(a, b, f"coarse grid {alg}", flag_mask=11 if mlp else 0xff)
+        _vs_oracle(a, h, y, cfg, f"coarse grid {alg}", alg=alg)
+        assert mlp or st[0] > 0                   # the exact path ran
 
 
 def test_circ_kernel_staged_rows(cuda_device):
