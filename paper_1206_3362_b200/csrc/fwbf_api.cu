@@ -28,6 +28,7 @@ template <typename YT>
 __global__ void noise_kernel(unsigned long long seed, long long first, long long count, double sigma,
                              const uint32_t *codeword, YT *y, long long ld, int n, int pm);
 template <int DV> __global__ void xdecode_kernel(const __grid_constant__ XParams P);
+template <int DV> __global__ void xinc_kernel(const __grid_constant__ XParams P);
 template <int KC, int TB, int WT, int NN, int PB, bool Q16> __global__ void cdecode_kernel(const __grid_constant__ KParams P);
 template <int TPC> __global__ void qdecode_kernel(const __grid_constant__ QParams P);
 template <int TPC, bool ALLP> __global__ void qinc_kernel(const __grid_constant__ QParams P);
@@ -93,6 +94,13 @@ struct XPlan {
   int off_tab = 0, off_cpos = 0;
   int wpc = 0, per_sm = 0, smem = 0; // warps per CTA, CTAs per SM, dynamic smem bytes
   bool ok = false;
+  // incremental variant (xinc_kernel): the base layout plus the check -> slots table after the CTA tables
+  // and the stored metrics + toggled-check list after each warp's region
+  bool inc_ok = false;
+  const void *inc_kern = nullptr;
+  uint16_t *d_ctab = nullptr;
+  int dcs_sh = 0, off_ctab = 0, inc_tables_bytes = 0, inc_warp_bytes = 0, wo_ek = 0, wo_tl = 0;
+  int inc_wpc = 0, inc_per_sm = 0, inc_smem = 0;
 };
 
 struct fwbf_code {
@@ -349,6 +357,7 @@ extern "C" int fwbf_code_destroy(fwbf_code *c) {
     cudaFree(x.d_rtab);
     cudaFree(x.d_cpos);
     cudaFree(x.d_invp);
+    cudaFree(x.d_ctab);
   }
   delete c;
   return FWBF_OK;
@@ -719,6 +728,43 @@ static int build_xplan(fwbf_code *c, int p, XPlan *out) {
     return rc;
   }
   x.ok = true;
+  // ---- incremental variant: per check label the slots of the check's columns ----
+  {
+    int dsh = 0;
+    while ((1 << dsh) < c->dc_max) ++dsh;
+    const long ctab_bytes = ((long)m << dsh) * 2;
+    if (c->dc_max >= 1 && dsh <= 5 && ctab_bytes <= 32 * 1024) {
+      std::vector<uint16_t> ctab((size_t)m << dsh, 0xffff);
+      for (int j = 0; j < m; ++j) {
+        const int chk = invp[j];
+        int q = 0;
+        for (int e = c->h_row_ptr[chk]; e < c->h_row_ptr[chk + 1]; ++e, ++q)
+          ctab[((size_t)j << dsh) + q] = cpos[c->h_row_idx[e]];
+      }
+      x.dcs_sh = dsh;
+      int o2 = x.tables_bytes;
+      x.off_ctab = o2;
+      o2 = align16(o2 + (int)ctab_bytes);
+      x.inc_tables_bytes = o2;
+      int w2 = x.warp_bytes;
+      x.wo_ek = w2;
+      w2 = align16(w2 + nslot * 4);
+      x.wo_tl = w2;
+      w2 = align16(w2 + (x.nb + 1) * x.dv * 2);
+      x.inc_warp_bytes = w2;
+      x.inc_kern = x.dv == 2 ? (const void *)fwbf::xinc_kernel<2>
+                   : x.dv == 3 ? (const void *)fwbf::xinc_kernel<3> : (const void *)fwbf::xinc_kernel<4>;
+      int bw = 0;
+      for (int wpc : {8, 4, 2, 1}) {
+        const int smem = x.inc_tables_bytes + wpc * x.inc_warp_bytes;
+        if (smem > c->smem_optin) continue;
+        int occ = 0;
+        if (plan_occupancy(c->device, x.inc_kern, 32 * wpc, smem, &occ)) return FWBF_ECUDA;
+        if (occ * wpc > bw) { bw = occ * wpc; x.inc_wpc = wpc; x.inc_per_sm = occ; x.inc_smem = smem; }
+      }
+      if (bw >= 8 && upload(&x.d_ctab, ctab) == FWBF_OK) x.inc_ok = true;
+    }
+  }
   *out = x;
   return FWBF_OK;
 }
@@ -748,8 +794,15 @@ static int launch_explicit(fwbf_code *c, const fwbf_params *p, const XPlan &x, c
   P.s2off = 1 << x.s2sh;
   P.off_tab = x.off_tab;
   P.off_cpos = x.off_cpos;
-  P.off_warp0 = x.tables_bytes;
-  P.warp_bytes = x.warp_bytes;
+  // the incremental kernel (stored metrics, only the columns of toggled checks recomputed) unless switched off
+  const bool inc = x.inc_ok && !getenv("FWBF_NO_XINC");
+  P.off_warp0 = inc ? x.inc_tables_bytes : x.tables_bytes;
+  P.warp_bytes = inc ? x.inc_warp_bytes : x.warp_bytes;
+  P.ctab = x.d_ctab;
+  P.off_ctab = x.off_ctab;
+  P.dcs_sh = x.dcs_sh;
+  P.wo_ek = x.wo_ek;
+  P.wo_tl = x.wo_tl;
   P.wo_rec = x.wo_rec;
   P.wo_ys = x.wo_ys;
   P.wo_am = x.wo_am;
@@ -776,11 +829,14 @@ static int launch_explicit(fwbf_code *c, const fwbf_params *p, const XPlan &x, c
   P.codeword_bits = o.codeword_bits;
   const unsigned slot = c->work_slot.fetch_add(1) % kWorkRing;
   P.work_counter = c->d_work + slot;
-  const long long grid = std::min<long long>((batch + x.wpc - 1) / x.wpc, (long long)x.per_sm * c->sm_count);
+  const int wpc = inc ? x.inc_wpc : x.wpc, per_sm = inc ? x.inc_per_sm : x.per_sm;
+  const long long grid = std::min<long long>((batch + wpc - 1) / wpc, (long long)per_sm * c->sm_count);
   CUDA_TRY(cudaMemsetAsync(P.work_counter, 0, sizeof(unsigned), stream));
   void *args[] = {&P};
-  CUDA_TRY(cudaLaunchKernel(x.kern, dim3((unsigned)grid), dim3(32 * x.wpc), args, x.smem, stream));
+  CUDA_TRY(cudaLaunchKernel(inc ? x.inc_kern : x.kern, dim3((unsigned)grid), dim3(32 * wpc), args,
+                            inc ? x.inc_smem : x.smem, stream));
   CUDA_TRY(cudaGetLastError());
+  g_last_kernel = inc ? "xinc" : "xdecode";
   return FWBF_OK;
 }
 
@@ -940,7 +996,6 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
     const XPlan *xp = get_xplan(c, p->block_len_p, &rc);
     if (rc) return rc;
     if (xp) {
-      g_last_kernel = "xdecode";
       return launch_explicit(c, p, *xp, (const float *)y, batch, ld, o, stream);
     }
   }

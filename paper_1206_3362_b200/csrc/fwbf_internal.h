@@ -184,6 +184,10 @@ struct XParams {
   int s2off, s2sh;               // min2 array offset in bytes (= 1 << s2sh) from the min1 array
   int off_tab, off_cpos, off_warp0, warp_bytes;
   int wo_rec, wo_ys, wo_am, wo_sb, wo_zw, wo_bf;
+  // xinc_kernel (incremental variant): per check label the slots of its columns [m << dcs_sh] (0xffff = none),
+  // per warp the stored metrics [nslot] floats and the toggled-check list
+  const uint16_t *ctab;
+  int off_ctab, dcs_sh, wo_ek, wo_tl;
   // input / outputs (as KParams)
   const float *y;
   long long ld;

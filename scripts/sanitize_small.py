@@ -12,7 +12,8 @@ from tests.golden.codebook import build_code, code_rate
 rng = np.random.default_rng(3)
 for code, p, kmax, db, frames, alg in (("eg5", 31, 30, 4.0, 40, "fwbf"), ("eg5", 93, 20, 4.0, 16, "fwbf"),
                                        ("eg4", 17, 20, 4.0, 16, "fwbf"), ("eg5", 31, 20, 4.0, 16, "mlp"),
-                                       ("qc4x32", 256, 12, 5.0, 6, "fwbf"), ("qc4x32", 64, 12, 5.5, 6, "fwbf")):
+                                       ("qc4x32", 256, 12, 5.0, 6, "fwbf"), ("qc4x32", 64, 12, 5.5, 6, "fwbf"),
+                                       ("gal504", 24, 30, 4.0, 40, "fwbf")):
     h = build_code(code)
     y = (1.0 + O.ebn0_to_sigma(db, code_rate(code)) * rng.standard_normal((frames, h.n_cols))).astype(np.float32)
     y[1] = np.round(y[1] * 2) / 2

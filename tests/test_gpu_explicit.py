@@ -33,13 +33,28 @@ def _same(a, b):
         assert torch.equal(getattr(a, name), getattr(b, name)), name
 
 
+@pytest.fixture(autouse=True, params=["xinc", "xdecode"])
+def warp_kernel_variant(request, monkeypatch):
+    """The warp-kernel cases run on both one-frame-per-warp kernels: the
+    incremental one (stored float32 roundings of the exact metrics, only the
+    columns of toggled checks recomputed; the default) and the full-pass one
+    (FWBF_NO_XINC=1).  The QC cases below ignore the switch."""
+    if request.param == "xdecode":
+        monkeypatch.setenv("FWBF_NO_XINC", "1")
+    return request.param
+
+
 @pytest.mark.parametrize("p", [1, 3, 7, 24, 32, 63, 96, 252, 504, 1000])
 @pytest.mark.parametrize("stall", ["flip-global-max", "terminate"])
-def test_warp_kernel_matches_cta_kernel_and_oracle(cuda_device, monkeypatch, p, stall):
+def test_warp_kernel_matches_cta_kernel_and_oracle(cuda_device, monkeypatch, warp_kernel_variant, p, stall):
+    from paper_1206_3362_b200 import _native as nat
     h = build_code("gal504")
     y = _y(h, 3000, 3.5, code_rate("gal504"), p, pad=(p % 2 == 0))
+    y[7] = (y[7] * 4).round() / 4                     # equal metrics: exact rounds / exact stall argmax
+    y[8] = 0.0
     cfg = DecoderConfig(block_len_p=p, k_max=50, stall_policy=stall)
     a = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+    assert nat.last_kernel() == warp_kernel_variant
     monkeypatch.setenv("FWBF_NO_WARP", "1")
     b = decode_batch(h, y, cfg, "fwbf", flip_log=True)
     _same(a, b)
@@ -87,6 +102,28 @@ def test_warp_kernel_dv4_and_columns_without_checks(cuda_device):
         for i in range(0, 300, 7):
             r = O.decode(g, y2[i], "fwbf", alpha=0.5, k_max=20, p=p)
             assert int(res.iterations[i]) == r.iterations and logs[i] == r.flip_log, (p, i)
+
+
+def test_warp_kernels_agree_on_special_frames(cuda_device, monkeypatch, warp_kernel_variant):
+    """Non-finite, all-zero and heavily quantised frames: both warp kernels
+    give what the CTA kernel gives (the incremental one decides such frames on
+    exact values everywhere)."""
+    import torch
+    h = build_code("gal504")
+    y = _y(h, 400, 4.0, code_rate("gal504"), 77, pad=True)
+    y[3, 5] = float("nan")
+    y[4, 100] = float("inf")
+    y[5, 200] = float("-inf")
+    y[6] = 0.0
+    y[10:200] = torch.round(y[10:200] * 2) / 2
+    for p, stall in ((24, "flip-global-max"), (24, "terminate"), (63, "flip-global-max")):
+        cfg = DecoderConfig(block_len_p=p, k_max=40, stall_policy=stall, alpha=0.5)
+        a = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+        monkeypatch.setenv("FWBF_NO_WARP", "1")
+        b = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+        monkeypatch.delenv("FWBF_NO_WARP")
+        _same(a, b)
+        assert a.flip_logs() == b.flip_logs()
 
 
 # ---- quasi-cyclic kernel (fwbf_qc.cu): config D's path ----
