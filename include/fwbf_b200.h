@@ -159,7 +159,8 @@ int fwbf_filter_stats(fwbf_code *code, int64_t *out, int32_t reset);
 
 /* Diagnostic: the decode kernel(s) the calling thread's last decode launched,
  * e.g. "cdecode+decode_kernel" (filtered circulant kernel, then the exact
- * kernel over the frames it deferred), "decode_kernel", "xdecode", "qinc"
+ * kernel over the frames it deferred), "decode_kernel", "xinc" / "xdecode"
+ * (incremental / full-pass one-frame-per-warp kernel), "qinc"
  * (incremental quasi-cyclic kernel), "qdecode" (full-pass quasi-cyclic kernel). */
 const char *fwbf_last_kernel(void);
 
