@@ -159,6 +159,10 @@ def test_circ_kernel_coarse_quantisation_grid(cuda_device):
         y[i, ::3] *= np.float32(64.0)
     for i in range(256, 320):                     # tiny values next to ordinary ones
         y[i, 1::2] *= np.float32(2.0 ** -12)
+    for i in range(320, 352):                     # a zero in every check: every minimum is 0 (vmax = 0)
+        y[i, ::2] = 0.0
+    for i in range(352, 384):                     # ... and in most checks
+        y[i, ::5] = 0.0
     for mlp in (False, True):
         cfg = DecoderConfig(lam=7, k_max=40) if mlp else DecoderConfig(block_len_p=31, k_max=60, alpha=0.2)
         alg = "mlp" if mlp else "fwbf"
