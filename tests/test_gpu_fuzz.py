@@ -82,3 +82,39 @@ def test_random_parity(cuda_device, seed):
         assert logs[i] == r.flip_log, (seed, i)
         assert np.array_equal(z[i], r.z), (seed, i)
         assert res.converged[i] == r.converged and res.stalled[i] == r.stalled
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("FWBF_FUZZ_QC_N", "48"))))
+def test_random_qc_parity(cuda_device, seed):
+    """Random quasi-cyclic codes (2-4 row blocks, 3-40 block columns, absent
+    blocks, Z = 32 / 64 / 128) with a block length the QC kernels accept
+    (32 | p, p | Z): the incremental QC kernel (float32 input) or the generic
+    path (float64 input) against the oracle, bit-exact, flip sequence included."""
+    from paper_1206_3362_b200.codes import qc_from_shifts
+    rng = np.random.default_rng(77000 + seed)
+    jb, kb = int(rng.integers(2, 5)), int(rng.integers(3, 41))
+    z = int(rng.choice([32, 64, 128]))
+    sh = rng.integers(0, z, size=(jb, kb))
+    if rng.integers(0, 2):
+        full = sh.copy()
+        sh[rng.random((jb, kb)) < 0.25] = -1
+        sh[0, :] = full[0, :]                         # every column keeps a check
+        for r in range(jb):                           # every check keeps at least two bits
+            if np.count_nonzero(sh[r] >= 0) < 2:
+                sh[r, :2] = full[r, :2]
+    h = qc_from_shifts(sh, z)
+    p = int(rng.choice([q for q in (32, 64, 128) if z % q == 0]))
+    cfg = DecoderConfig(alpha=float(rng.choice([0.0, 0.2, 0.7, 1.5])), k_max=int(rng.integers(1, 30)),
+                        block_len_p=p, stall_policy=["flip-global-max", "terminate"][int(rng.integers(0, 2))],
+                        weight_mode=["imwbf", "mwbf"][int(rng.integers(0, 2))])
+    y = random_y(rng, h.n_cols, int(rng.integers(1, 10)))
+    res = decode_batch(h, y, cfg, "fwbf", flip_log=True)
+    z_, its, logs = res.z(), res.iterations.cpu().numpy(), res.flip_logs()
+    g = O.Graph.of(h)
+    for i in range(y.shape[0]):
+        r = O.decode(g, y[i], "fwbf", alpha=cfg.alpha, k_max=cfg.k_max, p=p, stall=cfg.stall_policy,
+                     weight_mode=cfg.weight_mode)
+        assert its[i] == r.iterations, (seed, i)
+        assert logs[i] == r.flip_log, (seed, i)
+        assert np.array_equal(z_[i], r.z), (seed, i)
+        assert res.converged[i] == r.converged and res.stalled[i] == r.stalled
