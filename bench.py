@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--ref-1worker-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-chunk", type=int, default=1 << 17)
+    ap.add_argument("--e2e-chunk", type=int, default=1 << 14)
     return ap.parse_args()
 
 
@@ -403,7 +403,8 @@ def main():
                "h2d_link_bound": world * h2d_gbs * 1e9 / (ld * 4) * kinfo / 1e9,
                "h2d_bytes_per_step": B * ld * 4,
                "d2h_bytes_per_step": B * (zw * 4 + 4 + 1) + nat.NCOUNTERS * 8,
-               "path": "fwbf_decode_host_f32 (pinned host y; chunked H2D / decode / D2H on 3 streams ordered by events)",
+               "path": ("fwbf_decode_host_f32 (pinned host y; chunked H2D / decode / D2H on 5 streams ordered by events: "
+                        "consecutive chunks' decode kernels on alternating streams, so a chunk's drain overlaps the next chunk)"),
                "chunk_frames": a.e2e_chunk}
 
     if rank == 0:

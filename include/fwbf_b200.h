@@ -179,9 +179,11 @@ int fwbf_decode_awgn(fwbf_code *code, const fwbf_params *params, uint64_t seed,
 
 /* End-to-end call on HOST buffers: y_host [batch][ld] floats; outputs are host
  * arrays (any may be NULL; counters accumulated).  Copies are pipelined in
- * chunks of chunk_frames against decoding on two internal streams; pinned
- * host memory gives full overlap.  Synchronous: returns when results are in
- * host memory. */
+ * chunks of chunk_frames (<= 0: about 64 MB of y per chunk) against decoding
+ * on internal streams -- H2D, two alternating decode streams so that a
+ * chunk's last frames overlap the next chunk's first, D2H; four device chunk
+ * buffers; pinned host memory gives full overlap.  Synchronous: returns when
+ * results are in host memory. */
 int fwbf_decode_host_f32(fwbf_code *code, const fwbf_params *params, const float *y_host,
                          int64_t batch, int64_t ld, uint32_t *z_bits_host, int64_t z_ld,
                          int32_t *iterations_host, uint8_t *flags_host,

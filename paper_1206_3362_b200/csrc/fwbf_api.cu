@@ -126,9 +126,11 @@ struct fwbf_code {
   int smem_optin = 0;
   // host pipeline scratch
   std::mutex pipe_mu;
-  cudaStream_t pipe_s[3] = {nullptr, nullptr, nullptr}; // H2D copies, decodes, D2H copies
-  cudaEvent_t pipe_ev[3][2] = {};                         // [h2d done, decode done, d2h done][buffer]
-  void *pipe_buf[2] = {nullptr, nullptr};
+  // host pipeline (fwbf_decode_host_f32): H2D copies, two alternating decode streams, the
+  // deferred-frame launches (high priority), D2H copies; four chunk buffers
+  cudaStream_t pipe_s[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t pipe_ev[4][4] = {}; // [h2d done, main kernel done, decode done, d2h done][buffer]
+  void *pipe_buf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t pipe_bytes = 0;
   int64_t *pipe_counters = nullptr;
   void *noise_buf = nullptr;
@@ -339,12 +341,12 @@ extern "C" int fwbf_code_destroy(fwbf_code *c) {
   cudaFree(c->d_offpos);
   cudaFree(c->d_work);
   cudaFree(c->d_fstats);
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < 5; ++i)
     if (c->pipe_s[i]) cudaStreamDestroy(c->pipe_s[i]);
-    for (int b = 0; b < 2; ++b)
+  for (int i = 0; i < 4; ++i)
+    for (int b = 0; b < 4; ++b)
       if (c->pipe_ev[i][b]) cudaEventDestroy(c->pipe_ev[i][b]);
-  }
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 4; ++i)
     if (c->pipe_buf[i]) cudaFree(c->pipe_buf[i]);
   cudaFree(c->pipe_counters);
   cudaFree(c->noise_buf);
@@ -965,7 +967,12 @@ static const XPlan *get_xplan(fwbf_code *c, int p, int *rc) {
 template <typename YT>
 static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long long batch,
                          long long ld, const fwbf_outputs *out, cudaStream_t stream,
-                         double *metric_out = nullptr, long long metric_ld = 0) {
+                         double *metric_out = nullptr, long long metric_ld = 0,
+                         cudaStream_t dstream = nullptr, cudaEvent_t dev = nullptr) {
+  // dstream / dev (host pipeline): the second launch of a decode -- decode_kernel over the
+  // frames the filtered circulant kernel deferred -- goes on dstream, ordered after the first
+  // by dev, so the next chunk's main kernel (on another stream) can fill the SMs this one's
+  // last frames leave instead of waiting behind a launch that has almost nothing to do
   int rc = validate(c, p);
   if (rc) return rc;
   if (batch < 0) return fail(FWBF_EINVAL, "batch must be nonnegative");
@@ -1344,9 +1351,15 @@ static int launch_decode(fwbf_code *c, const fwbf_params *p, const YT *y, long l
       P.frame_count = dcount;
       P.work_counter = lwork;
       void *args[] = {&P};
-      CUDA_TRY(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(T), args, P.smem_bytes, stream));
+      cudaStream_t s2 = stream;
+      if (dstream && dev && dstream != stream) {
+        CUDA_TRY(cudaEventRecord(dev, stream));
+        CUDA_TRY(cudaStreamWaitEvent(dstream, dev, 0));
+        s2 = dstream;
+      }
+      CUDA_TRY(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(T), args, P.smem_bytes, s2));
       CUDA_TRY(cudaGetLastError());
-      CUDA_TRY(cudaFreeAsync(dlist, stream));
+      CUDA_TRY(cudaFreeAsync(dlist, s2));
       g_last_kernel = "cdecode+decode_kernel";
       return FWBF_OK;
     }
@@ -1539,82 +1552,95 @@ extern "C" int fwbf_decode_host_f32(fwbf_code *c, const fwbf_params *p, const fl
   if (ld < c->n) return fail(FWBF_EINVAL, "expected a length-%d frame (ld=%lld)", c->n, (long long)ld);
   const int zw = (c->n + 31) / 32;
   if (z_host && z_ld < zw) return fail(FWBF_EINVAL, "z_ld too small");
-  if (chunk <= 0) chunk = 65536;
+  // default chunk: about 64 MB of y per buffer (2^14 frames of EG(1023)): with the chunks' drains
+  // overlapped (below) small chunks cost nothing and shorten the pipeline's fill and flush
+  if (chunk <= 0) chunk = std::max<int64_t>(1024, (int64_t)(64 << 20) / (ld * (int64_t)sizeof(float)));
   chunk = std::min<int64_t>(chunk, batch);
   std::lock_guard<std::mutex> lock(c->pipe_mu);
   DeviceGuard dg;
   CUDA_TRY(cudaSetDevice(c->device));
-  // per-stream buffer: y chunk | z chunk | iterations | flags
+  // per-chunk buffer: y chunk | z chunk | iterations | flags
   const size_t yb = (size_t)chunk * ld * sizeof(float);
   const size_t zb = (size_t)chunk * zw * sizeof(uint32_t);
   const size_t ib = (size_t)chunk * sizeof(int32_t);
   const size_t fb = (size_t)chunk;
   const size_t need = align16((int)0) + yb + zb + ib + fb + 64;
+  constexpr int NBUF = 4;
   if (need > c->pipe_bytes) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NBUF; ++i) {
       if (c->pipe_buf[i]) cudaFree(c->pipe_buf[i]);
       c->pipe_buf[i] = nullptr;
     }
     c->pipe_bytes = 0;
-    for (int i = 0; i < 2; ++i) CUDA_TRY(cudaMalloc(&c->pipe_buf[i], need));
+    for (int i = 0; i < NBUF; ++i) CUDA_TRY(cudaMalloc(&c->pipe_buf[i], need));
     c->pipe_bytes = need;
   }
-  for (int i = 0; i < 3; ++i) {
-    if (!c->pipe_s[i]) CUDA_TRY(cudaStreamCreateWithFlags(&c->pipe_s[i], cudaStreamNonBlocking));
-    for (int b = 0; b < 2; ++b)
-      if (!c->pipe_ev[i][b]) CUDA_TRY(cudaEventCreateWithFlags(&c->pipe_ev[i][b], cudaEventDisableTiming));
+  if (!c->pipe_s[0]) {
+    int lo = 0, hi = 0;
+    CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    for (int i = 0; i < 5; ++i) // [3]: the deferred-frame launches, ahead of the main kernels' pending CTAs
+      CUDA_TRY(cudaStreamCreateWithPriority(&c->pipe_s[i], cudaStreamNonBlocking, i == 3 ? hi : lo));
   }
+  for (int i = 0; i < 4; ++i)
+    for (int b = 0; b < NBUF; ++b)
+      if (!c->pipe_ev[i][b]) CUDA_TRY(cudaEventCreateWithFlags(&c->pipe_ev[i][b], cudaEventDisableTiming));
   if (!c->pipe_counters) CUDA_TRY(cudaMalloc((void **)&c->pipe_counters, FWBF_NCOUNTERS * sizeof(int64_t)));
   CUDA_TRY(cudaMemsetAsync(c->pipe_counters, 0, FWBF_NCOUNTERS * sizeof(long long), c->pipe_s[1]));
   CUDA_TRY(cudaStreamSynchronize(c->pipe_s[1]));
-  // Three streams: H2D copies, decodes, D2H copies, ordered by events per
-  // buffer.  Decodes run one after another on their own stream, so a chunk's
-  // launches (the filtered kernel, then decode_kernel over its deferred
-  // frames) never queue behind the next chunk's persistent grid, while both
-  // copy directions overlap them.
-  cudaStream_t sin = c->pipe_s[0], sdec = c->pipe_s[1], sout = c->pipe_s[2];
+  // Five streams ordered by per-buffer events: H2D copies; the chunks' main
+  // decode kernels alternating between two streams, so chunk i+1's
+  // persistent grid is already queued when chunk i's CTAs run out of frames
+  // and takes over the SMs they leave (a chunk's last frames -- the ones that
+  // run all K_max iterations -- otherwise drain on a mostly idle GPU: 0.8 ms
+  // of a 15 ms chunk, measured); the second launch of a chunk (decode_kernel
+  // over the frames the filtered kernel deferred) on its own high-priority
+  // stream, where it waits for a slot instead of holding the next main kernel
+  // back; D2H copies.  A chunk's buffer is reused four chunks later.
+  cudaStream_t sin = c->pipe_s[0], sdef = c->pipe_s[3], sout = c->pipe_s[4];
   // chunk sizes ramp up geometrically (chunk/16, chunk/8, ... chunk) so the
   // first decode starts after a short copy instead of a full chunk's
   long long f0 = 0, cur = std::max<long long>(std::min<long long>(chunk, 4096), chunk / 16);
   for (long long ci = 0; f0 < batch; ++ci) {
-    const int s = (int)(ci & 1);
-    cudaStream_t st = sout;
+    const int s = (int)(ci % NBUF);
+    cudaStream_t sdec = c->pipe_s[1 + (ci & 1)];
     char *base = (char *)c->pipe_buf[s];
     float *dy = (float *)base;
     uint32_t *dz = (uint32_t *)(base + yb);
     int32_t *dit = (int32_t *)(base + yb + zb);
     uint8_t *dfl = (uint8_t *)(base + yb + zb + ib);
     const long long nb = std::min<long long>(cur, batch - f0);
-    if (ci >= 2) CUDA_TRY(cudaStreamWaitEvent(sin, c->pipe_ev[1][s], 0)); // chunk ci-2 decoded: y buffer free
+    if (ci >= NBUF) CUDA_TRY(cudaStreamWaitEvent(sin, c->pipe_ev[3][s], 0)); // chunk ci-4 decoded and copied out
     CUDA_TRY(cudaMemcpyAsync(dy, y_host + f0 * ld, (size_t)nb * ld * sizeof(float), cudaMemcpyHostToDevice, sin));
     CUDA_TRY(cudaEventRecord(c->pipe_ev[0][s], sin));
     CUDA_TRY(cudaStreamWaitEvent(sdec, c->pipe_ev[0][s], 0));
-    if (ci >= 2) CUDA_TRY(cudaStreamWaitEvent(sdec, c->pipe_ev[2][s], 0)); // chunk ci-2's outputs copied out
     fwbf_outputs o{};
     o.z_bits = z_host ? dz : nullptr;
     o.z_ld = zw;
     o.iterations = it_host ? dit : nullptr;
     o.flags = fl_host ? dfl : nullptr;
     o.counters = c->pipe_counters;
-    rc = launch_decode<float>(c, p, dy, nb, ld, &o, sdec);
+    rc = launch_decode<float>(c, p, dy, nb, ld, &o, sdec, nullptr, 0, sdef, c->pipe_ev[1][s]);
     if (rc) return rc;
+    // the chunk is decoded when everything on sdec and, after it, on sdef is done
     CUDA_TRY(cudaEventRecord(c->pipe_ev[1][s], sdec));
-    CUDA_TRY(cudaStreamWaitEvent(sout, c->pipe_ev[1][s], 0));
+    CUDA_TRY(cudaStreamWaitEvent(sdef, c->pipe_ev[1][s], 0));
+    CUDA_TRY(cudaEventRecord(c->pipe_ev[2][s], sdef));
+    CUDA_TRY(cudaStreamWaitEvent(sout, c->pipe_ev[2][s], 0));
     if (z_host) {
       if (z_ld == zw) {
-        CUDA_TRY(cudaMemcpyAsync(z_host + f0 * z_ld, dz, (size_t)nb * zw * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(z_host + f0 * z_ld, dz, (size_t)nb * zw * 4, cudaMemcpyDeviceToHost, sout));
       } else {
         CUDA_TRY(cudaMemcpy2DAsync(z_host + f0 * z_ld, (size_t)z_ld * 4, dz, (size_t)zw * 4, (size_t)zw * 4,
-                                   (size_t)nb, cudaMemcpyDeviceToHost, st));
+                                   (size_t)nb, cudaMemcpyDeviceToHost, sout));
       }
     }
-    if (it_host) CUDA_TRY(cudaMemcpyAsync(it_host + f0, dit, (size_t)nb * 4, cudaMemcpyDeviceToHost, st));
-    if (fl_host) CUDA_TRY(cudaMemcpyAsync(fl_host + f0, dfl, (size_t)nb, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaEventRecord(c->pipe_ev[2][s], sout));
+    if (it_host) CUDA_TRY(cudaMemcpyAsync(it_host + f0, dit, (size_t)nb * 4, cudaMemcpyDeviceToHost, sout));
+    if (fl_host) CUDA_TRY(cudaMemcpyAsync(fl_host + f0, dfl, (size_t)nb, cudaMemcpyDeviceToHost, sout));
+    CUDA_TRY(cudaEventRecord(c->pipe_ev[3][s], sout));
     f0 += nb;
     cur = std::min<long long>(chunk, 2 * cur);
   }
-  for (int i = 0; i < 3; ++i) CUDA_TRY(cudaStreamSynchronize(c->pipe_s[i]));
+  for (int i = 0; i < 5; ++i) CUDA_TRY(cudaStreamSynchronize(c->pipe_s[i]));
   if (cnt_host) {
     long long tmp[FWBF_NCOUNTERS];
     CUDA_TRY(cudaMemcpy(tmp, c->pipe_counters, sizeof tmp, cudaMemcpyDeviceToHost));
