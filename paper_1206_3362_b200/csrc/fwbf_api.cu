@@ -138,6 +138,8 @@ struct fwbf_code {
   cudaEvent_t noise_evt = nullptr; // last use of noise_buf (device-side ordering across streams)
   cudaStream_t noise_side = nullptr; // decode_awgn: odd chunks (noise + decode) on a second stream
   cudaEvent_t noise_fork = nullptr, noise_join = nullptr;
+  cudaStream_t noise_def = nullptr;           // decode_awgn: the chunks' deferred-frame launches (high priority)
+  cudaEvent_t noise_cev[3] = {}, noise_dev[3] = {}, noise_join2 = nullptr; // per scratch buffer: main kernel done, chunk done
   // explicit-code warp-per-frame plans, one per block length p
   std::mutex xplan_mu;
   std::list<XPlan> xplans; // stable addresses: launches hold a plan pointer outside the lock
@@ -354,6 +356,12 @@ extern "C" int fwbf_code_destroy(fwbf_code *c) {
   if (c->noise_side) cudaStreamDestroy(c->noise_side);
   if (c->noise_fork) cudaEventDestroy(c->noise_fork);
   if (c->noise_join) cudaEventDestroy(c->noise_join);
+  if (c->noise_def) cudaStreamDestroy(c->noise_def);
+  if (c->noise_join2) cudaEventDestroy(c->noise_join2);
+  for (int i = 0; i < 3; ++i) {
+    if (c->noise_cev[i]) cudaEventDestroy(c->noise_cev[i]);
+    if (c->noise_dev[i]) cudaEventDestroy(c->noise_dev[i]);
+  }
   for (XPlan &x : c->xplans) {
     cudaFree(x.d_tab);
     cudaFree(x.d_rtab);
@@ -1441,10 +1449,15 @@ static int decode_awgn_t(fwbf_code *c, const fwbf_params *p, uint64_t seed, int6
   const int n = c->n;
   const long long ld = o.y_out ? o.y_out_ld : ((n + 3) / 4 * 4);
   if (o.y_out && ld < n) return fail(FWBF_EINVAL, "y_out_ld too small");
-  // Scratch y: chunks alternate between two buffers and two streams (the
-  // caller's and a library side stream), so a chunk's noise generation and
-  // decode overlap the previous chunk's tail -- the frames that run to
-  // K_max keep a few SMs busy while the rest would idle.
+  // Scratch y: chunks rotate over three buffers and alternate between two
+  // streams (the caller's and a library side stream), so a chunk's noise
+  // generation and decode overlap the previous chunk's tail -- the frames that
+  // run to K_max keep a few SMs busy while the rest would idle.  A chunk's
+  // second launch (decode_kernel over the frames the filtered circulant kernel
+  // deferred) goes on a third, high-priority stream: behind the other
+  // stream's persistent grid it would find no slot until that grid drained and
+  // hold this stream's next chunk back.  Its buffer is
+  // free again three chunks later.
   long long chunk = std::min<long long>(count, o.y_out ? (1 << 18) : (1 << 17));
   const int bf = o.batch_word_err ? std::max(1, o.batch_frames) : 1;
   chunk = std::max<long long>(bf, chunk / bf * bf);
@@ -1460,7 +1473,7 @@ static int decode_awgn_t(fwbf_code *c, const fwbf_params *p, uint64_t seed, int6
     lock.lock();
     if (!c->noise_evt) CUDA_TRY(cudaEventCreateWithFlags(&c->noise_evt, cudaEventDisableTiming));
     else CUDA_TRY(cudaStreamWaitEvent(stream, c->noise_evt, 0));
-    const size_t need = (size_t)chunk * ld * sizeof(YT) * (two ? 2 : 1);
+    const size_t need = (size_t)chunk * ld * sizeof(YT) * (two ? 3 : 1);
     if (need > c->noise_bytes) {
       if (c->noise_buf) cudaFree(c->noise_buf);
       c->noise_buf = nullptr;
@@ -1483,13 +1496,25 @@ static int decode_awgn_t(fwbf_code *c, const fwbf_params *p, uint64_t seed, int6
     if (!c->noise_join) CUDA_TRY(cudaEventCreateWithFlags(&c->noise_join, cudaEventDisableTiming));
     CUDA_TRY(cudaEventRecord(c->noise_fork, stream)); // the side stream starts after the caller's prior work
     CUDA_TRY(cudaStreamWaitEvent(c->noise_side, c->noise_fork, 0));
+    if (!c->noise_def) {
+      int lo = 0, hi = 0;
+      CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CUDA_TRY(cudaStreamCreateWithPriority(&c->noise_def, cudaStreamNonBlocking, hi));
+    }
+    if (!c->noise_join2) CUDA_TRY(cudaEventCreateWithFlags(&c->noise_join2, cudaEventDisableTiming));
+    for (int i = 0; i < 3; ++i) {
+      if (!c->noise_cev[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->noise_cev[i], cudaEventDisableTiming));
+      if (!c->noise_dev[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->noise_dev[i], cudaEventDisableTiming));
+    }
   }
   const cudaStream_t caller = stream;
   long long ci = 0;
   for (long long s = 0; s < count; s += chunk, ++ci) {
     const long long nb = std::min(chunk, count - s);
-    stream = (two && (ci & 1)) ? c->noise_side : caller; // (chunk ci - 2 used this buffer on this stream)
-    YT *yb = o.y_out ? (YT *)o.y_out + s * ld : scratch + (two ? (ci & 1) * chunk * ld : 0);
+    stream = (two && (ci & 1)) ? c->noise_side : caller;
+    const int b3 = (int)(ci % 3);
+    if (two && ci >= 3) CUDA_TRY(cudaStreamWaitEvent(stream, c->noise_dev[b3], 0)); // chunk ci - 3 is done with the buffer
+    YT *yb = o.y_out ? (YT *)o.y_out + s * ld : scratch + (two ? b3 * chunk * ld : 0);
     static const bool cta_gen = getenv("FWBF_NOISE_CTA") != nullptr; // the CTA-per-frame generator
     if (cta_gen) {
       const int grid = (int)std::min<long long>(nb, (long long)c->sm_count * 32);
@@ -1513,13 +1538,24 @@ static int decode_awgn_t(fwbf_code *c, const fwbf_params *p, uint64_t seed, int6
     }
     if (o.batch_word_err) oc.batch_word_err = o.batch_word_err + s / bf;
     (void)maxf;
-    rc = launch_decode<YT>(c, p, yb, nb, ld, &oc, stream);
-    if (rc) return rc;
+    if (two) {
+      rc = launch_decode<YT>(c, p, yb, nb, ld, &oc, stream, nullptr, 0, c->noise_def, c->noise_cev[b3]);
+      if (rc) return rc;
+      // the chunk is done when everything on its stream and, after it, on the deferred stream is
+      CUDA_TRY(cudaEventRecord(c->noise_cev[b3], stream));
+      CUDA_TRY(cudaStreamWaitEvent(c->noise_def, c->noise_cev[b3], 0));
+      CUDA_TRY(cudaEventRecord(c->noise_dev[b3], c->noise_def));
+    } else {
+      rc = launch_decode<YT>(c, p, yb, nb, ld, &oc, stream);
+      if (rc) return rc;
+    }
   }
   stream = caller;
-  if (two) { // join: the caller's stream waits for the side stream's chunks
+  if (two) { // join: the caller's stream waits for the side and deferred streams' chunks
     CUDA_TRY(cudaEventRecord(c->noise_join, c->noise_side));
     CUDA_TRY(cudaStreamWaitEvent(stream, c->noise_join, 0));
+    CUDA_TRY(cudaEventRecord(c->noise_join2, c->noise_def));
+    CUDA_TRY(cudaStreamWaitEvent(stream, c->noise_join2, 0));
   }
   if (!o.y_out) CUDA_TRY(cudaEventRecord(c->noise_evt, stream));
   return FWBF_OK;
