@@ -1,6 +1,8 @@
 """fwbf_decode_host_f32 (the e2e path: host buffers, chunked copies pipelined
-with decode on two streams, chunk sizes ramping up) gives exactly the
-device-buffer decode's per-frame results and counters."""
+with decode -- consecutive chunks on two alternating decode streams, the
+deferred-frame launches on their own stream, four chunk buffers, chunk sizes
+ramping up) gives exactly the device-buffer decode's per-frame results and
+counters."""
 import ctypes as C
 
 import numpy as np
@@ -15,7 +17,9 @@ from oracle import wbf_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("batch,chunk,ld_pad,z_pad", [(20000, 8192, 1, 0), (5000, 0, 0, 3), (3, 1, 5, 1)])
+@pytest.mark.parametrize("batch,chunk,ld_pad,z_pad", [(20000, 8192, 1, 0), (5000, 0, 0, 3), (3, 1, 5, 1),
+                                                       (9000, 512, 1, 0),     # 18 chunks: every buffer reused 4 times
+                                                       (3000, 128, 0, 2)])    # many short chunks
 def test_host_pipeline_matches_device_decode(cuda_device, batch, chunk, ld_pad, z_pad):
     h = build_code("eg5")
     n = h.n_cols
@@ -24,6 +28,10 @@ def test_host_pipeline_matches_device_decode(cuda_device, batch, chunk, ld_pad, 
     rng = np.random.default_rng(batch)
     y = np.zeros((batch, ld), np.float32)
     y[:, :n] = 1.0 + sigma * rng.standard_normal((batch, n))
+    if batch >= 3000:                       # frames the filtered kernel defers, spread over the chunks
+        y[::97, :n] = 0.0
+        y[5::211, 7] = np.inf
+        y[9::173, 100] = 1e-30
     cfg = DecoderConfig(block_len_p=31, k_max=100)
     ref = decode_batch(h, y[:, :n].copy(), cfg, "fwbf")
     zw = (n + 31) // 32
