@@ -133,9 +133,10 @@ def test_decode_awgn_concurrent_streams_share_scratch(cuda_device):
 
 
 def test_decode_awgn_two_stream_chunks_equal_single_chunks(cuda_device):
-    """Batches larger than one chunk alternate two scratch buffers and two
-    streams; every frame's result and the accumulated counters equal those of
-    single-chunk calls over the same frame ranges."""
+    """Batches larger than one chunk rotate three scratch buffers over two
+    streams (deferred-frame launches on a third); with six chunks every buffer
+    is reused.  Every frame's result and the accumulated counters equal those
+    of single-chunk calls over the same frame ranges."""
     import torch
     from paper_1206_3362_b200 import DecoderConfig
     from paper_1206_3362_b200.decoders import decode_awgn
@@ -143,9 +144,8 @@ def test_decode_awgn_two_stream_chunks_equal_single_chunks(cuda_device):
     h = build_code("eg5")
     sigma = O.ebn0_to_sigma(4.5, code_rate("eg5"))
     cfg = DecoderConfig(block_len_p=31, k_max=60)
-    whole = decode_awgn(h, cfg, "fwbf", 7, 1000, 300000, sigma, noise="f32")
-    parts = [decode_awgn(h, cfg, "fwbf", 7, 1000 + s, n, sigma, noise="f32")
-             for s, n in ((0, 100000), (100000, 100000), (200000, 100000))]
+    whole = decode_awgn(h, cfg, "fwbf", 7, 1000, 700000, sigma, noise="f32")
+    parts = [decode_awgn(h, cfg, "fwbf", 7, 1000 + s, 100000, sigma, noise="f32") for s in range(0, 700000, 100000)]
     torch.cuda.synchronize()
     for name in ("iterations", "flags", "flips_total", "bit_errors", "z_bits"):
         a = getattr(whole, name).cpu().numpy()
